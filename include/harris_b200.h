@@ -1,0 +1,145 @@
+/*
+ * harris_b200.h — C-ABI of the fused B200 Harris corner detector.
+ *
+ * Drop-in for the Harris path of arXiv 2212.12035 (the Shine thesis; reference
+ * at /root/reference).  The reference has no compiled Harris entry point
+ * (SURVEY.md §0.1); the boundary is defined by the thesis itself:
+ *
+ *   - Rise type   harris : 3.(n+4).(m+4).f32 -> n.m.f32
+ *     planar channel-major RGB in, valid-region output 4 smaller per dimension,
+ *     no padding.
+ *   - generated kernel   harris(output, n0, n1, x0, t1, t2, t3) PAPER.md:4582-4583
+ *     "output parameter followed by input parameters".
+ *     Fusion removes the caller-provided scratch buffers t1..t3.
+ *   - host code convention  <name>_init / <name>_run / <name>_destroy over the
+ *     LRA runtime; caller owns all buffers.
+ *
+ * Conventions
+ *   - Sizes n, m are OUTPUT rows / columns; the input is (n+4) x (m+4) per channel.
+ *   - All pointers passed to harris_run* are DEVICE pointers (except
+ *     harris_run_host); calls are asynchronous on `cuda_stream` (a cudaStream_t,
+ *     NULL = legacy default stream).  The library never allocates in harris_run*.
+ *   - Return 0 on success, a negative HARRIS_ERR_* code otherwise; nothing throws
+ *     across this boundary.  harris_strerror() names the code.
+ *   - A ctx is immutable after harris_init except for the host-staging buffers of
+ *     harris_run_host, so harris_run* may be called concurrently on different
+ *     streams; harris_run_host must not be called concurrently on one ctx.
+ *   - Element type is f32 throughout; kappa is the coarsity constant (0.04 in the
+ *     thesis).
+ */
+#ifndef HARRIS_B200_H
+#define HARRIS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HARRIS_B200_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define HARRIS_API __attribute__((visibility("default")))
+#else
+#define HARRIS_API
+#endif
+
+#define HARRIS_OK                       0
+#define HARRIS_ERR_INVALID_ARGUMENT   (-1)  /* null pointer, bad pitch/stride, batch < 1 */
+#define HARRIS_ERR_SIZE               (-2)  /* n < 1 or m < 1 (input smaller than 5x5) or too large */
+#define HARRIS_ERR_ALIGNMENT          (-3)  /* explicit TMA request on unaligned data */
+#define HARRIS_ERR_CUDA               (-4)  /* CUDA runtime error (see harris_last_cuda_error) */
+#define HARRIS_ERR_NO_DEVICE          (-5)  /* no CUDA device / bad device ordinal */
+#define HARRIS_ERR_TMA                (-6)  /* cuTensorMapEncodeTiled failed */
+#define HARRIS_ERR_OUT_OF_MEMORY      (-7)
+#define HARRIS_ERR_UNSUPPORTED_DEVICE (-8)  /* not an sm_100 device */
+
+/* flags for harris_run_strided / harris_run_host */
+#define HARRIS_FLAG_EXACT_ORDER   0x1u  /* SURVEY.md App. B op order, no FMA: bit-identical
+                                           to oracle/harris_oracle.c oracle_harris_f32 */
+#define HARRIS_FLAG_FORCE_GENERIC 0x2u  /* use the generic (non-TMA) kernel */
+#define HARRIS_FLAG_FORCE_TMA     0x4u  /* fail with HARRIS_ERR_ALIGNMENT instead of falling
+                                           back to the generic GPU kernel */
+
+/* which kernel the last harris_run* on a ctx launched */
+#define HARRIS_PATH_NONE    0
+#define HARRIS_PATH_TMA     1  /* K1: TMA-staged warp-strip kernel (W%4==0, aligned) */
+#define HARRIS_PATH_GENERIC 2  /* K0: shared-memory tile kernel (any W, any pitch)   */
+
+typedef struct harris_ctx harris_ctx;
+
+/* ~ <name>_init: binds a device, caches its properties,
+ * configures the kernels.  cuda_device < 0 means the current device. */
+HARRIS_API int harris_init(harris_ctx** ctx, int cuda_device);
+
+/* ~ <name>_destroy. NULL is accepted. */
+HARRIS_API void harris_destroy(harris_ctx* ctx);
+
+/* ~ <name>_run / kernel harris(output, n0, n1, x0, ...)
+ * (PAPER.md:4582-4583).  out: n x m, row pitch out_pitch >= m elements
+ * (out_pitch = m+4 reproduces the thesis kernel's output layout);
+ * rgb: contiguous planar 3 x (n+4) x (m+4). */
+HARRIS_API int harris_run(harris_ctx* ctx, float* out, int64_t out_pitch, int64_t n, int64_t m,
+               const float* rgb, float kappa, void* cuda_stream);
+
+/* batch contiguous images: rgb batch x 3 x (n+4) x (m+4), out batch x n x m.
+ * One launch for the whole batch (image x strip grid). */
+HARRIS_API int harris_run_batched(harris_ctx* ctx, float* out, int64_t n, int64_t m,
+                       const float* rgb, int64_t batch, float kappa, void* cuda_stream);
+
+/* fully strided form every other entry point reduces to.
+ * input  element (b, c, y, x) at rgb[b*in_image_stride + c*in_chan_stride + y*in_pitch + x]
+ * output element (b, y, x)    at out[b*out_image_stride + y*out_pitch + x]
+ * A row band of a larger image is a sub-view: rgb + r0*in_pitch with the parent's
+ * in_chan_stride (this is how the multi-GPU driver shards with a 4-row halo). */
+HARRIS_API int harris_run_strided(harris_ctx* ctx, float* out, int64_t out_pitch, int64_t out_image_stride,
+                       int64_t n, int64_t m, const float* rgb, int64_t in_pitch,
+                       int64_t in_chan_stride, int64_t in_image_stride, int64_t batch,
+                       float kappa, uint32_t flags, void* cuda_stream);
+
+/* HOST buffers (pinned for full speed; pageable works).  Row bands (batch == 1) or
+ * image groups are pipelined H2D -> kernel -> D2H over three streams; returns when
+ * the output is in out_host.  rgb_host: batch x 3 x (n+4) x (m+4) contiguous;
+ * out_host: batch x n x out_pitch. */
+HARRIS_API int harris_run_host(harris_ctx* ctx, float* out_host, int64_t out_pitch, int64_t n, int64_t m,
+                    const float* rgb_host, int64_t batch, float kappa, uint32_t flags);
+
+/* Device synthetic-image generator used by the bench (bit-identical to
+ * oracle_synth_fill): dst (p, y, x) at dst[p*dst_plane_stride + y*dst_pitch + x] =
+ * value of global plane plane0+p, row row0+y of a planes x H_global x W stack.
+ * dist 0: U[0,1) (24-bit), dist 1: u8/255. */
+HARRIS_API int harris_synth_fill(float* dst, int64_t planes, int64_t rows, int64_t W, int64_t dst_pitch,
+                      int64_t dst_plane_stride, int64_t H_global, int64_t row0, int64_t plane0,
+                      uint64_t seed, int dist, void* cuda_stream);
+
+/* Launch geometry the TMA kernel would use (for tests / bench reporting). */
+typedef struct harris_plan_info {
+    int32_t path;           /* HARRIS_PATH_* that harris_run_strided would take */
+    int32_t warps_per_cta;
+    int32_t stages;
+    int32_t rows_per_stage;
+    int64_t band_rows;      /* output rows per tile */
+    int64_t bands;          /* tiles per image column */
+    int64_t col_segments;   /* 128-column warp strips per image */
+    int64_t tiles;          /* batch * bands * col_segments */
+    int64_t grid_ctas;
+    int64_t smem_bytes;     /* dynamic shared memory per CTA */
+} harris_plan_info;
+
+HARRIS_API int harris_plan(harris_ctx* ctx, int64_t n, int64_t m, int64_t batch, const float* rgb,
+                int64_t in_pitch, int64_t in_chan_stride, int64_t in_image_stride,
+                const float* out, int64_t out_pitch, int64_t out_image_stride,
+                uint32_t flags, harris_plan_info* info);
+
+HARRIS_API int harris_last_path(const harris_ctx* ctx);
+HARRIS_API int harris_device(const harris_ctx* ctx);
+HARRIS_API int harris_num_sms(const harris_ctx* ctx);
+HARRIS_API const char* harris_strerror(int code);
+HARRIS_API const char* harris_last_cuda_error(const harris_ctx* ctx);
+HARRIS_API int harris_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HARRIS_B200_H */

@@ -1,0 +1,110 @@
+"""ctypes binding of ``oracle/liboracle_harris.so`` — TEST INFRASTRUCTURE ONLY.
+
+The library is the C restatement in ``harris_oracle.c`` (f32 Appendix-B order,
+f64 sges order).  ``build()`` in ``__graft_entry__`` compiles it with
+``make -C oracle``; the built ``.so`` travels to the GPU box with the snapshot.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liboracle_harris.so")
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(LIB_PATH) or (
+            os.path.getmtime(LIB_PATH) < os.path.getmtime(os.path.join(_HERE, "harris_oracle.c"))):
+        subprocess.run(["make", "-C", _HERE, "-B" if force else "all"], check=True,
+                       stdout=subprocess.DEVNULL)
+    return LIB_PATH
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            build()
+        L = ctypes.CDLL(LIB_PATH)
+        i64, fp, dp, vp = ctypes.c_int64, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_double), ctypes.c_void_p
+        L.oracle_harris_f32.argtypes = [vp, i64, i64, i64, vp, i64, i64, ctypes.c_float, ctypes.c_int]
+        L.oracle_harris_f32.restype = ctypes.c_int
+        L.oracle_harris_f64.argtypes = [vp, i64, i64, i64, vp, i64, i64, ctypes.c_double, ctypes.c_int]
+        L.oracle_harris_f64.restype = ctypes.c_int
+        L.oracle_harris_f32_batched.argtypes = [vp, i64, i64, vp, i64, ctypes.c_float, ctypes.c_int]
+        L.oracle_harris_f32_batched.restype = ctypes.c_int
+        L.oracle_synth_fill.argtypes = [vp, i64, i64, i64, i64, i64, i64, i64, i64, ctypes.c_uint64, ctypes.c_int]
+        L.oracle_synth_fill.restype = None
+        L.oracle_max_threads.argtypes = []
+        L.oracle_max_threads.restype = ctypes.c_int
+        del fp, dp
+        _lib = L
+    return _lib
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def _check_rgb(rgb: np.ndarray) -> tuple[int, int]:
+    if rgb.dtype != np.float32 or rgb.ndim != 3 or rgb.shape[0] != 3:
+        raise ValueError("rgb must be float32 of shape (3, H, W)")
+    H, W = rgb.shape[1:]
+    if H < 5 or W < 5:
+        raise ValueError("harris needs H >= 5 and W >= 5")
+    return H, W
+
+
+def harris_f32(rgb: np.ndarray, kappa: float = 0.04, nthreads: int = 0) -> np.ndarray:
+    """f32 Appendix-B restatement. ``rgb``: (3, H, W) float32 -> (H-4, W-4) f32."""
+    rgb = np.ascontiguousarray(rgb)
+    H, W = _check_rgb(rgb)
+    out = np.empty((H - 4, W - 4), dtype=np.float32)
+    rc = lib().oracle_harris_f32(_ptr(out), W - 4, H - 4, W - 4, _ptr(rgb), W, H * W, kappa, nthreads)
+    if rc:
+        raise RuntimeError(f"oracle_harris_f32 failed ({rc})")
+    return out
+
+
+def harris_f64(rgb: np.ndarray, kappa: float = 0.04, nthreads: int = 0) -> np.ndarray:
+    """f64 restatement in sges evaluation order, from the f32 input."""
+    rgb = np.ascontiguousarray(rgb)
+    H, W = _check_rgb(rgb)
+    out = np.empty((H - 4, W - 4), dtype=np.float64)
+    rc = lib().oracle_harris_f64(_ptr(out), W - 4, H - 4, W - 4, _ptr(rgb), W, H * W, kappa, nthreads)
+    if rc:
+        raise RuntimeError(f"oracle_harris_f64 failed ({rc})")
+    return out
+
+
+def harris_f32_batched(rgb: np.ndarray, kappa: float = 0.04, nthreads: int = 0,
+                       out: np.ndarray | None = None) -> np.ndarray:
+    """(B, 3, H, W) float32 -> (B, H-4, W-4) float32."""
+    if rgb.dtype != np.float32 or rgb.ndim != 4 or rgb.shape[1] != 3 or not rgb.flags.c_contiguous:
+        raise ValueError("rgb must be C-contiguous float32 of shape (B, 3, H, W)")
+    B, _, H, W = rgb.shape
+    if out is None:
+        out = np.empty((B, H - 4, W - 4), dtype=np.float32)
+    rc = lib().oracle_harris_f32_batched(_ptr(out), H - 4, W - 4, _ptr(rgb), B, kappa, nthreads)
+    if rc:
+        raise RuntimeError(f"oracle_harris_f32_batched failed ({rc})")
+    return out
+
+
+def synth(planes: int, H: int, W: int, seed: int, dist: int = 0, row0: int = 0,
+          rows: int | None = None, plane0: int = 0, H_global: int | None = None) -> np.ndarray:
+    rows = H if rows is None else rows
+    Hg = H if H_global is None else H_global
+    out = np.empty((planes, rows, W), dtype=np.float32)
+    lib().oracle_synth_fill(_ptr(out), planes, rows, W, W, rows * W, Hg, row0, plane0, seed, dist)
+    return out
+
+
+def max_threads() -> int:
+    return int(lib().oracle_max_threads())

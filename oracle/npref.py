@@ -1,0 +1,52 @@
+"""Pure numpy restatement of the Harris pipeline — TEST INFRASTRUCTURE ONLY.
+
+Direct transcription of the Halide algorithm the thesis takes as ground truth
+ in the op order of SURVEY.md Appendix B, vectorised over
+whole planes.  ``harris_np(rgb, dtype=np.float32)`` follows the f32 contract
+(each product / sum rounded to f32, numpy never fuses); ``dtype=np.float64``
+follows the sges evaluation order.  Used to cross-check the C oracle and to
+evaluate known-answer images.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def harris_np(rgb: np.ndarray, kappa: float = 0.04, dtype=np.float32) -> np.ndarray:
+    rgb = np.asarray(rgb, dtype=np.float32)
+    if rgb.ndim != 3 or rgb.shape[0] != 3 or rgb.shape[1] < 5 or rgb.shape[2] < 5:
+        raise ValueError("rgb must be (3, H>=5, W>=5)")
+    f = np.dtype(dtype).type
+    R, G, B = (rgb[c].astype(dtype) for c in range(3))
+    if dtype == np.float32:
+        wg = (f(0.299), f(0.587), f(0.114))
+        a, b = f(0.083333336), f(0.16666667)
+    else:
+        wg = (0.299, 0.587, 0.114)
+        a, b = 1.0 / 12.0, 2.0 / 12.0
+    z = f(0.0)
+    g = ((z + wg[0] * R) + wg[1] * G) + wg[2] * B
+    H, W = g.shape
+    sx = ((-a, z, a), (-b, z, b), (-a, z, a))
+    sy = ((-a, -b, -a), (z, z, z), (a, b, a))
+    Ix = np.zeros((H - 2, W - 2), dtype=dtype)
+    Iy = np.zeros((H - 2, W - 2), dtype=dtype)
+    for i in range(3):
+        for j in range(3):
+            win = g[i:i + H - 2, j:j + W - 2]
+            Ix = Ix + sx[i][j] * win
+            Iy = Iy + sy[i][j] * win
+    Ixx, Ixy, Iyy = Ix * Ix, Ix * Iy, Iy * Iy
+    n, m = H - 4, W - 4
+    Sxx = np.zeros((n, m), dtype=dtype)
+    Sxy = np.zeros((n, m), dtype=dtype)
+    Syy = np.zeros((n, m), dtype=dtype)
+    for i in range(3):
+        for j in range(3):
+            Sxx = Sxx + Ixx[i:i + n, j:j + m]
+            Sxy = Sxy + Ixy[i:i + n, j:j + m]
+            Syy = Syy + Iyy[i:i + n, j:j + m]
+    k = f(kappa)
+    det = Sxx * Syy - Sxy * Sxy
+    tr = Sxx + Syy
+    return (det - (k * tr) * tr).astype(dtype)

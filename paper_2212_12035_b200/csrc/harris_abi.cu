@@ -1,0 +1,461 @@
+// harris_abi.cu — the C-ABI (include/harris_b200.h): device binding, argument
+// validation, the tile planner, TMA descriptor encoding, kernel dispatch and the
+// pipelined host-buffer path.  Nothing here throws; every entry point returns a
+// HARRIS_* code.
+//
+// Reference boundary being replaced: the thesis host-code convention
+// <name>_init / <name>_run / <name>_destroy over the LRA runtime
+// and the generated kernel
+// harris(output, n0, n1, x0, t1, t2, t3).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+
+#include "../../include/harris_b200.h"
+#include "harris_common.cuh"
+#include "harris_internal.h"
+
+using namespace harris;
+
+struct harris_ctx {
+    int device = 0;
+    int num_sms = 0;
+    int cc_major = 0, cc_minor = 0;
+    int tma_cfg = 0;
+    int occ[kNumTmaConfigs] = {0};
+    PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    int last_path = HARRIS_PATH_NONE;
+    char last_err[256] = {0};
+    // host-buffer pipeline (harris_run_host)
+    static constexpr int kSlots = 3;
+    cudaStream_t streams[kSlots] = {nullptr, nullptr, nullptr};
+    float* d_in[kSlots] = {nullptr, nullptr, nullptr};
+    float* d_out[kSlots] = {nullptr, nullptr, nullptr};
+    size_t cap_in = 0, cap_out = 0;
+};
+
+namespace {
+
+// Makes ctx->device current for the duration of a call, restores the caller's.
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+int cuda_fail(harris_ctx* ctx, cudaError_t e, const char* where) {
+    if (ctx) std::snprintf(ctx->last_err, sizeof(ctx->last_err), "%s: %s", where, cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? HARRIS_ERR_OUT_OF_MEMORY : HARRIS_ERR_CUDA;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+struct Call {
+    Geom g;
+    uint32_t flags;
+};
+
+int validate(const Call& c) {
+    const Geom& g = c.g;
+    if (!g.rgb || !g.out) return HARRIS_ERR_INVALID_ARGUMENT;
+    if (g.n < 1 || g.m < 1) return HARRIS_ERR_SIZE;  // input must be at least 5 x 5
+    if (g.n + 4 > INT32_MAX || g.m + 4 > INT32_MAX) return HARRIS_ERR_SIZE;
+    if (g.batch < 1) return HARRIS_ERR_INVALID_ARGUMENT;
+    if (g.in_pitch < g.m + 4 || g.out_pitch < g.m) return HARRIS_ERR_INVALID_ARGUMENT;
+    if (g.in_chan_stride < (g.n + 4) * g.in_pitch) return HARRIS_ERR_INVALID_ARGUMENT;
+    if (g.batch > 1) {
+        if (g.in_image_stride < 3 * g.in_chan_stride) return HARRIS_ERR_INVALID_ARGUMENT;
+        if (g.out_image_stride < g.n * g.out_pitch) return HARRIS_ERR_INVALID_ARGUMENT;
+    }
+    return HARRIS_OK;
+}
+
+bool tma_eligible(const Call& c) {
+    const Geom& g = c.g;
+    if (!aligned16(g.rgb) || !aligned16(g.out)) return false;
+    if ((g.in_pitch | g.in_chan_stride | g.out_pitch) & 3) return false;
+    if (g.batch > 1 && ((g.in_image_stride | g.out_image_stride) & 3)) return false;
+    const int64_t kMaxStrideBytes = (int64_t(1) << 40) - 16;
+    if (g.in_chan_stride * 4 > kMaxStrideBytes) return false;
+    if (g.batch > 1 && g.in_image_stride * 4 > kMaxStrideBytes) return false;
+    if (g.batch > INT32_MAX) return false;
+    return true;
+}
+
+// Pick the band height that minimises (waves x rows-per-tile) for a persistent
+// grid of `gw` warps: tiles = batch x bands x col_segments.
+void plan_tiles(int64_t n, int64_t m, int64_t batch, int64_t gw, int rows_per_stage, TileGeom& tg) {
+    const int64_t colsegs = (m + kWarpCols - 1) / kWarpCols;
+    const int64_t kTileOverheadRows = 6;  // pipeline/tile switch cost in row-equivalents
+    const int64_t max_bands = std::max<int64_t>(1, std::min<int64_t>(n, 1 + n / 8));
+    int64_t best_cost = INT64_MAX, best_rows = n, best_bands = 1;
+    for (int64_t nb = 1; nb <= max_bands; ++nb) {
+        const int64_t rows = (n + nb - 1) / nb;
+        const int64_t bands = (n + rows - 1) / rows;
+        if (bands != nb) continue;  // same split as a smaller nb
+        const int64_t tiles = batch * colsegs * bands;
+        const int64_t waves = (tiles + gw - 1) / gw;
+        const int64_t rows_in = ((rows + 4 + rows_per_stage - 1) / rows_per_stage) * rows_per_stage;
+        const int64_t cost = waves * (rows_in + kTileOverheadRows);
+        if (cost < best_cost) {
+            best_cost = cost;
+            best_rows = rows;
+            best_bands = bands;
+        }
+    }
+    tg.n = int32_t(n);
+    tg.m = int32_t(m);
+    tg.band_rows = int32_t(best_rows);
+    tg.bands = int32_t(best_bands);
+    tg.colsegs = int32_t(colsegs);
+    tg.tiles = batch * colsegs * best_bands;
+}
+
+int choose_path(const Call& c) {
+    if (c.flags & HARRIS_FLAG_FORCE_GENERIC) return HARRIS_PATH_GENERIC;
+    return tma_eligible(c) ? HARRIS_PATH_TMA : HARRIS_PATH_GENERIC;
+}
+
+void plan_launch(const harris_ctx* ctx, const Call& c, TileGeom& tg, int64_t& grid) {
+    const TmaConfig& cfg = kTmaConfigs[ctx->tma_cfg];
+    const int occ = std::max(1, ctx->occ[ctx->tma_cfg]);
+    const int64_t resident_ctas = int64_t(ctx->num_sms) * occ;
+    plan_tiles(c.g.n, c.g.m, c.g.batch, resident_ctas * cfg.warps, cfg.rows, tg);
+    grid = std::min<int64_t>((tg.tiles + cfg.warps - 1) / cfg.warps, resident_ctas);
+    tg.out = c.g.out;
+    tg.out_pitch = c.g.out_pitch;
+    tg.out_image_stride = c.g.out_image_stride;
+    tg.kappa = c.g.kappa;
+    tg.pad_ = 0;
+}
+
+int encode_tmap(harris_ctx* ctx, const Call& c, CUtensorMap* tmap) {
+    const Geom& g = c.g;
+    const TmaConfig& cfg = kTmaConfigs[ctx->tma_cfg];
+    cuuint64_t dims[4] = {cuuint64_t(g.m + 4), cuuint64_t(g.n + 4), 3, cuuint64_t(g.batch)};
+    const int64_t img_stride = g.batch > 1 ? g.in_image_stride : 3 * g.in_chan_stride;
+    cuuint64_t strides[3] = {cuuint64_t(g.in_pitch) * 4, cuuint64_t(g.in_chan_stride) * 4,
+                             cuuint64_t(img_stride) * 4};
+    cuuint32_t box[4] = {cuuint32_t(kBoxCols), cuuint32_t(cfg.rows), 3, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = ctx->encode(tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(g.rgb), dims, strides,
+                             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        std::snprintf(ctx->last_err, sizeof(ctx->last_err), "cuTensorMapEncodeTiled failed (CUresult %d)", int(r));
+        return HARRIS_ERR_TMA;
+    }
+    return HARRIS_OK;
+}
+
+int run(harris_ctx* ctx, const Call& c, cudaStream_t stream) {
+    if (!ctx) return HARRIS_ERR_INVALID_ARGUMENT;
+    int rc = validate(c);
+    if (rc) return rc;
+    const bool exact = (c.flags & HARRIS_FLAG_EXACT_ORDER) != 0;
+    int path = choose_path(c);
+    if (path != HARRIS_PATH_TMA && (c.flags & HARRIS_FLAG_FORCE_TMA)) return HARRIS_ERR_ALIGNMENT;
+    DeviceGuard guard(ctx->device);
+    if (!guard.ok) return cuda_fail(ctx, cudaGetLastError(), "cudaSetDevice");
+    cudaError_t e;
+    if (path == HARRIS_PATH_TMA) {
+        CUtensorMap tmap;
+        rc = encode_tmap(ctx, c, &tmap);
+        if (rc) return rc;
+        TileGeom tg;
+        int64_t grid = 0;
+        plan_launch(ctx, c, tg, grid);
+        e = launch_tma(ctx->tma_cfg, exact, tmap, tg, grid, stream);
+    } else {
+        e = launch_generic(exact, c.g, stream);
+    }
+    if (e != cudaSuccess) return cuda_fail(ctx, e, path == HARRIS_PATH_TMA ? "launch tma" : "launch generic");
+    ctx->last_path = path;
+    return HARRIS_OK;
+}
+
+Call make_call(float* out, int64_t out_pitch, int64_t out_image_stride, int64_t n, int64_t m, const float* rgb,
+               int64_t in_pitch, int64_t in_chan_stride, int64_t in_image_stride, int64_t batch, float kappa,
+               uint32_t flags) {
+    Call c;
+    c.g.n = n;
+    c.g.m = m;
+    c.g.batch = batch;
+    c.g.rgb = rgb;
+    c.g.in_pitch = in_pitch;
+    c.g.in_chan_stride = in_chan_stride;
+    c.g.in_image_stride = in_image_stride;
+    c.g.out = out;
+    c.g.out_pitch = out_pitch;
+    c.g.out_image_stride = out_image_stride;
+    c.g.kappa = kappa;
+    c.flags = flags;
+    return c;
+}
+
+}  // namespace
+
+extern "C" {
+
+int harris_abi_version(void) { return HARRIS_B200_ABI_VERSION; }
+
+const char* harris_strerror(int code) {
+    switch (code) {
+        case HARRIS_OK: return "ok";
+        case HARRIS_ERR_INVALID_ARGUMENT: return "invalid argument (null pointer, pitch, stride or batch)";
+        case HARRIS_ERR_SIZE: return "invalid size (input must be at least 5x5: n >= 1, m >= 1)";
+        case HARRIS_ERR_ALIGNMENT: return "TMA path requested but data is not 16-byte aligned";
+        case HARRIS_ERR_CUDA: return "CUDA runtime error";
+        case HARRIS_ERR_NO_DEVICE: return "no CUDA device";
+        case HARRIS_ERR_TMA: return "TMA descriptor encoding failed";
+        case HARRIS_ERR_OUT_OF_MEMORY: return "out of device memory";
+        case HARRIS_ERR_UNSUPPORTED_DEVICE: return "unsupported device (needs sm_100 / B200)";
+        default: return "unknown error";
+    }
+}
+
+int harris_init(harris_ctx** out_ctx, int cuda_device) {
+    if (!out_ctx) return HARRIS_ERR_INVALID_ARGUMENT;
+    *out_ctx = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return HARRIS_ERR_NO_DEVICE;
+    }
+    int dev = cuda_device;
+    if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) return HARRIS_ERR_NO_DEVICE;
+    if (dev >= count) return HARRIS_ERR_NO_DEVICE;
+    harris_ctx* ctx = new (std::nothrow) harris_ctx();
+    if (!ctx) return HARRIS_ERR_OUT_OF_MEMORY;
+    ctx->device = dev;
+    DeviceGuard guard(dev);
+    cudaDeviceProp prop;
+    if (!guard.ok || cudaGetDeviceProperties(&prop, dev) != cudaSuccess) {
+        delete ctx;
+        return HARRIS_ERR_NO_DEVICE;
+    }
+    ctx->num_sms = prop.multiProcessorCount;
+    ctx->cc_major = prop.major;
+    ctx->cc_minor = prop.minor;
+    if (prop.major != 10) {  // binary carries sm_100a SASS only
+        delete ctx;
+        return HARRIS_ERR_UNSUPPORTED_DEVICE;
+    }
+    const char* env = std::getenv("HARRIS_TMA_CONFIG");
+    if (env) {
+        int v = std::atoi(env);
+        if (v >= 0 && v < kNumTmaConfigs) ctx->tma_cfg = v;
+    }
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) {
+        int rc = cuda_fail(ctx, e, "cudaGetDriverEntryPoint(cuTensorMapEncodeTiled)");
+        delete ctx;
+        return rc;
+    }
+    ctx->encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    for (int k = 0; k < kNumTmaConfigs; ++k) {
+        e = tma_configure(k);
+        if (e == cudaSuccess) e = tma_occupancy(k, &ctx->occ[k]);
+        if (e != cudaSuccess) {
+            int rc = cuda_fail(ctx, e, "configure tma kernel");
+            delete ctx;
+            return rc;
+        }
+    }
+    *out_ctx = ctx;
+    return HARRIS_OK;
+}
+
+void harris_destroy(harris_ctx* ctx) {
+    if (!ctx) return;
+    {
+        DeviceGuard guard(ctx->device);
+        for (int k = 0; k < harris_ctx::kSlots; ++k) {
+            if (ctx->streams[k]) {
+                cudaStreamSynchronize(ctx->streams[k]);
+                cudaStreamDestroy(ctx->streams[k]);
+            }
+            cudaFree(ctx->d_in[k]);
+            cudaFree(ctx->d_out[k]);
+        }
+    }
+    delete ctx;
+}
+
+int harris_run(harris_ctx* ctx, float* out, int64_t out_pitch, int64_t n, int64_t m, const float* rgb, float kappa,
+               void* stream) {
+    const int64_t W = m + 4, H = n + 4;
+    return run(ctx, make_call(out, out_pitch, n * out_pitch, n, m, rgb, W, H * W, 3 * H * W, 1, kappa, 0),
+               static_cast<cudaStream_t>(stream));
+}
+
+int harris_run_batched(harris_ctx* ctx, float* out, int64_t n, int64_t m, const float* rgb, int64_t batch,
+                       float kappa, void* stream) {
+    const int64_t W = m + 4, H = n + 4;
+    return run(ctx, make_call(out, m, n * m, n, m, rgb, W, H * W, 3 * H * W, batch, kappa, 0),
+               static_cast<cudaStream_t>(stream));
+}
+
+int harris_run_strided(harris_ctx* ctx, float* out, int64_t out_pitch, int64_t out_image_stride, int64_t n,
+                       int64_t m, const float* rgb, int64_t in_pitch, int64_t in_chan_stride,
+                       int64_t in_image_stride, int64_t batch, float kappa, uint32_t flags, void* stream) {
+    return run(ctx,
+               make_call(out, out_pitch, out_image_stride, n, m, rgb, in_pitch, in_chan_stride, in_image_stride,
+                         batch, kappa, flags),
+               static_cast<cudaStream_t>(stream));
+}
+
+int harris_plan(harris_ctx* ctx, int64_t n, int64_t m, int64_t batch, const float* rgb, int64_t in_pitch,
+                int64_t in_chan_stride, int64_t in_image_stride, const float* out, int64_t out_pitch,
+                int64_t out_image_stride, uint32_t flags, harris_plan_info* info) {
+    if (!ctx || !info) return HARRIS_ERR_INVALID_ARGUMENT;
+    Call c = make_call(const_cast<float*>(out), out_pitch, out_image_stride, n, m, rgb, in_pitch, in_chan_stride,
+                       in_image_stride, batch, 0.04f, flags);
+    int rc = validate(c);
+    if (rc) return rc;
+    std::memset(info, 0, sizeof(*info));
+    info->path = choose_path(c);
+    const TmaConfig& cfg = kTmaConfigs[ctx->tma_cfg];
+    info->warps_per_cta = cfg.warps;
+    info->stages = cfg.stages;
+    info->rows_per_stage = cfg.rows;
+    TileGeom tg;
+    int64_t grid = 0;
+    plan_launch(ctx, c, tg, grid);
+    info->band_rows = tg.band_rows;
+    info->bands = tg.bands;
+    info->col_segments = tg.colsegs;
+    info->tiles = tg.tiles;
+    info->grid_ctas = grid;
+    info->smem_bytes = int64_t(tma_smem_bytes(ctx->tma_cfg));
+    return HARRIS_OK;
+}
+
+int harris_last_path(const harris_ctx* ctx) { return ctx ? ctx->last_path : HARRIS_PATH_NONE; }
+int harris_device(const harris_ctx* ctx) { return ctx ? ctx->device : -1; }
+int harris_num_sms(const harris_ctx* ctx) { return ctx ? ctx->num_sms : 0; }
+const char* harris_last_cuda_error(const harris_ctx* ctx) { return ctx ? ctx->last_err : ""; }
+
+int harris_synth_fill(float* dst, int64_t planes, int64_t rows, int64_t W, int64_t dst_pitch,
+                      int64_t dst_plane_stride, int64_t H_global, int64_t row0, int64_t plane0, uint64_t seed,
+                      int dist, void* stream) {
+    if (!dst || planes < 0 || rows < 0 || W < 1 || dst_pitch < W || row0 < 0 || plane0 < 0 ||
+        row0 + rows > H_global || (planes > 1 && dst_plane_stride < rows * dst_pitch))
+        return HARRIS_ERR_INVALID_ARGUMENT;
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = launch_synth(dst, planes, rows, W, dst_pitch, dst_plane_stride, H_global, row0, plane0, seed,
+                                 dist, sms, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? HARRIS_OK : HARRIS_ERR_CUDA;
+}
+
+// ------------------------------------------------------------- host buffers
+static int ensure_staging(harris_ctx* ctx, size_t in_bytes, size_t out_bytes) {
+    cudaError_t e;
+    for (int k = 0; k < harris_ctx::kSlots; ++k) {
+        if (!ctx->streams[k]) {
+            e = cudaStreamCreateWithFlags(&ctx->streams[k], cudaStreamNonBlocking);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaStreamCreate");
+        }
+    }
+    if (in_bytes > ctx->cap_in) {
+        for (int k = 0; k < harris_ctx::kSlots; ++k) {
+            cudaFree(ctx->d_in[k]);
+            ctx->d_in[k] = nullptr;
+            e = cudaMalloc(&ctx->d_in[k], in_bytes);
+            if (e != cudaSuccess) {
+                ctx->cap_in = 0;
+                return cuda_fail(ctx, e, "cudaMalloc staging in");
+            }
+        }
+        ctx->cap_in = in_bytes;
+    }
+    if (out_bytes > ctx->cap_out) {
+        for (int k = 0; k < harris_ctx::kSlots; ++k) {
+            cudaFree(ctx->d_out[k]);
+            ctx->d_out[k] = nullptr;
+            e = cudaMalloc(&ctx->d_out[k], out_bytes);
+            if (e != cudaSuccess) {
+                ctx->cap_out = 0;
+                return cuda_fail(ctx, e, "cudaMalloc staging out");
+            }
+        }
+        ctx->cap_out = out_bytes;
+    }
+    return HARRIS_OK;
+}
+
+int harris_run_host(harris_ctx* ctx, float* out_host, int64_t out_pitch, int64_t n, int64_t m,
+                    const float* rgb_host, int64_t batch, float kappa, uint32_t flags) {
+    if (!ctx || !out_host || !rgb_host) return HARRIS_ERR_INVALID_ARGUMENT;
+    if (n < 1 || m < 1) return HARRIS_ERR_SIZE;
+    if (batch < 1 || out_pitch < m) return HARRIS_ERR_INVALID_ARGUMENT;
+    DeviceGuard guard(ctx->device);
+    if (!guard.ok) return cuda_fail(ctx, cudaGetLastError(), "cudaSetDevice");
+    const int64_t H = n + 4, W = m + 4;
+    const int64_t img_in = 3 * H * W;
+    const int64_t kChunkBytes = int64_t(48) << 20;  // input bytes per pipeline chunk
+    // chunk = a group of whole images, or (batch == 1 and large) a row band + 4-row halo
+    const bool banded = batch == 1 && img_in * 4 > kChunkBytes;
+    const int64_t imgs_per_chunk = banded ? 1 : std::max<int64_t>(1, kChunkBytes / (img_in * 4));
+    const int64_t band_rows = banded ? std::max<int64_t>(1, kChunkBytes / (3 * W * 4) - 4) : n;
+    const size_t in_bytes = size_t(banded ? 3 * (band_rows + 4) * W : imgs_per_chunk * img_in) * 4;
+    const size_t out_bytes = size_t(banded ? band_rows * m : imgs_per_chunk * n * m) * 4;
+    int rc = ensure_staging(ctx, in_bytes, out_bytes);
+    if (rc) return rc;
+    const int64_t nchunks = banded ? (n + band_rows - 1) / band_rows : (batch + imgs_per_chunk - 1) / imgs_per_chunk;
+    cudaError_t e = cudaSuccess;
+    for (int64_t k = 0; k < nchunks && rc == HARRIS_OK; ++k) {
+        const int slot = int(k % harris_ctx::kSlots);
+        cudaStream_t s = ctx->streams[slot];
+        float* din = ctx->d_in[slot];
+        float* dout = ctx->d_out[slot];
+        if (banded) {
+            const int64_t r0 = k * band_rows;
+            const int64_t rows = std::min(band_rows, n - r0);
+            const int64_t rin = rows + 4;
+            for (int c = 0; c < 3 && e == cudaSuccess; ++c)
+                e = cudaMemcpyAsync(din + c * rin * W, rgb_host + c * H * W + r0 * W, size_t(rin * W) * 4,
+                                    cudaMemcpyHostToDevice, s);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D band");
+            rc = run(ctx, make_call(dout, m, rows * m, rows, m, din, W, rin * W, 3 * rin * W, 1, kappa, flags), s);
+            if (rc) break;
+            e = cudaMemcpy2DAsync(out_host + r0 * out_pitch, size_t(out_pitch) * 4, dout, size_t(m) * 4,
+                                  size_t(m) * 4, size_t(rows), cudaMemcpyDeviceToHost, s);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "D2H band");
+        } else {
+            const int64_t b0 = k * imgs_per_chunk;
+            const int64_t nb = std::min(imgs_per_chunk, batch - b0);
+            e = cudaMemcpyAsync(din, rgb_host + b0 * img_in, size_t(nb * img_in) * 4, cudaMemcpyHostToDevice, s);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D images");
+            rc = run(ctx, make_call(dout, m, n * m, n, m, din, W, H * W, img_in, nb, kappa, flags), s);
+            if (rc) break;
+            e = cudaMemcpy2DAsync(out_host + b0 * n * out_pitch, size_t(out_pitch) * 4, dout, size_t(m) * 4,
+                                  size_t(m) * 4, size_t(nb * n), cudaMemcpyDeviceToHost, s);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "D2H images");
+        }
+    }
+    for (int k = 0; k < harris_ctx::kSlots; ++k) {
+        cudaError_t se = cudaStreamSynchronize(ctx->streams[k]);
+        if (se != cudaSuccess && rc == HARRIS_OK) rc = cuda_fail(ctx, se, "pipeline sync");
+    }
+    return rc;
+}
+
+}  // extern "C"

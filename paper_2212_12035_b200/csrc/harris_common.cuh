@@ -1,0 +1,147 @@
+// harris_common.cuh — arithmetic contract and sm_100a PTX helpers shared by the
+// fused Harris kernels.
+//
+// Arithmetic (thesis PAPER.md:2346-2374 / 4587-4730):
+//   g    = ((0.299f*R) + (0.587f*G)) + (0.114f*B)
+//   Ix   = 9-tap SX accumulation from 0 in row-major order, SX = [[-a,0,a],[-b,0,b],[-a,0,a]]
+//   Iy   = 9-tap SY = SX^T,  a = 0.083333336f (1/12), b = 0.16666667f (2/12)
+//   S**  = 9-tap box sums of the products Ix*Ix, Ix*Iy, Iy*Iy, row-major from 0
+//   out  = (Sxx*Syy - Sxy*Sxy) - (k*(Sxx+Syy))*(Sxx+Syy)
+// EXACT mode evaluates exactly that with __fmul_rn/__fadd_rn (never contracted),
+// so it is bit-identical to oracle/harris_oracle.c (-ffp-contract=off).  FAST
+// mode uses the separable (cbuf+rrot) order with FMAs and the
+// 1/12 Sobel scale folded into the gray weights; it is checked against the f64
+// oracle under the SURVEY.md §8(d) tolerance.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace harris {
+
+// thesis constants
+constexpr float kGrayR = 0.299f, kGrayG = 0.587f, kGrayB = 0.114f;
+constexpr float kSobA = 0.083333336f, kSobB = 0.16666667f;
+// FAST mode: gray pre-scaled by 1/12 so the separable Sobel needs no final scale
+constexpr float kGrayR12 = 0.299f / 12.0f, kGrayG12 = 0.587f / 12.0f, kGrayB12 = 0.114f / 12.0f;
+
+constexpr int kLanes = 32;
+constexpr int kColsPerLane = 4;                     // one float4 per lane
+constexpr int kWarpCols = kLanes * kColsPerLane;    // 128 output columns per warp strip
+constexpr int kBoxCols = kWarpCols + 4;             // + 4-column halo = 132 input columns
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "HARRIS_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra HARRIS_WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// 4-D TMA tile load global -> shared (x = column, y = row, c = channel,
+// b = image); completion is counted in bytes on `bar`.
+__device__ __forceinline__ void tma_load_4d(void* smem_dst, const void* tmap, uint64_t* bar, int x, int y,
+                                            int c, int b, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(x), "r"(y), "r"(c), "r"(b), "r"(smem_u32(bar)),
+        "l"(policy)
+        : "memory");
+}
+
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ void prefetch_tmap(const void* tmap) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
+}
+
+// plain C++ load (ordered after mbar_wait's "memory" clobber, free to schedule
+// otherwise); p must be 16-byte aligned shared memory
+__device__ __forceinline__ float4 lds128(const float* p) {
+    return *reinterpret_cast<const float4*>(p);
+}
+
+// streaming 16-byte store (output is written once, never re-read by the kernel)
+__device__ __forceinline__ void stg128_cs(float* p, float a, float b, float c, float d) {
+    asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
+                 : "memory");
+}
+
+// ------------------------------------------------------------ exact arithmetic
+__device__ __forceinline__ float gray_exact(float r, float g, float b) {
+    float t = __fadd_rn(0.0f, __fmul_rn(kGrayR, r));
+    t = __fadd_rn(t, __fmul_rn(kGrayG, g));
+    return __fadd_rn(t, __fmul_rn(kGrayB, b));
+}
+
+// 9-tap accumulation from 0 in row-major order, including the zero taps
+// (PAPER.md:4613-4635).  w is row-major 3x3; g0,g1,g2 are gray rows at x..x+2.
+__device__ __forceinline__ float conv9_exact(const float (&w)[9], float a0, float a1, float a2, float b0,
+                                             float b1, float b2, float c0, float c1, float c2) {
+    float t = 0.0f;
+    t = __fadd_rn(t, __fmul_rn(w[0], a0));
+    t = __fadd_rn(t, __fmul_rn(w[1], a1));
+    t = __fadd_rn(t, __fmul_rn(w[2], a2));
+    t = __fadd_rn(t, __fmul_rn(w[3], b0));
+    t = __fadd_rn(t, __fmul_rn(w[4], b1));
+    t = __fadd_rn(t, __fmul_rn(w[5], b2));
+    t = __fadd_rn(t, __fmul_rn(w[6], c0));
+    t = __fadd_rn(t, __fmul_rn(w[7], c1));
+    t = __fadd_rn(t, __fmul_rn(w[8], c2));
+    return t;
+}
+
+__device__ __forceinline__ float sum9_exact(float a0, float a1, float a2, float b0, float b1, float b2,
+                                            float c0, float c1, float c2) {
+    float s = __fadd_rn(0.0f, a0);
+    s = __fadd_rn(s, a1);
+    s = __fadd_rn(s, a2);
+    s = __fadd_rn(s, b0);
+    s = __fadd_rn(s, b1);
+    s = __fadd_rn(s, b2);
+    s = __fadd_rn(s, c0);
+    s = __fadd_rn(s, c1);
+    s = __fadd_rn(s, c2);
+    return s;
+}
+
+__device__ __forceinline__ float coarsity_exact(float sxx, float sxy, float syy, float k) {
+    float det = __fsub_rn(__fmul_rn(sxx, syy), __fmul_rn(sxy, sxy));
+    float tr = __fadd_rn(sxx, syy);
+    return __fsub_rn(det, __fmul_rn(__fmul_rn(k, tr), tr));
+}
+
+__device__ __forceinline__ float coarsity_fast(float sxx, float sxy, float syy, float k) {
+    float det = fmaf(-sxy, sxy, sxx * syy);
+    float tr = sxx + syy;
+    return fmaf(-k * tr, tr, det);
+}
+
+}  // namespace harris

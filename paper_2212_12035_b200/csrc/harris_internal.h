@@ -1,0 +1,52 @@
+// harris_internal.h — declarations shared between the kernel translation units
+// and the C-ABI layer (not part of the public ABI).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace harris {
+
+// Image geometry of one harris_run_strided call (element strides, not bytes).
+struct Geom {
+    int64_t n, m, batch;                       // output rows, cols; images
+    const float* rgb;
+    int64_t in_pitch, in_chan_stride, in_image_stride;
+    float* out;
+    int64_t out_pitch, out_image_stride;
+    float kappa;
+};
+
+// Tile decomposition for the TMA kernel: a tile is one 128-column warp strip of
+// `band_rows` output rows of one image.
+struct TileGeom {
+    int32_t n, m;
+    int32_t band_rows, bands, colsegs;
+    int32_t pad_;
+    int64_t tiles;
+    int64_t out_pitch, out_image_stride;
+    float* out;
+    float kappa;
+};
+
+// TMA kernel configurations (warps per CTA, pipeline stages per warp, input rows
+// per stage).  Index 0 is the default; HARRIS_TMA_CONFIG selects another one.
+struct TmaConfig {
+    int warps, stages, rows;
+};
+constexpr int kNumTmaConfigs = 4;
+extern const TmaConfig kTmaConfigs[kNumTmaConfigs];
+
+size_t tma_smem_bytes(int cfg);
+cudaError_t tma_configure(int cfg);                                   // smem attribute, once
+cudaError_t tma_occupancy(int cfg, int* ctas_per_sm);
+cudaError_t launch_tma(int cfg, bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid,
+                       cudaStream_t stream);
+
+cudaError_t launch_generic(bool exact, const Geom& g, cudaStream_t stream);
+
+cudaError_t launch_synth(float* dst, int64_t planes, int64_t rows, int64_t W, int64_t dst_pitch,
+                         int64_t dst_plane_stride, int64_t H_global, int64_t row0, int64_t plane0,
+                         uint64_t seed, int dist, int num_sms, cudaStream_t stream);
+
+}  // namespace harris

@@ -1,0 +1,210 @@
+"""PyTorch-facing mirror of the thesis Harris boundary, backed by the C-ABI.
+
+``harris(rgb)`` is the Rise ``harris : 3.(n+4).(m+4).f32 -> n.m.f32``
+(PAPER.md:2482-2496): planar RGB in, the valid region (4 smaller in each
+dimension, no padding) out.  A leading batch dimension is accepted.  CUDA
+tensors run on the current stream with no host synchronisation; CPU tensors /
+numpy arrays go through ``harris_run_host`` (pipelined H2D -> fused kernel ->
+D2H on the device), never through a CPU implementation.
+
+Torch is plumbing here (device memory, streams); the arithmetic is in
+``csrc/harris_tma.cu`` / ``csrc/harris_generic.cu``.
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import FLAG_EXACT_ORDER, FLAG_FORCE_GENERIC, FLAG_FORCE_TMA, PlanInfo, check, lib
+
+KAPPA = 0.04
+
+
+class HarrisContext:
+    """One ``harris_ctx`` bound to a CUDA device (``harris_init`` / ``harris_destroy``)."""
+
+    def __init__(self, device: int):
+        self.device = int(device)
+        h = ctypes.c_void_p()
+        check(lib().harris_init(ctypes.byref(h), self.device), f"harris_init(cuda:{self.device})")
+        self._h = h
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        return self._h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().harris_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def last_path(self) -> int:
+        return int(lib().harris_last_path(self._h))
+
+    @property
+    def num_sms(self) -> int:
+        return int(lib().harris_num_sms(self._h))
+
+    def run_strided(self, out_ptr: int, out_pitch: int, out_image_stride: int, n: int, m: int, rgb_ptr: int,
+                    in_pitch: int, in_chan_stride: int, in_image_stride: int, batch: int,
+                    kappa: float = KAPPA, flags: int = 0, stream: int = 0) -> None:
+        rc = lib().harris_run_strided(self._h, out_ptr, out_pitch, out_image_stride, n, m, rgb_ptr, in_pitch,
+                                      in_chan_stride, in_image_stride, batch, kappa, flags, stream)
+        check(rc, "harris_run_strided", self._h)
+
+    def plan(self, n: int, m: int, batch: int = 1, rgb_ptr: int = 0, in_pitch: Optional[int] = None,
+             in_chan_stride: Optional[int] = None, in_image_stride: Optional[int] = None, out_ptr: int = 0,
+             out_pitch: Optional[int] = None, out_image_stride: Optional[int] = None, flags: int = 0) -> dict:
+        W, H = m + 4, n + 4
+        in_pitch = W if in_pitch is None else in_pitch
+        in_chan_stride = H * in_pitch if in_chan_stride is None else in_chan_stride
+        in_image_stride = 3 * in_chan_stride if in_image_stride is None else in_image_stride
+        out_pitch = m if out_pitch is None else out_pitch
+        out_image_stride = n * out_pitch if out_image_stride is None else out_image_stride
+        # a dummy 256-byte aligned address stands in for "some aligned buffer"
+        rgb_ptr = rgb_ptr or 1 << 20
+        out_ptr = out_ptr or 1 << 21
+        info = PlanInfo()
+        rc = lib().harris_plan(self._h, n, m, batch, rgb_ptr, in_pitch, in_chan_stride, in_image_stride,
+                               out_ptr, out_pitch, out_image_stride, flags, ctypes.byref(info))
+        check(rc, "harris_plan", self._h)
+        return info.as_dict()
+
+    def run_host(self, rgb: np.ndarray, out: Optional[np.ndarray] = None, kappa: float = KAPPA,
+                 flags: int = 0) -> np.ndarray:
+        """Host buffers in, host buffer out (pinned memory gives full PCIe speed)."""
+        if rgb.dtype != np.float32 or not rgb.flags.c_contiguous:
+            raise ValueError("rgb must be C-contiguous float32")
+        batched = rgb.ndim == 4
+        x = rgb if batched else rgb[None]
+        if x.ndim != 4 or x.shape[1] != 3:
+            raise ValueError("rgb must be (3, H, W) or (B, 3, H, W)")
+        B, _, H, W = x.shape
+        n, m = H - 4, W - 4
+        if out is None:
+            out = np.empty((B, n, m) if batched else (n, m), dtype=np.float32)
+        if out.dtype != np.float32 or not out.flags.c_contiguous or out.size != B * max(n, 0) * max(m, 0):
+            raise ValueError("out must be C-contiguous float32 of the output shape")
+        rc = lib().harris_run_host(self._h, out.ctypes.data, m, n, m, x.ctypes.data, B, kappa, flags)
+        check(rc, "harris_run_host", self._h)
+        return out
+
+
+_ctx_lock = threading.Lock()
+_contexts: dict[int, HarrisContext] = {}
+
+
+def context(device: Optional[int] = None) -> HarrisContext:
+    """The process-wide context of a CUDA device (created on first use)."""
+    dev = torch.cuda.current_device() if device is None else int(device)
+    with _ctx_lock:
+        c = _contexts.get(dev)
+        if c is None:
+            c = HarrisContext(dev)
+            _contexts[dev] = c
+        return c
+
+
+def _flags(exact: bool, force_generic: bool, force_tma: bool) -> int:
+    return (FLAG_EXACT_ORDER if exact else 0) | (FLAG_FORCE_GENERIC if force_generic else 0) | (
+        FLAG_FORCE_TMA if force_tma else 0)
+
+
+def _check_rgb(rgb: torch.Tensor) -> tuple[int, int, int]:
+    if rgb.dtype != torch.float32:
+        raise TypeError("harris expects float32 planar RGB (Rise type 3.(n+4).(m+4).f32)")
+    if rgb.dim() == 3:
+        B = 1
+        C, H, W = rgb.shape
+    elif rgb.dim() == 4:
+        B, C, H, W = rgb.shape
+    else:
+        raise ValueError("rgb must be (3, H, W) or (B, 3, H, W)")
+    if C != 3:
+        raise ValueError(f"expected 3 planar channels, got {C}")
+    if H < 5 or W < 5:
+        raise ValueError(f"harris needs an input of at least 5x5, got {H}x{W}")
+    return B, H, W
+
+
+def harris(rgb, kappa: float = KAPPA, *, out: Optional[torch.Tensor] = None, exact: bool = False,
+           force_generic: bool = False, force_tma: bool = False, stream: Optional[torch.cuda.Stream] = None):
+    """Fused Harris coarsity of planar RGB f32.
+
+    rgb: ``(3, H, W)`` or ``(B, 3, H, W)`` float32; CUDA tensor (device path,
+    asynchronous on ``stream`` / the current stream) or CPU tensor / numpy array
+    (host path through the device).  Returns ``(H-4, W-4)`` / ``(B, H-4, W-4)``.
+    ``exact=True`` selects the Appendix-B op order (bit-identical to the C
+    oracle); the default is the FMA/separable order, within the SURVEY.md §8(d)
+    tolerance of the f64 reference.
+    """
+    flags = _flags(exact, force_generic, force_tma)
+    if isinstance(rgb, np.ndarray) or (isinstance(rgb, torch.Tensor) and not rgb.is_cuda):
+        arr = rgb if isinstance(rgb, np.ndarray) else rgb.numpy()
+        arr = np.ascontiguousarray(arr, dtype=np.float32)
+        dev = torch.cuda.current_device()
+        res = context(dev).run_host(arr, kappa=kappa, flags=flags)
+        return res if isinstance(rgb, np.ndarray) else torch.from_numpy(res)
+    B, H, W = _check_rgb(rgb)
+    if rgb.stride(-1) != 1:
+        rgb = rgb.contiguous()
+    n, m = H - 4, W - 4
+    batched = rgb.dim() == 4
+    if out is None:
+        out = torch.empty((B, n, m) if batched else (n, m), dtype=torch.float32, device=rgb.device)
+    else:
+        if out.dtype != torch.float32 or out.device != rgb.device:
+            raise ValueError("out must be float32 on the input's device")
+        if tuple(out.shape) != ((B, n, m) if batched else (n, m)) or out.stride(-1) != 1:
+            raise ValueError("out has the wrong shape or a non-unit column stride")
+    s_in = rgb.stride()
+    s_out = out.stride()
+    if batched:
+        in_image, in_chan, in_pitch = s_in[0], s_in[1], s_in[2]
+        out_image, out_pitch = s_out[0], s_out[1]
+    else:
+        in_chan, in_pitch = s_in[0], s_in[1]
+        in_image = 3 * in_chan
+        out_pitch = s_out[0]
+        out_image = n * out_pitch
+    dev = rgb.device.index if rgb.device.index is not None else torch.cuda.current_device()
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    context(dev).run_strided(out.data_ptr(), out_pitch, out_image, n, m, rgb.data_ptr(), in_pitch, in_chan,
+                             in_image, B, kappa, flags, st.cuda_stream)
+    return out
+
+
+def synth_(dst: torch.Tensor, seed: int, dist: int = 0, *, H_global: Optional[int] = None, row0: int = 0,
+           plane0: int = 0, stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """Fill ``dst`` (planes, rows, W) float32 CUDA, unit column stride, with the
+    synthetic image stack (see ``harris_synth_fill``); returns ``dst``."""
+    if dst.dtype != torch.float32 or not dst.is_cuda or dst.dim() != 3 or dst.stride(-1) != 1:
+        raise ValueError("dst must be a (planes, rows, W) float32 CUDA tensor with unit column stride")
+    P, R, W = dst.shape
+    Hg = R if H_global is None else H_global
+    st = stream if stream is not None else torch.cuda.current_stream(dst.device)
+    with torch.cuda.device(dst.device):
+        rc = lib().harris_synth_fill(dst.data_ptr(), P, R, W, dst.stride(1), dst.stride(0), Hg, row0, plane0,
+                                     seed, dist, st.cuda_stream)
+    check(rc, "harris_synth_fill")
+    return dst
+
+
+def algorithmic_bytes(n: int, m: int, batch: int = 1) -> int:
+    """12 B read per input pixel + 4 B written per output pixel (BASELINE.json)."""
+    return batch * (12 * (n + 4) * (m + 4) + 4 * n * m)
+
+
+__all__ = ["HarrisContext", "context", "harris", "synth_", "algorithmic_bytes", "KAPPA", "_lib"]

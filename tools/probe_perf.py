@@ -1,0 +1,84 @@
+"""Quick device-time probe of the fused kernel per TMA config (dev tool, not the bench).
+
+python tools/probe_perf.py [--configs 0,1,2,3] [--iters 20]
+Prints one line per (workload, config): ms, MP/s, algorithmic GB/s, fraction of
+MEASURED_PEAKS.json hbm_gbs.  Inputs are larger than L2 (no flush needed).
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_2212_12035_b200 as hb  # noqa: E402
+
+
+def peak():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    except Exception:
+        return 6650.0
+
+
+def time_cfg(cfg, workloads, iters, exact=False, generic=False):
+    env = dict(os.environ, HARRIS_TMA_CONFIG=str(cfg))
+    code = f"""
+import sys, torch, json
+sys.path.insert(0, {ROOT!r})
+import paper_2212_12035_b200 as hb
+res = []
+for (B, H, W) in {workloads!r}:
+    x = torch.empty((B, 3, H, W), device='cuda')
+    hb.synth_(x.view(B * 3, H, W), seed=12035)
+    out = torch.empty((B, H - 4, W - 4), device='cuda')
+    for _ in range(3):
+        hb.harris(x, out=out, exact={exact}, force_generic={generic})
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ts = []
+    for _ in range({iters}):
+        ev[0].record(); hb.harris(x, out=out, exact={exact}, force_generic={generic}); ev[1].record()
+        torch.cuda.synchronize(); ts.append(ev[0].elapsed_time(ev[1]))
+    ts.sort()
+    ms = ts[len(ts) // 2]
+    info = hb.context().plan(H - 4, W - 4, B)
+    res.append(dict(B=B, H=H, W=W, ms=ms, min_ms=ts[0], plan=info, path=hb.context().last_path))
+    del x, out
+    torch.cuda.empty_cache()
+print(json.dumps(res))
+"""
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+    if r.returncode != 0:
+        print(r.stderr[-2000:])
+        return []
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="0,1,2,3")
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--exact", action="store_true")
+    ap.add_argument("--generic", action="store_true")
+    a = ap.parse_args()
+    workloads = [(1, 8192, 8192), (1024, 1080, 1920), (1, 1536, 2560)]
+    pk = peak()
+    for cfg in [int(c) for c in a.configs.split(",")]:
+        for r in time_cfg(cfg, workloads, a.iters, a.exact, a.generic):
+            B, H, W = r["B"], r["H"], r["W"]
+            nbytes = hb.algorithmic_bytes(H - 4, W - 4, B)
+            gbs = nbytes / (r["ms"] * 1e-3) / 1e9
+            mps = B * (H - 4) * (W - 4) / (r["ms"] * 1e-3) / 1e6
+            print(f"cfg{cfg} exact={a.exact} generic={a.generic} {B}x{H}x{W}: {r['ms']:.4f} ms (min {r['min_ms']:.4f}) "
+                  f"{mps:,.0f} MP/s {gbs:,.0f} GB/s frac={gbs / pk:.3f} path={r['path']} "
+                  f"plan=bands{r['plan']['bands']}x{r['plan']['band_rows']} tiles={r['plan']['tiles']} "
+                  f"grid={r['plan']['grid_ctas']}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
