@@ -1,0 +1,493 @@
+#!/usr/bin/env python
+"""bench.py — fused Harris on B200: megapixels/s, % of HBM roofline, vs host CPU.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload batch|image8192|image1536|image32768]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
+    python bench.py --impl reference          # the reference CPU path (oracle port, all host cores)
+
+A step is one pass of the fused kernel over the workload: for the default
+workload (BASELINE.json configs[4], the only config quoted at 1/2/4/8 GPUs) a
+batch of 1024 synthetic 1920x1080 planar RGB f32 images, image-sharded across
+ranks (one batched launch per rank per step, no collective in the data path).
+Inputs (25.5 GB) are far larger than the 126 MB L2, so no flush is needed.
+Time = CUDA events on the launching stream, barrier + synchronize on both sides,
+max over ranks.  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+SEED = 12035
+KAPPA = 0.04
+METRIC_FALLBACK = "Harris megapixels/sec at 1/2/4/8 B200 and % of HBM roofline vs host CPU"
+
+WORKLOADS = {
+    "batch": dict(B=1024, H=1080, W=1920, sharding="image",
+                  desc="configs[4]: batch of 1024 images at 1920x1080 RGB f32, image-sharded"),
+    "image8192": dict(B=1, H=8192, W=8192, sharding="rows",
+                      desc="configs[2]: 8192x8192 RGB f32 (bandwidth-roofline run)"),
+    "image1536": dict(B=1, H=1536, W=2560, sharding="rows",
+                      desc="configs[1]: 1536x2560 RGB f32 (thesis image size)"),
+    "image32768": dict(B=1, H=32768, W=32768, sharding="rows",
+                       desc="configs[3]: 32768x32768 RGB f32, row bands with 4-row halos"),
+}
+
+NVML_REASONS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+    0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+    0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+}
+
+
+def metric_name() -> str:
+    try:
+        return json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+    except Exception:
+        return METRIC_FALLBACK
+
+
+def measured_peak() -> tuple[float, str]:
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(workload: str):
+    """Per-image DRAM bytes of the fused kernel from the committed ncu capture."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        return d.get(workload)
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock + clock-event reasons through NVML every ~5 ms in a thread."""
+
+    def __init__(self, device: int):
+        self.samples: list[tuple[float, int, int]] = []
+        self._stop = threading.Event()
+        self._thread = None
+        self.sm_max = None
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            uuid = str(torch.cuda.get_device_properties(device).uuid)
+            uuid = uuid if uuid.startswith("GPU-") else "GPU-" + uuid
+            try:
+                self.h = pynvml.nvmlDeviceGetHandleByUUID(uuid)
+            except Exception:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.nv = pynvml
+            self.sm_max = int(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+            fn = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            self._reasons = fn
+            self.ok = True
+        except Exception as e:  # pragma: no cover - NVML missing
+            self.err = repr(e)
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                c = int(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = int(self._reasons(self.h))
+                self.samples.append((time.perf_counter(), c, r))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def start(self):
+        if self.ok:
+            self._thread = threading.Thread(target=self._loop, daemon=True)
+            self._thread.start()
+
+    def stop(self):
+        if self._thread:
+            self._stop.set()
+            self._thread.join()
+
+    def summary(self, t0: float, t1: float) -> dict:
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "note": "nvml unavailable"}
+        inside = [s for s in self.samples if t0 <= s[0] <= t1]
+        use = inside if inside else self.samples[-5:]
+        mhz = [s[1] for s in use]
+        mask = 0
+        for s in use:
+            mask |= s[2]
+        reasons = [name for bit, name in NVML_REASONS.items() if mask & bit and name != "gpu_idle"]
+        return {"sm_mhz": float(statistics.median(mhz)) if mhz else None, "sm_max_mhz": self.sm_max,
+                "reasons": reasons, "samples": len(inside)}
+
+
+# ------------------------------------------------------------------ setup
+def dist_setup(init: bool = True):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not init:
+        return world, rank, local
+    if world > 1 and not dist.is_initialized():
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int, device) -> float:
+    if world == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+class Shard:
+    """This rank's share of the workload: images [b0, b0+nb) or output rows [r0, r0+rows)."""
+
+    def __init__(self, wl: dict, world: int, rank: int):
+        from paper_2212_12035_b200 import shard
+        self.H, self.W = wl["H"], wl["W"]
+        self.n, self.m = self.H - 4, self.W - 4
+        if wl["sharding"] == "image":
+            s = shard.image_shards(wl["B"], world)[rank]
+            self.b0, self.nb = s.image0, s.images
+            self.r0, self.rows = 0, self.n
+        else:
+            b = shard.row_bands(self.n, world)[rank]
+            self.b0, self.nb = 0, 1
+            self.r0, self.rows = b.out_row0, b.out_rows
+        self.total_px = wl["B"] * self.n * self.m
+        self.local_px = self.nb * self.rows * self.m
+
+    @property
+    def in_rows(self):
+        return self.rows + 4
+
+    def in_bytes(self):
+        return self.nb * 3 * self.in_rows * self.W * 4
+
+    def out_bytes(self):
+        return self.nb * self.rows * self.m * 4
+
+    def algorithmic_bytes(self):
+        # 12 B read per input pixel + 4 B written per output pixel
+        return self.nb * (12 * self.in_rows * self.W + 4 * self.rows * self.m)
+
+
+def make_inputs(sh: Shard, device):
+    import paper_2212_12035_b200 as hb
+    x = torch.empty((sh.nb, 3, sh.in_rows, sh.W), dtype=torch.float32, device=device)
+    # planes of global images b0.. (3 per image), rows r0.. of an H-row image
+    hb.synth_(x.view(sh.nb * 3, sh.in_rows, sh.W), seed=SEED, H_global=sh.H, row0=sh.r0, plane0=3 * sh.b0)
+    out = torch.empty((sh.nb, sh.rows, sh.m), dtype=torch.float32, device=device)
+    return x, out
+
+
+# ------------------------------------------------------------ CPU (oracle)
+def cpu_sample(sh_all: dict, images: int, rows: int | None):
+    """Host copy of a bounded sample of the workload: the first `images` images (or the
+    first `rows` output rows of the image), regenerated bit-exactly on the host."""
+    from oracle import cref
+    H, W = sh_all["H"], sh_all["W"]
+    if rows is None:
+        x = cref.synth(3 * images, H, W, seed=SEED).reshape(images, 3, H, W)
+        return x, images * (H - 4) * (W - 4), f"{images} image(s) of {W}x{H} (first of the batch)"
+    r = min(rows, H - 4)
+    x = cref.synth(3, H, W, seed=SEED, rows=r + 4).reshape(1, 3, r + 4, W)
+    return x, r * (W - 4), f"first {r} output rows of the {W}x{H} image"
+
+
+def cpu_time(x: np.ndarray, threads: int, min_seconds: float) -> tuple[float, int]:
+    """Seconds per pass of the C oracle (f32 App.-B order, OpenMP strips) and passes run."""
+    from oracle import cref
+    out = np.empty((x.shape[0], x.shape[2] - 4, x.shape[3] - 4), dtype=np.float32)
+    cref.harris_f32_batched(x, nthreads=threads, out=out)  # warm
+    t0 = time.perf_counter()
+    k = 0
+    while True:
+        cref.harris_f32_batched(x, nthreads=threads, out=out)
+        k += 1
+        dt = time.perf_counter() - t0
+        if dt >= min_seconds:
+            return dt / k, k
+
+
+def cpu_baseline(wl_name: str, wl: dict, min_seconds: float = 10.0) -> dict:
+    threads = os.cpu_count() or 1
+    if wl["B"] > 1:
+        x, px, desc = cpu_sample(wl, images=16, rows=None)
+    else:
+        x, px, desc = cpu_sample(wl, images=1, rows=max(64, (32 << 20) // (12 * wl["W"])))
+    per, k = cpu_time(x, threads, min_seconds)
+    return {"value": px / per / 1e6, "unit": "MP/s", "cores": threads, "kind": "port",
+            "sample": f"{desc}, repeated {k}x over {per * k:.1f} s; oracle/harris_oracle.c f32 "
+                      f"Appendix-B order, OpenMP 32-row strips (thesis cbuf schedule)",
+            "cpu_model": cpu_model()}
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# --------------------------------------------------------------- GPU arm
+def run_gpu(a, world, rank, local) -> dict | None:
+    import paper_2212_12035_b200 as hb
+    dev = torch.device("cuda", local)
+    wl = WORKLOADS[a.workload]
+    sh = Shard(wl, world, rank)
+    ctx = hb.context(local)
+    x, out = make_inputs(sh, dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        hb.harris(x if wl["B"] > 1 else x[0], out=out if wl["B"] > 1 else out[0])
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    assert ctx.last_path == hb._lib.PATH_TMA, "fused TMA kernel did not run"
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.02)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    w0 = time.perf_counter()
+    ev0.record(stream)
+    for _ in range(a.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    w1 = time.perf_counter()
+    barrier(world)
+    sampler.stop()
+    local_ms = ev0.elapsed_time(ev1)
+    ms = max_over_ranks(local_ms, world, dev)
+    clocks = sampler.summary(w0, w1)
+    value = sh.total_px * a.steps / (ms * 1e-3) / 1e6
+
+    peak, peak_kind = measured_peak()
+    launch_s = ms * 1e-3 / a.steps
+    achieved = sh.algorithmic_bytes() / launch_s / 1e9
+    tr = ncu_traffic(a.workload)
+    traffic = None
+    if tr and tr.get("dram_bytes_per_image") and wl["B"] > 1:
+        traffic = tr["dram_bytes_per_image"] * sh.nb
+    elif tr and tr.get("dram_bytes_per_launch") and world == 1:
+        traffic = tr["dram_bytes_per_launch"]
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "peak_kind": peak_kind,
+                "algorithmic_bytes_per_launch": sh.algorithmic_bytes(),
+                "per": "one fused-kernel launch per rank per step (max over ranks)"}
+    plan = ctx.plan(sh.rows, sh.m, sh.nb)
+
+    e2e = None
+    if not a.no_e2e:
+        e2e = run_e2e(a, sh, x, dev, world, ctx)
+    del x, out
+    torch.cuda.empty_cache()
+
+    extra = {}
+    if world == 1 and rank == 0 and not a.no_extra and a.workload == "batch":
+        extra = run_extra(a, ctx, dev)
+    cpu = None
+    if world == 1 and rank == 0 and not a.no_cpu_baseline:
+        cpu = cpu_baseline(a.workload, wl, a.cpu_seconds)
+    if rank != 0:
+        return None
+    return {
+        "metric": metric_name(), "value": value, "unit": "MP/s", "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32",
+        "data": f"synthetic planar RGB f32 U[0,1) (splitmix64 of the global pixel index, seed {SEED}), "
+                "generated on device",
+        "config": {"workload": wl["desc"], "images": wl["B"], "height": wl["H"], "width": wl["W"],
+                   "output": [wl["B"], wl["H"] - 4, wl["W"] - 4], "kappa": KAPPA,
+                   "parallelism": f"{'image' if wl['sharding'] == 'image' else 'row-band'}-sharded x{world}, "
+                                  "no data-path collective",
+                   "l2": "inputs larger than L2 (no flush needed)" if sh.in_bytes() > 512 << 20 else
+                         "inputs smaller than L2: see extra.l2_flushed",
+                   "kernel": "harris_tma_kernel (fused gray/Sobel/products/box/coarsity, TMA ring, FAST order)",
+                   "tma_config": os.environ.get("HARRIS_TMA_CONFIG", "default"), "plan": plan},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "clocks": clocks,
+        "gpu_launches": a.steps,
+        "impl": "b200",
+        "extra": extra,
+    }
+
+
+def run_e2e(a, sh: Shard, x_dev, dev, world, ctx) -> dict:
+    """Same metric through the public host-buffer API (HarrisContext.run_host ->
+    harris_run_host): pinned host input in, pinned host output back, every step."""
+    host_in = torch.empty(tuple(x_dev.shape), dtype=torch.float32, pin_memory=True)
+    host_in.copy_(x_dev)
+    host_out = torch.empty((sh.nb, sh.rows, sh.m), dtype=torch.float32, pin_memory=True)
+    hin = host_in.numpy() if sh.nb > 1 else host_in.numpy()[0]
+    hout = host_out.numpy() if sh.nb > 1 else host_out.numpy()[0]
+    ctx.run_host(hin, out=hout)  # warm-up (staging buffers)
+    steps = max(1, min(a.steps, a.e2e_steps))
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        ctx.run_host(hin, out=hout)
+    t1 = time.perf_counter()
+    barrier(world)
+    dt = max_over_ranks(t1 - t0, world, dev)
+    return {"value": sh.total_px * steps / dt / 1e6, "unit": "MP/s", "h2d_bytes_per_step": sh.in_bytes(),
+            "d2h_bytes_per_step": sh.out_bytes(), "steps": steps,
+            "api": "HarrisContext.run_host -> harris_run_host (pipelined H2D/kernel/D2H, 3 streams)",
+            "note": "bytes are per rank; host wall clock, max over ranks"}
+
+
+def time_launches(fn, iters: int, flush=None) -> list[float]:
+    ts = []
+    for _ in range(iters):
+        if flush is not None:
+            flush()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return ts
+
+
+def run_extra(a, ctx, dev) -> dict:
+    """Single-GPU roofline runs of the other configs (not the headline line)."""
+    import paper_2212_12035_b200 as hb
+    peak, _ = measured_peak()
+    res = {}
+    scratch = torch.empty(1 << 28, dtype=torch.float32, device=dev)  # 1 GiB > L2
+
+    def flush():
+        scratch.fill_(0.0)
+
+    for name, flushed in (("image8192", False), ("image1536", True)):
+        wl = WORKLOADS[name]
+        H, W = wl["H"], wl["W"]
+        x = torch.empty((3, H, W), device=dev)
+        hb.synth_(x, seed=SEED)
+        out = torch.empty((H - 4, W - 4), device=dev)
+        for _ in range(3):
+            hb.harris(x, out=out)
+        torch.cuda.synchronize()
+        ts = sorted(time_launches(lambda: hb.harris(x, out=out), 30, flush if flushed else None))
+        med = ts[len(ts) // 2]
+        nbytes = hb.algorithmic_bytes(H - 4, W - 4)
+        gbs = nbytes / (med * 1e-3) / 1e9
+        res[name] = {"workload": wl["desc"], "ms_median_of_30": med, "ms_min": ts[0],
+                     "value": (H - 4) * (W - 4) / (med * 1e-3) / 1e6, "unit": "MP/s",
+                     "achieved_gbs": gbs, "frac_of_measured_hbm": gbs / peak,
+                     "l2": "flushed (1 GiB write) before every launch" if flushed else "input 768 MiB > L2",
+                     "plan": ctx.plan(H - 4, W - 4, 1)}
+        del x, out
+    del scratch
+    torch.cuda.empty_cache()
+    return res
+
+
+# ---------------------------------------------------------- reference arm
+def run_reference(a, world, rank) -> dict | None:
+    """The reference's CPU implementation of the path on this box's host cores.  The
+    reference package is Python (sges) and does not travel to the GPU box, so the arm
+    runs the oracle port of it (oracle/harris_oracle.c, pinned bit-for-bit to the
+    reference evaluator by tests/golden)."""
+    if rank != 0:
+        return None
+    wl = WORKLOADS[a.workload]
+    threads = os.cpu_count() or 1
+    if wl["B"] > 1:
+        x, px, desc = cpu_sample(wl, images=a.ref_images, rows=None)
+    else:
+        x, px, desc = cpu_sample(wl, images=1, rows=max(64, (32 << 20) // (12 * wl["W"])))
+    from oracle import cref
+    outb = np.empty((x.shape[0], x.shape[2] - 4, x.shape[3] - 4), dtype=np.float32)
+    for _ in range(a.warmup):
+        cref.harris_f32_batched(x, nthreads=threads, out=outb)
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        cref.harris_f32_batched(x, nthreads=threads, out=outb)
+    dt = time.perf_counter() - t0
+    value = px * a.steps / dt / 1e6
+    return {
+        "metric": metric_name(), "value": value, "unit": "MP/s", "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": dt * 1e3 / a.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": f"synthetic planar RGB f32 (seed {SEED}), host",
+        "config": {"workload": wl["desc"], "images": wl["B"], "height": wl["H"], "width": wl["W"],
+                   "sample_per_step": desc},
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "MP/s", "cores": threads, "kind": "port",
+                         "sample": f"{desc} per step; oracle/harris_oracle.c (f32 Appendix-B order, "
+                                   "OpenMP 32-row strips)", "cpu_model": cpu_model()},
+        "e2e": {"value": value, "unit": "MP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=None)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="batch")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--ref-images", type=int, default=32)
+    a = ap.parse_args()
+    a.warmup = max(3, a.warmup)
+    world, rank, local = dist_setup(init=a.impl == "b200")
+    if a.gpus is not None and a.gpus != world and world > 1:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
+    if a.impl == "reference":
+        res = run_reference(a, world, rank)
+    else:
+        res = run_gpu(a, world, rank, local)
+    if res is not None:
+        print(json.dumps(res), flush=True)
+    if world > 1 and dist.is_initialized():
+        if a.impl == "b200":
+            dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -46,10 +46,10 @@
 namespace harris {
 
 const TmaConfig kTmaConfigs[kNumTmaConfigs] = {
-    {4, 4, 3},  // 0: default, 78 KB smem / CTA
+    {8, 3, 3},  // 0: default, 117 KB smem / CTA, 1 CTA (8 warps) per SM
     {2, 4, 3},  // 1
     {4, 3, 6},  // 2
-    {8, 3, 3},  // 3
+    {4, 4, 3},  // 3
 };
 
 template <int NW, int NS, int CH>
@@ -314,30 +314,30 @@ static cudaError_t occupancy_one(int* n) {
 
 size_t tma_smem_bytes(int cfg) {
     switch (cfg) {
-        case 0: return TmaShape<4, 4, 3>::kSmemBytes;
+        case 0: return TmaShape<8, 3, 3>::kSmemBytes;
         case 1: return TmaShape<2, 4, 3>::kSmemBytes;
         case 2: return TmaShape<4, 3, 6>::kSmemBytes;
-        case 3: return TmaShape<8, 3, 3>::kSmemBytes;
+        case 3: return TmaShape<4, 4, 3>::kSmemBytes;
         default: return 0;
     }
 }
 
 cudaError_t tma_configure(int cfg) {
     switch (cfg) {
-        case 0: return configure_one<4, 4, 3>();
+        case 0: return configure_one<8, 3, 3>();
         case 1: return configure_one<2, 4, 3>();
         case 2: return configure_one<4, 3, 6>();
-        case 3: return configure_one<8, 3, 3>();
+        case 3: return configure_one<4, 4, 3>();
         default: return cudaErrorInvalidValue;
     }
 }
 
 cudaError_t tma_occupancy(int cfg, int* ctas_per_sm) {
     switch (cfg) {
-        case 0: return occupancy_one<4, 4, 3>(ctas_per_sm);
+        case 0: return occupancy_one<8, 3, 3>(ctas_per_sm);
         case 1: return occupancy_one<2, 4, 3>(ctas_per_sm);
         case 2: return occupancy_one<4, 3, 6>(ctas_per_sm);
-        case 3: return occupancy_one<8, 3, 3>(ctas_per_sm);
+        case 3: return occupancy_one<4, 4, 3>(ctas_per_sm);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -345,10 +345,10 @@ cudaError_t tma_occupancy(int cfg, int* ctas_per_sm) {
 cudaError_t launch_tma(int cfg, bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid,
                        cudaStream_t stream) {
     switch (cfg) {
-        case 0: return launch_one<4, 4, 3>(exact, tmap, tg, grid, stream);
+        case 0: return launch_one<8, 3, 3>(exact, tmap, tg, grid, stream);
         case 1: return launch_one<2, 4, 3>(exact, tmap, tg, grid, stream);
         case 2: return launch_one<4, 3, 6>(exact, tmap, tg, grid, stream);
-        case 3: return launch_one<8, 3, 3>(exact, tmap, tg, grid, stream);
+        case 3: return launch_one<4, 4, 3>(exact, tmap, tg, grid, stream);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -122,14 +122,15 @@ def _flags(exact: bool, force_generic: bool, force_tma: bool) -> int:
         FLAG_FORCE_TMA if force_tma else 0)
 
 
-def _check_rgb(rgb: torch.Tensor) -> tuple[int, int, int]:
-    if rgb.dtype != torch.float32:
+def _check_rgb(rgb) -> tuple[int, int, int]:
+    if rgb.dtype not in (torch.float32, np.float32):
         raise TypeError("harris expects float32 planar RGB (Rise type 3.(n+4).(m+4).f32)")
-    if rgb.dim() == 3:
+    shape = tuple(rgb.shape)
+    if len(shape) == 3:
         B = 1
-        C, H, W = rgb.shape
-    elif rgb.dim() == 4:
-        B, C, H, W = rgb.shape
+        C, H, W = shape
+    elif len(shape) == 4:
+        B, C, H, W = shape
     else:
         raise ValueError("rgb must be (3, H, W) or (B, 3, H, W)")
     if C != 3:
@@ -152,8 +153,9 @@ def harris(rgb, kappa: float = KAPPA, *, out: Optional[torch.Tensor] = None, exa
     """
     flags = _flags(exact, force_generic, force_tma)
     if isinstance(rgb, np.ndarray) or (isinstance(rgb, torch.Tensor) and not rgb.is_cuda):
+        _check_rgb(rgb)
         arr = rgb if isinstance(rgb, np.ndarray) else rgb.numpy()
-        arr = np.ascontiguousarray(arr, dtype=np.float32)
+        arr = np.ascontiguousarray(arr)
         dev = torch.cuda.current_device()
         res = context(dev).run_host(arr, kappa=kappa, flags=flags)
         return res if isinstance(rgb, np.ndarray) else torch.from_numpy(res)
