@@ -1,0 +1,80 @@
+"""Register the fused B200 kernel as an ambient Rise primitive in the reference
+``sges`` package (the in-package drop-in hook of SURVEY.md §8b(ii)).
+
+The reference's type checker treats any name in ``env`` as a polymorphic scheme
+instantiated per use (infer.py:190-196, 252-253) and its evaluator lets ``amb``
+override primitive semantics (evalref.py:142-144).  Registering
+
+    env["harris"] = 3.(?n+4).(?m+4).f32 -> ?n.?m.f32
+    amb["harris"] = <callable running the fused kernel>
+
+makes ``harris rgb`` type-check to ``n.m.f32`` and evaluate on the GPU.  Values
+cross that boundary as nested Python lists (evalref.py:1-7), so this bridge is
+for interoperability and parity harnesses, not for throughput.
+
+The reference type checker does not reject degenerate sizes (it solves
+``?m = -2`` for a 3x5x2 input, nat.py:211-239), so the bridge validates
+``H, W >= 5`` itself before calling the C-ABI (which also rejects them).
+"""
+from __future__ import annotations
+
+import os
+import sys
+from typing import Callable, Optional
+
+import numpy as np
+
+HARRIS_SCHEME = "3.(?n+4).(?m+4).f32 -> ?n.?m.f32"
+
+
+def _sges(reference_src: Optional[str] = None):
+    src = reference_src or os.environ.get("HARRIS_REFERENCE_SRC")
+    if src and src not in sys.path:
+        sys.path.insert(0, src)
+    try:
+        from sges import parser  # noqa: F401
+    except ImportError as e:  # pragma: no cover - depends on the user's install
+        raise ImportError("the reference package `sges` is not importable; set HARRIS_REFERENCE_SRC "
+                          "to its src directory") from e
+    from sges import evalref, infer, parser
+    return parser, infer, evalref
+
+
+def gpu_impl(kappa: float = 0.04) -> Callable[[np.ndarray], np.ndarray]:
+    """(3, H, W) float32 host array -> (H-4, W-4) through the fused kernel."""
+    import torch
+
+    from .harris import harris
+
+    def run(rgb: np.ndarray) -> np.ndarray:
+        t = torch.from_numpy(np.ascontiguousarray(rgb, dtype=np.float32)).cuda()
+        out = harris(t, kappa)
+        return out.cpu().numpy()
+
+    return run
+
+
+def register(env: dict, amb: dict, impl: Optional[Callable[[np.ndarray], np.ndarray]] = None,
+             reference_src: Optional[str] = None) -> tuple[dict, dict]:
+    """Add the ``harris`` scheme to a type environment and its implementation to
+    an evaluator ambient map; ``impl`` defaults to the B200 kernel."""
+    parser, _, _ = _sges(reference_src)
+    fn = impl or gpu_impl()
+    env["harris"] = parser.parse_type(HARRIS_SCHEME)
+
+    def _call(rgb_lists):
+        arr = np.asarray(rgb_lists, dtype=np.float32)
+        if arr.ndim != 3 or arr.shape[0] != 3 or arr.shape[1] < 5 or arr.shape[2] < 5:
+            raise ValueError(f"harris needs a 3 x (n+4) x (m+4) input with n, m >= 1, got {arr.shape}")
+        return np.asarray(fn(arr), dtype=np.float64).tolist()
+
+    amb["harris"] = _call
+    return env, amb
+
+
+def evaluate(src: str, env: dict, amb: dict, sizes=(), nenv: Optional[dict] = None,
+             reference_src: Optional[str] = None):
+    """Parse, type and evaluate a Rise program that may call ``harris``."""
+    parser, infer, evalref = _sges(reference_src)
+    term = infer.from_named(parser.parse_term(src), env=env, sizes=set(sizes))
+    return term, evalref.eval_term(term, (), amb, nenv or {})

@@ -120,3 +120,26 @@ def test_live_reference_types_and_ambient_boundary():
     rgb = synth.synth_numpy(3, 9, 12, seed=3)
     via = sges_oracle.eval_via_ambient(rgb, cref.harris_f64)
     assert np.array_equal(via, sges_oracle.harris_sges(rgb))
+
+
+@needs_ref
+def test_sges_bridge_registration_types_and_evaluates(oracle_lib):
+    """The product-side bridge registers `harris` with the reference type checker; here
+    the implementation is the oracle (no GPU in this container) — on a GPU box with the
+    reference installed the default implementation is the fused kernel."""
+    from paper_2212_12035_b200 import sges_bridge
+    from sges import types, nat
+    rgb = synth.synth_numpy(3, 8, 10, seed=17)
+    env = {"rgb": types.data(types.array(nat.const(3), types.array(nat.const(8),
+                             types.array(nat.const(10), types.scalar()))))}
+    amb = {"rgb": rgb.astype(np.float64).tolist()}
+    sges_bridge.register(env, amb, impl=cref.harris_f64, reference_src=sges_oracle.REFERENCE_SRC)
+    term, val = sges_bridge.evaluate("harris rgb", env, amb, reference_src=sges_oracle.REFERENCE_SRC)
+    assert "4" in str(term.ty) and "6" in str(term.ty)
+    assert np.array_equal(np.asarray(val), sges_oracle.harris_sges(rgb))
+    bad = {"rgb": types.data(types.array(nat.const(3), types.array(nat.const(5),
+                             types.array(nat.const(2), types.scalar()))))}
+    amb_bad = {"rgb": np.zeros((3, 5, 2)).tolist()}
+    sges_bridge.register(bad, amb_bad, impl=cref.harris_f64, reference_src=sges_oracle.REFERENCE_SRC)
+    with pytest.raises(ValueError):
+        sges_bridge.evaluate("harris rgb", bad, amb_bad, reference_src=sges_oracle.REFERENCE_SRC)
