@@ -139,15 +139,28 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ setup
-def dist_setup(init: bool = True):
+_BACKEND = "nccl"
+
+
+def dist_setup(init: bool = True, backend: str = "nccl"):
+    """One process per GPU (torchrun env).  backend="gloo" together with
+    HARRIS_BENCH_SHARE_GPU=1 lets several ranks share one GPU to exercise the N>1
+    code path on a single-GPU box (a test mode, never a reported number)."""
+    global _BACKEND
+    _BACKEND = backend
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("HARRIS_BENCH_SHARE_GPU") == "1" and torch.cuda.is_available():
+        local = local % torch.cuda.device_count()
     if not init:
         return world, rank, local
     if world > 1 and not dist.is_initialized():
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     elif torch.cuda.is_available():
         torch.cuda.set_device(local)
     return world, rank, local
@@ -161,7 +174,7 @@ def barrier(world):
 def max_over_ranks(x: float, world: int, device) -> float:
     if world == 1:
         return x
-    t = torch.tensor([x], dtype=torch.float64, device=device)
+    t = torch.tensor([x], dtype=torch.float64, device=device if _BACKEND == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -375,7 +388,10 @@ def run_e2e(a, sh: Shard, x_dev, dev, world, ctx) -> dict:
 
 
 def time_launches(fn, iters: int, flush=None) -> list[float]:
-    ts = []
+    """Per-launch CUDA-event times of back-to-back launches (one sync at the end, so the
+    GPU never idles between launches); with `flush`, an L2-flushing write precedes
+    every launch outside its event pair."""
+    evs = []
     for _ in range(iters):
         if flush is not None:
             flush()
@@ -383,9 +399,9 @@ def time_launches(fn, iters: int, flush=None) -> list[float]:
         e0.record()
         fn()
         e1.record()
-        torch.cuda.synchronize()
-        ts.append(e0.elapsed_time(e1))
-    return ts
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in evs]
 
 
 def run_extra(a, ctx, dev) -> dict:
@@ -472,9 +488,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-images", type=int, default=32)
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl")
     a = ap.parse_args()
     a.warmup = max(3, a.warmup)
-    world, rank, local = dist_setup(init=a.impl == "b200")
+    world, rank, local = dist_setup(init=a.impl == "b200", backend=a.dist_backend)
     if a.gpus is not None and a.gpus != world and world > 1:
         raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
     if a.impl == "reference":

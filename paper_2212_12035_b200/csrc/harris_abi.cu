@@ -29,6 +29,8 @@ struct harris_ctx {
     int num_sms = 0;
     int cc_major = 0, cc_minor = 0;
     int tma_cfg = 0;
+    int l2_policy = 1;  // evict_normal: the 4-column halo sectors are re-read by the neighbouring strip
+    int64_t force_band_rows = 0;  // dev knob (HARRIS_BAND_ROWS): override the planner
     int occ[kNumTmaConfigs] = {0};
     PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     int last_path = HARRIS_PATH_NONE;
@@ -98,8 +100,19 @@ bool tma_eligible(const Call& c) {
 
 // Pick the band height that minimises (waves x rows-per-tile) for a persistent
 // grid of `gw` warps: tiles = batch x bands x col_segments.
-void plan_tiles(int64_t n, int64_t m, int64_t batch, int64_t gw, int rows_per_stage, TileGeom& tg) {
+void plan_tiles(int64_t n, int64_t m, int64_t batch, int64_t gw, int rows_per_stage, int64_t force_rows,
+                TileGeom& tg) {
     const int64_t colsegs = (m + kWarpCols - 1) / kWarpCols;
+    if (force_rows > 0) {
+        const int64_t rows = std::min(force_rows, n);
+        tg.n = int32_t(n);
+        tg.m = int32_t(m);
+        tg.band_rows = int32_t(rows);
+        tg.bands = int32_t((n + rows - 1) / rows);
+        tg.colsegs = int32_t(colsegs);
+        tg.tiles = batch * colsegs * tg.bands;
+        return;
+    }
     const int64_t kTileOverheadRows = 6;  // pipeline/tile switch cost in row-equivalents
     const int64_t max_bands = std::max<int64_t>(1, std::min<int64_t>(n, 1 + n / 8));
     int64_t best_cost = INT64_MAX, best_rows = n, best_bands = 1;
@@ -134,13 +147,13 @@ void plan_launch(const harris_ctx* ctx, const Call& c, TileGeom& tg, int64_t& gr
     const TmaConfig& cfg = kTmaConfigs[ctx->tma_cfg];
     const int occ = std::max(1, ctx->occ[ctx->tma_cfg]);
     const int64_t resident_ctas = int64_t(ctx->num_sms) * occ;
-    plan_tiles(c.g.n, c.g.m, c.g.batch, resident_ctas * cfg.warps, cfg.rows, tg);
+    plan_tiles(c.g.n, c.g.m, c.g.batch, resident_ctas * cfg.warps, cfg.rows, ctx->force_band_rows, tg);
     grid = std::min<int64_t>((tg.tiles + cfg.warps - 1) / cfg.warps, resident_ctas);
     tg.out = c.g.out;
     tg.out_pitch = c.g.out_pitch;
     tg.out_image_stride = c.g.out_image_stride;
     tg.kappa = c.g.kappa;
-    tg.pad_ = 0;
+    tg.l2_policy = ctx->l2_policy;
 }
 
 int encode_tmap(harris_ctx* ctx, const Call& c, CUtensorMap* tmap) {
@@ -259,6 +272,13 @@ int harris_init(harris_ctx** out_ctx, int cuda_device) {
     if (env) {
         int v = std::atoi(env);
         if (v >= 0 && v < kNumTmaConfigs) ctx->tma_cfg = v;
+    }
+    env = std::getenv("HARRIS_BAND_ROWS");
+    if (env) ctx->force_band_rows = std::atoll(env);
+    env = std::getenv("HARRIS_L2_POLICY");
+    if (env) {
+        int v = std::atoi(env);
+        if (v >= 0 && v <= 2) ctx->l2_policy = v;
     }
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;

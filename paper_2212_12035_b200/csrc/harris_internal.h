@@ -22,7 +22,7 @@ struct Geom {
 struct TileGeom {
     int32_t n, m;
     int32_t band_rows, bands, colsegs;
-    int32_t pad_;
+    int32_t l2_policy;  // 0 evict_first, 1 evict_normal (default), 2 evict_last
     int64_t tiles;
     int64_t out_pitch, out_image_stride;
     float* out;

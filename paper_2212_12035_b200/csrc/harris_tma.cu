@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
         fence_barrier_init();
     }
     __syncwarp();
-    const uint64_t policy = l2_policy_evict_first();
+    const uint64_t policy = l2_policy(g.l2_policy);
 
     // ---- producer cursor (warp-uniform; lane 0 issues) ----
     int64_t pt = gw;

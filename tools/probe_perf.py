@@ -39,12 +39,13 @@ for (B, H, W) in {workloads!r}:
     for _ in range(3):
         hb.harris(x, out=out, exact={exact}, force_generic={generic})
     torch.cuda.synchronize()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    ts = []
+    evs = []
     for _ in range({iters}):
-        ev[0].record(); hb.harris(x, out=out, exact={exact}, force_generic={generic}); ev[1].record()
-        torch.cuda.synchronize(); ts.append(ev[0].elapsed_time(ev[1]))
-    ts.sort()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(); hb.harris(x, out=out, exact={exact}, force_generic={generic}); e1.record()
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    ts = sorted(a.elapsed_time(b) for a, b in evs)
     ms = ts[len(ts) // 2]
     info = hb.context().plan(H - 4, W - 4, B)
     res.append(dict(B=B, H=H, W=W, ms=ms, min_ms=ts[0], plan=info, path=hb.context().last_path))
