@@ -112,6 +112,22 @@ HARRIS_API int harris_synth_fill(float* dst, int64_t planes, int64_t rows, int64
                       int64_t dst_plane_stride, int64_t H_global, int64_t row0, int64_t plane0,
                       uint64_t seed, int dist, void* cuda_stream);
 
+/* Kernel-grouping design space of the thesis, for the fusion
+ * ablation: each group is a separate kernel that round-trips its intermediates
+ * through HBM in caller-provided scratch (the thesis's t1..t3 temporaries).
+ * Groupings 1-3 always evaluate the Appendix-B order (bit-identical to the oracle);
+ * grouping 4 is harris_run_strided (flags honoured).  Contiguous single image. */
+#define HARRIS_GROUPING_UNFUSED    1  /* [Sx],[Sy],[x],[+],[coarsity]  5 kernels */
+#define HARRIS_GROUPING_SOBEL_PROD 2  /* [Sx,Sy,x],[+,coarsity]        2 kernels */
+#define HARRIS_GROUPING_SOBEL      3  /* [Sx,Sy],[x,+,coarsity]        2 kernels */
+#define HARRIS_GROUPING_FUSED      4  /* [Sx,Sy,x,+,coarsity]          1 kernel  */
+
+HARRIS_API int64_t harris_grouping_scratch_bytes(int grouping, int64_t n, int64_t m);
+HARRIS_API int harris_grouping_launches(int grouping);
+HARRIS_API int harris_run_grouping(harris_ctx* ctx, int grouping, float* out, int64_t n, int64_t m,
+                                   const float* rgb, void* scratch, int64_t scratch_bytes, float kappa,
+                                   uint32_t flags, void* cuda_stream);
+
 /* Launch geometry the TMA kernel would use (for tests / bench reporting). */
 typedef struct harris_plan_info {
     int32_t path;           /* HARRIS_PATH_* that harris_run_strided would take */

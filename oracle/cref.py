@@ -39,6 +39,10 @@ def lib() -> ctypes.CDLL:
         L.oracle_harris_f64.restype = ctypes.c_int
         L.oracle_harris_f32_batched.argtypes = [vp, i64, i64, vp, i64, ctypes.c_float, ctypes.c_int]
         L.oracle_harris_f32_batched.restype = ctypes.c_int
+        L.oracle_harris_f32_rrot.argtypes = [vp, i64, i64, i64, vp, i64, i64, ctypes.c_float, ctypes.c_int]
+        L.oracle_harris_f32_rrot.restype = ctypes.c_int
+        L.oracle_harris_f32_rrot_batched.argtypes = [vp, i64, i64, vp, i64, ctypes.c_float, ctypes.c_int]
+        L.oracle_harris_f32_rrot_batched.restype = ctypes.c_int
         L.oracle_synth_fill.argtypes = [vp, i64, i64, i64, i64, i64, i64, i64, i64, ctypes.c_uint64, ctypes.c_int]
         L.oracle_synth_fill.restype = None
         L.oracle_max_threads.argtypes = []
@@ -72,6 +76,17 @@ def harris_f32(rgb: np.ndarray, kappa: float = 0.04, nthreads: int = 0) -> np.nd
     return out
 
 
+def harris_f32_rrot(rgb: np.ndarray, kappa: float = 0.04, nthreads: int = 0) -> np.ndarray:
+    """Thesis cbuf+rrot schedule (separable order) in f32."""
+    rgb = np.ascontiguousarray(rgb)
+    H, W = _check_rgb(rgb)
+    out = np.empty((H - 4, W - 4), dtype=np.float32)
+    rc = lib().oracle_harris_f32_rrot(_ptr(out), W - 4, H - 4, W - 4, _ptr(rgb), W, H * W, kappa, nthreads)
+    if rc:
+        raise RuntimeError(f"oracle_harris_f32_rrot failed ({rc})")
+    return out
+
+
 def harris_f64(rgb: np.ndarray, kappa: float = 0.04, nthreads: int = 0) -> np.ndarray:
     """f64 restatement in sges evaluation order, from the f32 input."""
     rgb = np.ascontiguousarray(rgb)
@@ -94,6 +109,22 @@ def harris_f32_batched(rgb: np.ndarray, kappa: float = 0.04, nthreads: int = 0,
     rc = lib().oracle_harris_f32_batched(_ptr(out), H - 4, W - 4, _ptr(rgb), B, kappa, nthreads)
     if rc:
         raise RuntimeError(f"oracle_harris_f32_batched failed ({rc})")
+    return out
+
+
+def harris_batched(rgb: np.ndarray, variant: str = "cbuf", kappa: float = 0.04, nthreads: int = 0,
+                   out: np.ndarray | None = None) -> np.ndarray:
+    """Batched CPU Harris with the thesis schedule `variant` in {"cbuf", "rrot"}."""
+    if variant == "cbuf":
+        return harris_f32_batched(rgb, kappa, nthreads, out)
+    if rgb.dtype != np.float32 or rgb.ndim != 4 or rgb.shape[1] != 3 or not rgb.flags.c_contiguous:
+        raise ValueError("rgb must be C-contiguous float32 of shape (B, 3, H, W)")
+    B, _, H, W = rgb.shape
+    if out is None:
+        out = np.empty((B, H - 4, W - 4), dtype=np.float32)
+    rc = lib().oracle_harris_f32_rrot_batched(_ptr(out), H - 4, W - 4, _ptr(rgb), B, kappa, nthreads)
+    if rc:
+        raise RuntimeError(f"oracle_harris_f32_rrot_batched failed ({rc})")
     return out
 
 

@@ -316,6 +316,119 @@ int oracle_harris_f64(double* out, int64_t out_pitch, int64_t n, int64_t m,
     return err;
 }
 
+/* ----------------------------------------------- f32 cbuf+rrot CPU port --- */
+/* The thesis's fastest CPU schedule, cbuf+rrot (1.24x over
+ * cbuf on ARM): 32-row strips, 3-line circular buffers of gray,
+ * SEPARATED convolutions — vertical [1,2,1] / [-1,0,1] sums of gray, then the
+ * horizontal +-1/12, 1/6 taps — and box sums as vertical
+ * 3-row sums of the products followed by horizontal 3-sums,
+ * every accumulation from 0 in listing order (-ffp-contract=off).  A different
+ * op order from Appendix B (results agree within the SURVEY.md §8(d) tolerance,
+ * not bit-for-bit); used as the strongest CPU baseline. */
+int oracle_harris_f32_rrot(float* out, int64_t out_pitch, int64_t n, int64_t m,
+                           const float* rgb, int64_t in_pitch, int64_t chan_stride,
+                           float kappa, int nthreads) {
+    if (n < 1 || m < 1 || !out || !rgb || out_pitch < m || in_pitch < m + 4) return -1;
+    const int64_t W = m + 4, Ws = m + 2;
+    const int64_t nstrips = (n + STRIP - 1) / STRIP;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+    int err = 0;
+#pragma omp parallel
+    {
+        /* 3 gray lines, 2 vertical-sum lines, 3 Ix + 3 Iy lines, 3 vertical box lines */
+        float* buf = (float*)malloc(sizeof(float) * (size_t)(5 * W + 6 * Ws + 3 * Ws));
+        if (!buf) {
+#pragma omp atomic write
+            err = -2;
+        }
+#pragma omp for schedule(dynamic, 1)
+        for (int64_t s = 0; s < nstrips; ++s) {
+            if (!buf) continue;
+            float* gl[3] = {buf, buf + W, buf + 2 * W};
+            float* vs = buf + 3 * W;          /* vertical [1,2,1] sum, width W */
+            float* vd = buf + 4 * W;          /* vertical [-1,0,1] diff, width W */
+            float* sb = buf + 5 * W;
+            float *ix[3], *iy[3];
+            for (int k = 0; k < 3; ++k) { ix[k] = sb + k * Ws; iy[k] = sb + (3 + k) * Ws; }
+            float* vxx = sb + 6 * Ws;
+            float* vxy = sb + 7 * Ws;
+            float* vyy = sb + 8 * Ws;
+            const int64_t y0 = s * STRIP;
+            const int64_t y1 = (y0 + STRIP < n) ? y0 + STRIP : n;
+            for (int64_t r = y0; r < y1 + 4; ++r) {
+                const float* R = rgb + 0 * chan_stride + r * in_pitch;
+                const float* G = rgb + 1 * chan_stride + r * in_pitch;
+                const float* B = rgb + 2 * chan_stride + r * in_pitch;
+                gray_line_f32(gl[r % 3], R, G, B, W);
+                if (r >= y0 + 2) {
+                    const int64_t q = r - 2;
+                    const float* g0 = gl[q % 3];
+                    const float* g1 = gl[(q + 1) % 3];
+                    const float* g2 = gl[(q + 2) % 3];
+                    for (int64_t x = 0; x < W; ++x) {
+                        float t = 0.0f;
+                        t += 1.0f * g0[x]; t += 2.0f * g1[x]; t += 1.0f * g2[x];
+                        vs[x] = t;
+                        float u = 0.0f;
+                        u += -1.0f * g0[x]; u += 0.0f * g1[x]; u += 1.0f * g2[x];
+                        vd[x] = u;
+                    }
+                    float* px = ix[q % 3];
+                    float* py = iy[q % 3];
+                    for (int64_t x = 0; x < Ws; ++x) {
+                        float t = 0.0f;
+                        t = t + (-SA) * vs[x]; t = t + 0.0f * vs[x + 1]; t = t + SA * vs[x + 2];
+                        px[x] = t;
+                        float u = 0.0f;
+                        u = u + SA * vd[x]; u = u + SB * vd[x + 1]; u = u + SA * vd[x + 2];
+                        py[x] = u;
+                    }
+                }
+                if (r >= y0 + 4) {
+                    const int64_t y = r - 4;
+                    const float* a0 = ix[y % 3]; const float* a1 = ix[(y + 1) % 3]; const float* a2 = ix[(y + 2) % 3];
+                    const float* b0 = iy[y % 3]; const float* b1 = iy[(y + 1) % 3]; const float* b2 = iy[(y + 2) % 3];
+                    for (int64_t x = 0; x < Ws; ++x) {
+                        float t = 0.0f;
+                        t = t + a0[x] * a0[x]; t = t + a1[x] * a1[x]; t = t + a2[x] * a2[x];
+                        vxx[x] = t;
+                        float u = 0.0f;
+                        u = u + a0[x] * b0[x]; u = u + a1[x] * b1[x]; u = u + a2[x] * b2[x];
+                        vxy[x] = u;
+                        float v = 0.0f;
+                        v = v + b0[x] * b0[x]; v = v + b1[x] * b1[x]; v = v + b2[x] * b2[x];
+                        vyy[x] = v;
+                    }
+                    float* o = out + y * out_pitch;
+                    for (int64_t x = 0; x < m; ++x) {
+                        float sxy = 0.0f; sxy = sxy + vxy[x]; sxy = sxy + vxy[x + 1]; sxy = sxy + vxy[x + 2];
+                        float syy = 0.0f; syy = syy + vyy[x]; syy = syy + vyy[x + 1]; syy = syy + vyy[x + 2];
+                        float sxx = 0.0f; sxx = sxx + vxx[x]; sxx = sxx + vxx[x + 1]; sxx = sxx + vxx[x + 2];
+                        o[x] = sxx * syy - sxy * sxy - kappa * (sxx + syy) * (sxx + syy);
+                    }
+                }
+            }
+        }
+        free(buf);
+    }
+    return err;
+}
+
+int oracle_harris_f32_rrot_batched(float* out, int64_t n, int64_t m, const float* rgb,
+                                   int64_t batch, float kappa, int nthreads) {
+    const int64_t H = n + 4, W = m + 4;
+    for (int64_t b = 0; b < batch; ++b) {
+        int rc = oracle_harris_f32_rrot(out + b * n * m, m, n, m, rgb + b * 3 * H * W, W, H * W,
+                                        kappa, nthreads);
+        if (rc) return rc;
+    }
+    return 0;
+}
+
 /* batched f32 convenience for the CPU baseline: images are contiguous
  * 3 x H x W planes, outputs contiguous n x m. */
 int oracle_harris_f32_batched(float* out, int64_t n, int64_t m, const float* rgb,

@@ -15,6 +15,7 @@ The compute path is ``libharris_b200.so`` (``csrc/``, sm_100a only).  There is
 no CPU fallback: without the library or a B200 every entry point raises.
 """
 from ._lib import HarrisError, build  # noqa: F401
-from .harris import KAPPA, HarrisContext, algorithmic_bytes, context, harris, synth_  # noqa: F401
+from .harris import (GROUPINGS, KAPPA, HarrisContext, algorithmic_bytes, context, grouping_hbm_bytes,  # noqa: F401
+                     harris, harris_grouping, synth_)
 
 __version__ = "0.1.0"

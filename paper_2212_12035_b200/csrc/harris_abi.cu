@@ -86,11 +86,13 @@ int validate(const Call& c) {
     return HARRIS_OK;
 }
 
+// TMA needs a 16-byte aligned base and 16-byte multiple strides on the INPUT only;
+// the output side falls back to scalar stores when its rows are not 16-B aligned.
 bool tma_eligible(const Call& c) {
     const Geom& g = c.g;
-    if (!aligned16(g.rgb) || !aligned16(g.out)) return false;
-    if ((g.in_pitch | g.in_chan_stride | g.out_pitch) & 3) return false;
-    if (g.batch > 1 && ((g.in_image_stride | g.out_image_stride) & 3)) return false;
+    if (!aligned16(g.rgb)) return false;
+    if ((g.in_pitch | g.in_chan_stride) & 3) return false;
+    if (g.batch > 1 && (g.in_image_stride & 3)) return false;
     const int64_t kMaxStrideBytes = (int64_t(1) << 40) - 16;
     if (g.in_chan_stride * 4 > kMaxStrideBytes) return false;
     if (g.batch > 1 && g.in_image_stride * 4 > kMaxStrideBytes) return false;
@@ -154,6 +156,8 @@ void plan_launch(const harris_ctx* ctx, const Call& c, TileGeom& tg, int64_t& gr
     tg.out_image_stride = c.g.out_image_stride;
     tg.kappa = c.g.kappa;
     tg.l2_policy = ctx->l2_policy;
+    tg.vec_store = aligned16(c.g.out) && (c.g.out_pitch & 3) == 0 && (c.g.batch == 1 || (c.g.out_image_stride & 3) == 0);
+    tg.pad_ = 0;
 }
 
 int encode_tmap(harris_ctx* ctx, const Call& c, CUtensorMap* tmap) {
@@ -383,6 +387,35 @@ int harris_synth_fill(float* dst, int64_t planes, int64_t rows, int64_t W, int64
     cudaError_t e = launch_synth(dst, planes, rows, W, dst_pitch, dst_plane_stride, H_global, row0, plane0, seed,
                                  dist, sms, static_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? HARRIS_OK : HARRIS_ERR_CUDA;
+}
+
+int64_t harris_grouping_scratch_bytes(int grouping, int64_t n, int64_t m) {
+    if (n < 1 || m < 1) return -1;
+    const int64_t f = grouping_scratch_floats(grouping, n, m);
+    return f < 0 ? -1 : f * 4;
+}
+
+int harris_grouping_launches(int grouping) { return grouping_launches(grouping); }
+
+int harris_run_grouping(harris_ctx* ctx, int grouping, float* out, int64_t n, int64_t m, const float* rgb,
+                        void* scratch, int64_t scratch_bytes, float kappa, uint32_t flags, void* stream) {
+    if (!ctx || !out || !rgb) return HARRIS_ERR_INVALID_ARGUMENT;
+    if (n < 1 || m < 1) return HARRIS_ERR_SIZE;
+    if (grouping == HARRIS_GROUPING_FUSED) {
+        const int64_t W = m + 4, H = n + 4;
+        return run(ctx, make_call(out, m, n * m, n, m, rgb, W, H * W, 3 * H * W, 1, kappa, flags),
+                   static_cast<cudaStream_t>(stream));
+    }
+    const int64_t need = harris_grouping_scratch_bytes(grouping, n, m);
+    if (need < 0) return HARRIS_ERR_INVALID_ARGUMENT;
+    if (!scratch || scratch_bytes < need) return HARRIS_ERR_INVALID_ARGUMENT;
+    DeviceGuard guard(ctx->device);
+    if (!guard.ok) return cuda_fail(ctx, cudaGetLastError(), "cudaSetDevice");
+    cudaError_t e = launch_grouping(grouping, out, n, m, rgb, static_cast<float*>(scratch), kappa, ctx->num_sms,
+                                    static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "launch grouping");
+    ctx->last_path = HARRIS_PATH_NONE;
+    return HARRIS_OK;
 }
 
 // ------------------------------------------------------------- host buffers

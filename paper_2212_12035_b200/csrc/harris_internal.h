@@ -23,6 +23,8 @@ struct TileGeom {
     int32_t n, m;
     int32_t band_rows, bands, colsegs;
     int32_t l2_policy;  // 0 evict_first, 1 evict_normal (default), 2 evict_last
+    int32_t vec_store;  // 1: output rows 16-byte aligned -> float4 streaming stores
+    int32_t pad_;
     int64_t tiles;
     int64_t out_pitch, out_image_stride;
     float* out;
@@ -44,6 +46,11 @@ cudaError_t launch_tma(int cfg, bool exact, const CUtensorMap& tmap, const TileG
                        cudaStream_t stream);
 
 cudaError_t launch_generic(bool exact, const Geom& g, cudaStream_t stream);
+
+int64_t grouping_scratch_floats(int grouping, int64_t n, int64_t m);
+int grouping_launches(int grouping);
+cudaError_t launch_grouping(int grouping, float* out, int64_t n, int64_t m, const float* rgb, float* scratch,
+                            float kappa, int num_sms, cudaStream_t stream);
 
 cudaError_t launch_synth(float* dst, int64_t planes, int64_t rows, int64_t W, int64_t dst_pitch,
                          int64_t dst_plane_stride, int64_t H_global, int64_t row0, int64_t plane0,

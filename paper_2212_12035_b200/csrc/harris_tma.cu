@@ -263,9 +263,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
                 }
                 if (i >= 4 && i - 4 < rows_out && col_ok) {
                     float* po = orow + int64_t(i - 4) * g.out_pitch;
-                    if (col0 + kColsPerLane <= g.m) {
+                    if (g.vec_store && col0 + kColsPerLane <= g.m) {
                         stg128_cs(po, out4[0], out4[1], out4[2], out4[3]);
-                    } else {  // ragged right edge when m % 4 != 0 (padded input pitch)
+                    } else {  // unaligned output rows, or the ragged right edge when m % 4 != 0
 #pragma unroll
                         for (int k = 0; k < kColsPerLane; ++k)
                             if (col0 + k < g.m) po[k] = out4[k];

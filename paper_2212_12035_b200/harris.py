@@ -188,6 +188,54 @@ def harris(rgb, kappa: float = KAPPA, *, out: Optional[torch.Tensor] = None, exa
     return out
 
 
+GROUPINGS = {
+    1: "[Sx],[Sy],[x],[+],[coarsity]",
+    2: "[Sx,Sy,x],[+,coarsity]",
+    3: "[Sx,Sy],[x,+,coarsity]",
+    4: "[Sx,Sy,x,+,coarsity]",
+}
+
+
+def grouping_hbm_bytes(grouping: int, n: int, m: int) -> int:
+    """Compulsory HBM bytes of one image under a kernel grouping (each group reads its
+    inputs once and writes its outputs once; stencil halos ignored)."""
+    H, W, s, o = n + 4, m + 4, (n + 2) * (m + 2), n * m
+    rgb = 12 * H * W
+    return {
+        1: (rgb + 4 * s) + (rgb + 4 * s) + (8 * s + 12 * s) + (12 * s + 12 * o) + (12 * o + 4 * o),
+        2: (rgb + 12 * s) + (12 * s + 4 * o),
+        3: (rgb + 8 * s) + (8 * s + 4 * o),
+        4: rgb + 4 * o,
+    }[grouping]
+
+
+def harris_grouping(rgb: torch.Tensor, grouping: int, kappa: float = KAPPA, *, out: Optional[torch.Tensor] = None,
+                    scratch: Optional[torch.Tensor] = None, exact: bool = False) -> torch.Tensor:
+    """The thesis's kernel-grouping design space on one contiguous
+    (3, H, W) CUDA image; groupings 1-3 round-trip intermediates through HBM scratch."""
+    B, H, W = _check_rgb(rgb)
+    if rgb.dim() != 3 or not rgb.is_cuda or not rgb.is_contiguous():
+        raise ValueError("harris_grouping takes one contiguous (3, H, W) CUDA image")
+    n, m = H - 4, W - 4
+    L = lib()
+    need = int(L.harris_grouping_scratch_bytes(grouping, n, m))
+    if need < 0:
+        raise ValueError(f"unknown grouping {grouping}")
+    if scratch is None and need > 0:
+        scratch = torch.empty(need // 4, dtype=torch.float32, device=rgb.device)
+    if out is None:
+        out = torch.empty((n, m), dtype=torch.float32, device=rgb.device)
+    dev = rgb.device.index
+    ctx = context(dev)
+    st = torch.cuda.current_stream(dev).cuda_stream
+    rc = L.harris_run_grouping(ctx.handle, grouping, out.data_ptr(), n, m, rgb.data_ptr(),
+                               scratch.data_ptr() if scratch is not None else None,
+                               scratch.numel() * 4 if scratch is not None else 0, kappa,
+                               FLAG_EXACT_ORDER if exact else 0, st)
+    check(rc, "harris_run_grouping", ctx.handle)
+    return out
+
+
 def synth_(dst: torch.Tensor, seed: int, dist: int = 0, *, H_global: Optional[int] = None, row0: int = 0,
            plane0: int = 0, stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
     """Fill ``dst`` (planes, rows, W) float32 CUDA, unit column stride, with the
@@ -209,4 +257,5 @@ def algorithmic_bytes(n: int, m: int, batch: int = 1) -> int:
     return batch * (12 * (n + 4) * (m + 4) + 4 * n * m)
 
 
-__all__ = ["HarrisContext", "context", "harris", "synth_", "algorithmic_bytes", "KAPPA", "_lib"]
+__all__ = ["HarrisContext", "context", "harris", "harris_grouping", "grouping_hbm_bytes", "GROUPINGS", "synth_",
+           "algorithmic_bytes", "KAPPA", "_lib"]

@@ -220,3 +220,27 @@ def test_plan_geometry(cuda_ctx):
     assert info["col_segments"] == 64
     assert info["bands"] * info["band_rows"] >= 8188
     assert info["grid_ctas"] % cuda_ctx.num_sms == 0 or info["grid_ctas"] * info["warps_per_cta"] >= info["tiles"]
+
+
+@pytest.mark.parametrize("grouping", [1, 2, 3, 4])
+@pytest.mark.parametrize("H,W", [(5, 5), (13, 17), (70, 261), (300, 1028)])
+def test_kernel_groupings_bitexact(cuda_ctx, grouping, H, W):
+    """The thesis's four kernel groupings: different HBM traffic,
+    identical results (Appendix-B order everywhere)."""
+    rgb = synth.synth_numpy(3, H, W, seed=H * 31 + W)
+    got = hb.harris_grouping(_dev(rgb), grouping, exact=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(got.cpu().numpy(), cref.harris_f32(rgb))
+
+
+def test_grouping_scratch_contract(cuda_ctx):
+    L = _lib.lib()
+    assert L.harris_grouping_scratch_bytes(4, 10, 10) == 0
+    assert L.harris_grouping_scratch_bytes(9, 10, 10) == -1
+    assert L.harris_grouping_launches(1) == 5
+    rgb = _dev(synth.synth_numpy(3, 20, 20, seed=1))
+    out = torch.empty((16, 16), device="cuda")
+    small = torch.empty(8, device="cuda")
+    rc = L.harris_run_grouping(cuda_ctx.handle, 1, out.data_ptr(), 16, 16, rgb.data_ptr(), small.data_ptr(), 32,
+                               0.04, 0, None)
+    assert rc == _lib.HARRIS_ERR_INVALID_ARGUMENT
