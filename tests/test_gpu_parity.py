@@ -163,7 +163,8 @@ def test_thesis_output_pitch(cuda_ctx):
 
 
 def test_padded_pitch_ragged_width(cuda_ctx):
-    """Input rows padded to a 16-byte pitch with m % 4 != 0 still take the TMA path."""
+    """Input rows padded to a 16-byte pitch with m % 4 != 0 still take the TMA path
+    (unaligned output rows use scalar stores)."""
     H, W = 50, 139
     base = synth.synth_numpy(3, H, W, seed=4)
     padded = torch.zeros((3, H, 144), device="cuda")
@@ -172,6 +173,13 @@ def test_padded_pitch_ragged_width(cuda_ctx):
     assert cuda_ctx.last_path == _lib.PATH_TMA
     torch.cuda.synchronize()
     assert np.array_equal(got.cpu().numpy(), cref.harris_f32(base))
+    # misaligned output base (1 float offset) with aligned input: still TMA, scalar stores
+    buf = torch.zeros((H - 4) * (W - 4) + 1, device="cuda")
+    out = buf[1:].view(H - 4, W - 4)
+    hb.harris(padded[:, :, :W], out=out, exact=True)
+    assert cuda_ctx.last_path == _lib.PATH_TMA
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), cref.harris_f32(base))
 
 
 def test_host_path_matches_device(cuda_ctx):
