@@ -104,6 +104,21 @@ HARRIS_API int harris_run_strided(harris_ctx* ctx, float* out, int64_t out_pitch
 HARRIS_API int harris_run_host(harris_ctx* ctx, float* out_host, int64_t out_pitch, int64_t n, int64_t m,
                     const float* rgb_host, int64_t batch, float kappa, uint32_t flags);
 
+/* Interleaved 8-bit RGB input (HWC, e.g. a decoded rgb.png):
+ * byte (b, y, x, c) at rgb8[b*in_image_stride_bytes + y*in_pitch_bytes + 3*x + c],
+ * value = byte / 255.0f.  The conversion is fused into the kernel's load stage
+ * (3 B per input pixel from HBM instead of 12); results equal harris_run_strided on the
+ * planar f32 image byte/255 (bit-for-bit with HARRIS_FLAG_EXACT_ORDER).  TMA path when
+ * the base and byte strides are 16-byte aligned, generic GPU kernel otherwise. */
+HARRIS_API int harris_run_u8(harris_ctx* ctx, float* out, int64_t out_pitch, int64_t out_image_stride,
+                             int64_t n, int64_t m, const uint8_t* rgb8, int64_t in_pitch_bytes,
+                             int64_t in_image_stride_bytes, int64_t batch, float kappa, uint32_t flags,
+                             void* cuda_stream);
+
+/* host-buffer form of harris_run_u8: rgb8_host batch x (n+4) x (m+4) x 3 contiguous */
+HARRIS_API int harris_run_host_u8(harris_ctx* ctx, float* out_host, int64_t out_pitch, int64_t n, int64_t m,
+                                  const uint8_t* rgb8_host, int64_t batch, float kappa, uint32_t flags);
+
 /* Device synthetic-image generator used by the bench (bit-identical to
  * oracle_synth_fill): dst (p, y, x) at dst[p*dst_plane_stride + y*dst_pitch + x] =
  * value of global plane plane0+p, row row0+y of a planes x H_global x W stack.

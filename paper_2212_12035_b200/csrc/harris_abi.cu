@@ -29,6 +29,8 @@ struct harris_ctx {
     int num_sms = 0;
     int cc_major = 0, cc_minor = 0;
     int tma_cfg = 0;
+    int u8_cfg = 0;
+    int occ_u8[kNumU8Configs] = {0};
     int l2_policy = 1;  // evict_normal: the 4-column halo sectors are re-read by the neighbouring strip
     int64_t force_band_rows = 0;  // dev knob (HARRIS_BAND_ROWS): override the planner
     int occ[kNumTmaConfigs] = {0};
@@ -66,9 +68,12 @@ int cuda_fail(harris_ctx* ctx, cudaError_t e, const char* where) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+enum Format { kF32Planar = 0, kU8Interleaved = 1 };
+
 struct Call {
     Geom g;
     uint32_t flags;
+    int fmt = kF32Planar;  // u8: g.rgb is the byte base, in_pitch / in_image_stride are bytes
 };
 
 int validate(const Call& c) {
@@ -77,7 +82,14 @@ int validate(const Call& c) {
     if (g.n < 1 || g.m < 1) return HARRIS_ERR_SIZE;  // input must be at least 5 x 5
     if (g.n + 4 > INT32_MAX || g.m + 4 > INT32_MAX) return HARRIS_ERR_SIZE;
     if (g.batch < 1) return HARRIS_ERR_INVALID_ARGUMENT;
-    if (g.in_pitch < g.m + 4 || g.out_pitch < g.m) return HARRIS_ERR_INVALID_ARGUMENT;
+    if (g.out_pitch < g.m) return HARRIS_ERR_INVALID_ARGUMENT;
+    if (g.batch > 1 && g.out_image_stride < g.n * g.out_pitch) return HARRIS_ERR_INVALID_ARGUMENT;
+    if (c.fmt == kU8Interleaved) {
+        if (g.in_pitch < 3 * (g.m + 4)) return HARRIS_ERR_INVALID_ARGUMENT;
+        if (g.batch > 1 && g.in_image_stride < (g.n + 4) * g.in_pitch) return HARRIS_ERR_INVALID_ARGUMENT;
+        return HARRIS_OK;
+    }
+    if (g.in_pitch < g.m + 4) return HARRIS_ERR_INVALID_ARGUMENT;
     if (g.in_chan_stride < (g.n + 4) * g.in_pitch) return HARRIS_ERR_INVALID_ARGUMENT;
     if (g.batch > 1) {
         if (g.in_image_stride < 3 * g.in_chan_stride) return HARRIS_ERR_INVALID_ARGUMENT;
@@ -91,6 +103,11 @@ int validate(const Call& c) {
 bool tma_eligible(const Call& c) {
     const Geom& g = c.g;
     if (!aligned16(g.rgb)) return false;
+    if (c.fmt == kU8Interleaved) {  // byte strides, tensor map over 32-bit words
+        if ((g.in_pitch & 15) || (g.batch > 1 && (g.in_image_stride & 15))) return false;
+        if (g.batch > INT32_MAX) return false;
+        return true;
+    }
     if ((g.in_pitch | g.in_chan_stride) & 3) return false;
     if (g.batch > 1 && (g.in_image_stride & 3)) return false;
     const int64_t kMaxStrideBytes = (int64_t(1) << 40) - 16;
@@ -146,8 +163,9 @@ int choose_path(const Call& c) {
 }
 
 void plan_launch(const harris_ctx* ctx, const Call& c, TileGeom& tg, int64_t& grid) {
-    const TmaConfig& cfg = kTmaConfigs[ctx->tma_cfg];
-    const int occ = std::max(1, ctx->occ[ctx->tma_cfg]);
+    const bool u8 = c.fmt == kU8Interleaved;
+    const TmaConfig& cfg = u8 ? kU8Configs[ctx->u8_cfg] : kTmaConfigs[ctx->tma_cfg];
+    const int occ = std::max(1, u8 ? ctx->occ_u8[ctx->u8_cfg] : ctx->occ[ctx->tma_cfg]);
     const int64_t resident_ctas = int64_t(ctx->num_sms) * occ;
     plan_tiles(c.g.n, c.g.m, c.g.batch, resident_ctas * cfg.warps, cfg.rows, ctx->force_band_rows, tg);
     grid = std::min<int64_t>((tg.tiles + cfg.warps - 1) / cfg.warps, resident_ctas);
@@ -160,7 +178,27 @@ void plan_launch(const harris_ctx* ctx, const Call& c, TileGeom& tg, int64_t& gr
     tg.pad_ = 0;
 }
 
+int encode_tmap_u8(harris_ctx* ctx, const Call& c, CUtensorMap* tmap) {
+    const Geom& g = c.g;
+    const TmaConfig& cfg = kU8Configs[ctx->u8_cfg];
+    cuuint64_t dims[3] = {cuuint64_t((3 * (g.m + 4) + 3) / 4), cuuint64_t(g.n + 4), cuuint64_t(g.batch)};
+    const int64_t img_stride = g.batch > 1 ? g.in_image_stride : (g.n + 4) * g.in_pitch;
+    cuuint64_t strides[2] = {cuuint64_t(g.in_pitch), cuuint64_t((img_stride + 15) / 16 * 16)};
+    cuuint32_t box[3] = {cuuint32_t(kU8BoxWords), cuuint32_t(cfg.rows), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = ctx->encode(tmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<float*>(g.rgb), dims, strides, box,
+                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        std::snprintf(ctx->last_err, sizeof(ctx->last_err), "cuTensorMapEncodeTiled (u8) failed (CUresult %d)",
+                      int(r));
+        return HARRIS_ERR_TMA;
+    }
+    return HARRIS_OK;
+}
+
 int encode_tmap(harris_ctx* ctx, const Call& c, CUtensorMap* tmap) {
+    if (c.fmt == kU8Interleaved) return encode_tmap_u8(ctx, c, tmap);
     const Geom& g = c.g;
     const TmaConfig& cfg = kTmaConfigs[ctx->tma_cfg];
     cuuint64_t dims[4] = {cuuint64_t(g.m + 4), cuuint64_t(g.n + 4), 3, cuuint64_t(g.batch)};
@@ -196,9 +234,10 @@ int run(harris_ctx* ctx, const Call& c, cudaStream_t stream) {
         TileGeom tg;
         int64_t grid = 0;
         plan_launch(ctx, c, tg, grid);
-        e = launch_tma(ctx->tma_cfg, exact, tmap, tg, grid, stream);
+        e = c.fmt == kU8Interleaved ? launch_tma_u8(ctx->u8_cfg, exact, tmap, tg, grid, stream)
+                                    : launch_tma(ctx->tma_cfg, exact, tmap, tg, grid, stream);
     } else {
-        e = launch_generic(exact, c.g, stream);
+        e = c.fmt == kU8Interleaved ? launch_generic_u8(exact, c.g, stream) : launch_generic(exact, c.g, stream);
     }
     if (e != cudaSuccess) return cuda_fail(ctx, e, path == HARRIS_PATH_TMA ? "launch tma" : "launch generic");
     ctx->last_path = path;
@@ -277,6 +316,11 @@ int harris_init(harris_ctx** out_ctx, int cuda_device) {
         int v = std::atoi(env);
         if (v >= 0 && v < kNumTmaConfigs) ctx->tma_cfg = v;
     }
+    env = std::getenv("HARRIS_U8_CONFIG");
+    if (env) {
+        int v = std::atoi(env);
+        if (v >= 0 && v < kNumU8Configs) ctx->u8_cfg = v;
+    }
     env = std::getenv("HARRIS_BAND_ROWS");
     if (env) ctx->force_band_rows = std::atoll(env);
     env = std::getenv("HARRIS_L2_POLICY");
@@ -298,6 +342,15 @@ int harris_init(harris_ctx** out_ctx, int cuda_device) {
         if (e == cudaSuccess) e = tma_occupancy(k, &ctx->occ[k]);
         if (e != cudaSuccess) {
             int rc = cuda_fail(ctx, e, "configure tma kernel");
+            delete ctx;
+            return rc;
+        }
+    }
+    for (int k = 0; k < kNumU8Configs; ++k) {
+        e = u8_configure(k);
+        if (e == cudaSuccess) e = u8_occupancy(k, &ctx->occ_u8[k]);
+        if (e != cudaSuccess) {
+            int rc = cuda_fail(ctx, e, "configure u8 tma kernel");
             delete ctx;
             return rc;
         }
@@ -343,6 +396,16 @@ int harris_run_strided(harris_ctx* ctx, float* out, int64_t out_pitch, int64_t o
                make_call(out, out_pitch, out_image_stride, n, m, rgb, in_pitch, in_chan_stride, in_image_stride,
                          batch, kappa, flags),
                static_cast<cudaStream_t>(stream));
+}
+
+int harris_run_u8(harris_ctx* ctx, float* out, int64_t out_pitch, int64_t out_image_stride, int64_t n, int64_t m,
+                  const uint8_t* rgb8, int64_t in_pitch_bytes, int64_t in_image_stride_bytes, int64_t batch,
+                  float kappa, uint32_t flags, void* stream) {
+    Call c = make_call(out, out_pitch, out_image_stride, n, m, reinterpret_cast<const float*>(rgb8), in_pitch_bytes,
+                       0, in_image_stride_bytes, batch, kappa, flags);
+    c.fmt = kU8Interleaved;
+    if (!rgb8) return HARRIS_ERR_INVALID_ARGUMENT;
+    return run(ctx, c, static_cast<cudaStream_t>(stream));
 }
 
 int harris_plan(harris_ctx* ctx, int64_t n, int64_t m, int64_t batch, const float* rgb, int64_t in_pitch,
@@ -454,61 +517,87 @@ static int ensure_staging(harris_ctx* ctx, size_t in_bytes, size_t out_bytes) {
     return HARRIS_OK;
 }
 
-int harris_run_host(harris_ctx* ctx, float* out_host, int64_t out_pitch, int64_t n, int64_t m,
-                    const float* rgb_host, int64_t batch, float kappa, uint32_t flags) {
-    if (!ctx || !out_host || !rgb_host) return HARRIS_ERR_INVALID_ARGUMENT;
+static int run_host_impl(harris_ctx* ctx, int fmt, float* out_host, int64_t out_pitch, int64_t n, int64_t m,
+                         const void* in_host, int64_t batch, float kappa, uint32_t flags) {
+    if (!ctx || !out_host || !in_host) return HARRIS_ERR_INVALID_ARGUMENT;
     if (n < 1 || m < 1) return HARRIS_ERR_SIZE;
     if (batch < 1 || out_pitch < m) return HARRIS_ERR_INVALID_ARGUMENT;
     DeviceGuard guard(ctx->device);
     if (!guard.ok) return cuda_fail(ctx, cudaGetLastError(), "cudaSetDevice");
+    const bool u8 = fmt == kU8Interleaved;
     const int64_t H = n + 4, W = m + 4;
-    const int64_t img_in = 3 * H * W;
+    // bytes of one input row of all channels, and of one image
+    const int64_t row_bytes = u8 ? 3 * W : 3 * W * 4;
+    const int64_t img_bytes = H * row_bytes;
     const int64_t kChunkBytes = int64_t(48) << 20;  // input bytes per pipeline chunk
     // chunk = a group of whole images, or (batch == 1 and large) a row band + 4-row halo
-    const bool banded = batch == 1 && img_in * 4 > kChunkBytes;
-    const int64_t imgs_per_chunk = banded ? 1 : std::max<int64_t>(1, kChunkBytes / (img_in * 4));
-    const int64_t band_rows = banded ? std::max<int64_t>(1, kChunkBytes / (3 * W * 4) - 4) : n;
-    const size_t in_bytes = size_t(banded ? 3 * (band_rows + 4) * W : imgs_per_chunk * img_in) * 4;
+    const bool banded = batch == 1 && img_bytes > kChunkBytes;
+    const int64_t imgs_per_chunk = banded ? 1 : std::max<int64_t>(1, kChunkBytes / img_bytes);
+    const int64_t band_rows = banded ? std::max<int64_t>(1, kChunkBytes / row_bytes - 4) : n;
+    const size_t in_bytes = size_t(banded ? (band_rows + 4) * row_bytes : imgs_per_chunk * img_bytes);
     const size_t out_bytes = size_t(banded ? band_rows * m : imgs_per_chunk * n * m) * 4;
     int rc = ensure_staging(ctx, in_bytes, out_bytes);
     if (rc) return rc;
     const int64_t nchunks = banded ? (n + band_rows - 1) / band_rows : (batch + imgs_per_chunk - 1) / imgs_per_chunk;
+    const unsigned char* src = static_cast<const unsigned char*>(in_host);
     cudaError_t e = cudaSuccess;
     for (int64_t k = 0; k < nchunks && rc == HARRIS_OK; ++k) {
         const int slot = int(k % harris_ctx::kSlots);
         cudaStream_t s = ctx->streams[slot];
-        float* din = ctx->d_in[slot];
+        unsigned char* din = reinterpret_cast<unsigned char*>(ctx->d_in[slot]);
         float* dout = ctx->d_out[slot];
+        int64_t rows = n, nb = 1, r0 = 0, b0 = 0;
+        Call c;
         if (banded) {
-            const int64_t r0 = k * band_rows;
-            const int64_t rows = std::min(band_rows, n - r0);
+            r0 = k * band_rows;
+            rows = std::min(band_rows, n - r0);
             const int64_t rin = rows + 4;
-            for (int c = 0; c < 3 && e == cudaSuccess; ++c)
-                e = cudaMemcpyAsync(din + c * rin * W, rgb_host + c * H * W + r0 * W, size_t(rin * W) * 4,
-                                    cudaMemcpyHostToDevice, s);
+            if (u8) {  // HWC: the band is one contiguous run of rows
+                e = cudaMemcpyAsync(din, src + r0 * 3 * W, size_t(rin * 3 * W), cudaMemcpyHostToDevice, s);
+                c = make_call(dout, m, rows * m, rows, m, reinterpret_cast<const float*>(din), 3 * W, 0,
+                              rin * 3 * W, 1, kappa, flags);
+            } else {   // planar: one run per channel
+                for (int ch = 0; ch < 3 && e == cudaSuccess; ++ch)
+                    e = cudaMemcpyAsync(din + size_t(ch * rin * W) * 4, src + size_t(ch * H * W + r0 * W) * 4,
+                                        size_t(rin * W) * 4, cudaMemcpyHostToDevice, s);
+                c = make_call(dout, m, rows * m, rows, m, reinterpret_cast<const float*>(din), W, rin * W,
+                              3 * rin * W, 1, kappa, flags);
+            }
             if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D band");
-            rc = run(ctx, make_call(dout, m, rows * m, rows, m, din, W, rin * W, 3 * rin * W, 1, kappa, flags), s);
-            if (rc) break;
-            e = cudaMemcpy2DAsync(out_host + r0 * out_pitch, size_t(out_pitch) * 4, dout, size_t(m) * 4,
-                                  size_t(m) * 4, size_t(rows), cudaMemcpyDeviceToHost, s);
-            if (e != cudaSuccess) return cuda_fail(ctx, e, "D2H band");
         } else {
-            const int64_t b0 = k * imgs_per_chunk;
-            const int64_t nb = std::min(imgs_per_chunk, batch - b0);
-            e = cudaMemcpyAsync(din, rgb_host + b0 * img_in, size_t(nb * img_in) * 4, cudaMemcpyHostToDevice, s);
+            b0 = k * imgs_per_chunk;
+            nb = std::min(imgs_per_chunk, batch - b0);
+            e = cudaMemcpyAsync(din, src + size_t(b0 * img_bytes), size_t(nb * img_bytes), cudaMemcpyHostToDevice,
+                                s);
             if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D images");
-            rc = run(ctx, make_call(dout, m, n * m, n, m, din, W, H * W, img_in, nb, kappa, flags), s);
-            if (rc) break;
-            e = cudaMemcpy2DAsync(out_host + b0 * n * out_pitch, size_t(out_pitch) * 4, dout, size_t(m) * 4,
-                                  size_t(m) * 4, size_t(nb * n), cudaMemcpyDeviceToHost, s);
-            if (e != cudaSuccess) return cuda_fail(ctx, e, "D2H images");
+            c = u8 ? make_call(dout, m, n * m, n, m, reinterpret_cast<const float*>(din), 3 * W, 0, img_bytes, nb,
+                               kappa, flags)
+                   : make_call(dout, m, n * m, n, m, reinterpret_cast<const float*>(din), W, H * W, 3 * H * W, nb,
+                               kappa, flags);
         }
+        c.fmt = fmt;
+        rc = run(ctx, c, s);
+        if (rc) break;
+        e = cudaMemcpy2DAsync(out_host + (banded ? r0 : b0 * n) * out_pitch, size_t(out_pitch) * 4, dout,
+                              size_t(m) * 4, size_t(m) * 4, size_t(banded ? rows : nb * n), cudaMemcpyDeviceToHost,
+                              s);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "D2H");
     }
     for (int k = 0; k < harris_ctx::kSlots; ++k) {
         cudaError_t se = cudaStreamSynchronize(ctx->streams[k]);
         if (se != cudaSuccess && rc == HARRIS_OK) rc = cuda_fail(ctx, se, "pipeline sync");
     }
     return rc;
+}
+
+int harris_run_host(harris_ctx* ctx, float* out_host, int64_t out_pitch, int64_t n, int64_t m,
+                    const float* rgb_host, int64_t batch, float kappa, uint32_t flags) {
+    return run_host_impl(ctx, kF32Planar, out_host, out_pitch, n, m, rgb_host, batch, kappa, flags);
+}
+
+int harris_run_host_u8(harris_ctx* ctx, float* out_host, int64_t out_pitch, int64_t n, int64_t m,
+                       const uint8_t* rgb8_host, int64_t batch, float kappa, uint32_t flags) {
+    return run_host_impl(ctx, kU8Interleaved, out_host, out_pitch, n, m, rgb8_host, batch, kappa, flags);
 }
 
 }  // extern "C"

@@ -28,6 +28,7 @@ constexpr int kLanes = 32;
 constexpr int kColsPerLane = 4;                     // one float4 per lane
 constexpr int kWarpCols = kLanes * kColsPerLane;    // 128 output columns per warp strip
 constexpr int kBoxCols = kWarpCols + 4;             // + 4-column halo = 132 input columns
+constexpr int kU8BoxWords = 100;  // u8 HWC box: 400 bytes >= 132 px * 3 B (TMA inner box: 16-B multiple)
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -69,6 +70,16 @@ __device__ __forceinline__ void tma_load_4d(void* smem_dst, const void* tmap, ui
         " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_u32(smem_dst)),
         "l"(reinterpret_cast<uint64_t>(tmap)), "r"(x), "r"(y), "r"(c), "r"(b), "r"(smem_u32(bar)),
         "l"(policy)
+        : "memory");
+}
+
+// 3-D TMA tile load (x = inner element, y = row, z = image).
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const void* tmap, uint64_t* bar, int x, int y, int z,
+                                            uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
 

@@ -21,7 +21,9 @@ constexpr int kGG = kGT + 4;     // gray tile edge
 constexpr int kGS = kGT + 2;     // Sobel / product tile edge
 constexpr int kGThreadsX = 32, kGThreadsY = 8;
 
-template <bool EXACT>
+// U8: interleaved RGB bytes (HWC), value/255; Geom.rgb is the byte base pointer and
+// in_pitch / in_image_stride are byte strides.
+template <bool EXACT, bool U8>
 __global__ void __launch_bounds__(kGThreadsX* kGThreadsY)
     harris_generic_kernel(const Geom g, int tiles_x, int tiles_y) {
     __shared__ float gs[kGG][kGG + 1];
@@ -36,7 +38,8 @@ __global__ void __launch_bounds__(kGThreadsX* kGThreadsY)
     const float WY[9] = {-kSobA, -kSobB, -kSobA, 0.f, 0.f, 0.f, kSobA, kSobB, kSobA};
 
     for (int64_t b = blockIdx.z; b < g.batch; b += gridDim.z) {
-        const float* img = g.rgb + b * g.in_image_stride;
+        const float* img = U8 ? g.rgb : g.rgb + b * g.in_image_stride;
+        const uint8_t* img8 = reinterpret_cast<const uint8_t*>(g.rgb) + (U8 ? b * g.in_image_stride : 0);
         float* out = g.out + b * g.out_image_stride;
         for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
             const int64_t y0 = (t / tiles_x) * kGT, x0 = (t % tiles_x) * kGT;
@@ -46,8 +49,18 @@ __global__ void __launch_bounds__(kGThreadsX* kGThreadsY)
                 const int64_t y = y0 + yy, x = x0 + xx;
                 float v = 0.f;
                 if (y < H && x < W) {
-                    const float* p = img + y * g.in_pitch + x;
-                    const float r = __ldg(p), gr = __ldg(p + g.in_chan_stride), bl = __ldg(p + 2 * g.in_chan_stride);
+                    float r, gr, bl;
+                    if (U8) {
+                        const uint8_t* p = img8 + y * g.in_pitch + 3 * x;
+                        r = __fdiv_rn(float(__ldg(p)), 255.0f);
+                        gr = __fdiv_rn(float(__ldg(p + 1)), 255.0f);
+                        bl = __fdiv_rn(float(__ldg(p + 2)), 255.0f);
+                    } else {
+                        const float* p = img + y * g.in_pitch + x;
+                        r = __ldg(p);
+                        gr = __ldg(p + g.in_chan_stride);
+                        bl = __ldg(p + 2 * g.in_chan_stride);
+                    }
                     v = EXACT ? gray_exact(r, gr, bl) : fmaf(kGrayB, bl, fmaf(kGrayG, gr, kGrayR * r));
                 }
                 gs[yy][xx] = v;
@@ -104,7 +117,8 @@ __global__ void __launch_bounds__(kGThreadsX* kGThreadsY)
     }
 }
 
-cudaError_t launch_generic(bool exact, const Geom& g, cudaStream_t stream) {
+template <bool U8>
+static cudaError_t launch_generic_t(bool exact, const Geom& g, cudaStream_t stream) {
     const int tiles_x = int((g.m + kGT - 1) / kGT), tiles_y = int((g.n + kGT - 1) / kGT);
     const int64_t tiles = int64_t(tiles_x) * tiles_y;
     const dim3 block{kGThreadsX, kGThreadsY, 1};
@@ -112,10 +126,18 @@ cudaError_t launch_generic(bool exact, const Geom& g, cudaStream_t stream) {
     const unsigned gz = unsigned(g.batch < 65535 ? g.batch : 65535);
     const dim3 grid{gx, 1, gz};
     if (exact)
-        harris_generic_kernel<true><<<grid, block, 0, stream>>>(g, tiles_x, tiles_y);
+        harris_generic_kernel<true, U8><<<grid, block, 0, stream>>>(g, tiles_x, tiles_y);
     else
-        harris_generic_kernel<false><<<grid, block, 0, stream>>>(g, tiles_x, tiles_y);
+        harris_generic_kernel<false, U8><<<grid, block, 0, stream>>>(g, tiles_x, tiles_y);
     return cudaGetLastError();
+}
+
+cudaError_t launch_generic(bool exact, const Geom& g, cudaStream_t stream) {
+    return launch_generic_t<false>(exact, g, stream);
+}
+
+cudaError_t launch_generic_u8(bool exact, const Geom& g, cudaStream_t stream) {
+    return launch_generic_t<true>(exact, g, stream);
 }
 
 }  // namespace harris

@@ -47,6 +47,17 @@ cudaError_t launch_tma(int cfg, bool exact, const CUtensorMap& tmap, const TileG
 
 cudaError_t launch_generic(bool exact, const Geom& g, cudaStream_t stream);
 
+// interleaved RGB u8 (HWC) input: TMA configs + generic fallback (Geom.rgb is then the
+// byte base pointer; in_pitch / in_image_stride are in BYTES, in_chan_stride unused)
+constexpr int kNumU8Configs = 3;
+extern const TmaConfig kU8Configs[kNumU8Configs];
+size_t u8_smem_bytes(int cfg);
+cudaError_t u8_configure(int cfg);
+cudaError_t u8_occupancy(int cfg, int* ctas_per_sm);
+cudaError_t launch_tma_u8(int cfg, bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid,
+                          cudaStream_t stream);
+cudaError_t launch_generic_u8(bool exact, const Geom& g, cudaStream_t stream);
+
 int64_t grouping_scratch_floats(int grouping, int64_t n, int64_t m);
 int grouping_launches(int grouping);
 cudaError_t launch_grouping(int grouping, float* out, int64_t n, int64_t m, const float* rgb, float* scratch,

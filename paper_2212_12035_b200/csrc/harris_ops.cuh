@@ -1,0 +1,234 @@
+// harris_ops.cuh — the Harris stencil as strip-pipeline ops (strip_pipeline.cuh).
+//
+// HarrisCore<EXACT> is the per-row register machine shared by every input
+// format: given this lane's 4 gray values of input row i (and, for lane 31, the
+// 4 gray values of the box's right halo), it updates the rolling 3-row windows
+// and produces the 4 coarsity outputs of row i-4.
+//   FAST : separable Sobel (horizontal diff / smooth, then vertical), box sums as
+//          horizontal shared-pair 3-sums then vertical 3-sums, FMAs, gray already
+//          scaled by 1/12 (cbuf+rrot order).
+//   EXACT: Appendix-B 9-tap row-major accumulations, never contracted (bit-exact
+//          with oracle/harris_oracle.c).
+// Slot s2 = R%3 holds row i, s0 = (R+1)%3 row i-2, s1 = (R+2)%3 row i-1.
+//
+// Input-format ops supply gray:
+//   HarrisF32Op : planar RGB f32, 4-D TMA box {132 cols, CH rows, 3 channels, 1 image}
+//   HarrisU8Op  : interleaved RGB u8 (HWC, value/255), 3-D TMA box over 32-bit words
+//                 {100 words = 400 bytes >= 132 px * 3, CH rows, 1 image}; the byte->float
+//                 conversion is fused into the row step.
+#pragma once
+#include <cuda.h>
+
+#include <cstdint>
+
+#include "harris_common.cuh"
+
+namespace harris {
+
+__device__ __forceinline__ void hsum4(const float (&p)[6], float& o0, float& o1, float& o2, float& o3) {
+    const float q1 = p[1] + p[2], q3 = p[3] + p[4];
+    o0 = p[0] + q1;
+    o1 = q1 + p[3];
+    o2 = p[2] + q3;
+    o3 = q3 + p[5];
+}
+
+template <bool EXACT>
+struct HarrisCore {
+    float kappa;
+    // FAST state: horizontal Sobel partials (6 cols) and product 3-sums (3 x 4 cols)
+    float D[3][6], Hs[3][6], HB[3][12];
+    // EXACT state: gray rows (8 cols) and product rows (3 x 6 cols)
+    float G3[3][8], P[3][18];
+
+    __device__ __forceinline__ explicit HarrisCore(float k) : kappa(k) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+#pragma unroll
+            for (int k2 = 0; k2 < 6; ++k2) D[a][k2] = Hs[a][k2] = 0.f;
+#pragma unroll
+            for (int k2 = 0; k2 < 12; ++k2) HB[a][k2] = 0.f;
+#pragma unroll
+            for (int k2 = 0; k2 < 8; ++k2) G3[a][k2] = 0.f;
+#pragma unroll
+            for (int k2 = 0; k2 < 18; ++k2) P[a][k2] = 0.f;
+        }
+    }
+
+    // gown: this lane's 4 gray values; halo(h0..h3) fills the right halo (lane 31 only)
+    template <int R, class HaloFn>
+    __device__ __forceinline__ void step(const float (&gown)[4], int lane, HaloFn&& halo, float (&out)[4]) {
+        constexpr int s2 = R % 3, s0 = (R + 1) % 3, s1 = (R + 2) % 3;
+        if constexpr (!EXACT) {
+            float gr[8];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) gr[k] = gown[k];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) gr[4 + k] = __shfl_down_sync(0xffffffffu, gr[k], 1);
+            if (lane == 31) halo(gr[4], gr[5], gr[6], gr[7]);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+                D[s2][k] = gr[k + 2] - gr[k];
+                Hs[s2][k] = fmaf(2.f, gr[k + 1], gr[k]) + gr[k + 2];
+            }
+            float pxx[6], pxy[6], pyy[6];
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+                const float ix = fmaf(2.f, D[s1][k], D[s0][k] + D[s2][k]);
+                const float iy = Hs[s2][k] - Hs[s0][k];
+                pxx[k] = ix * ix;
+                pxy[k] = ix * iy;
+                pyy[k] = iy * iy;
+            }
+            hsum4(pxx, HB[s2][0], HB[s2][1], HB[s2][2], HB[s2][3]);
+            hsum4(pxy, HB[s2][4], HB[s2][5], HB[s2][6], HB[s2][7]);
+            hsum4(pyy, HB[s2][8], HB[s2][9], HB[s2][10], HB[s2][11]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float sxx = (HB[s0][0 + j] + HB[s1][0 + j]) + HB[s2][0 + j];
+                const float sxy = (HB[s0][4 + j] + HB[s1][4 + j]) + HB[s2][4 + j];
+                const float syy = (HB[s0][8 + j] + HB[s1][8 + j]) + HB[s2][8 + j];
+                out[j] = coarsity_fast(sxx, sxy, syy, kappa);
+            }
+        } else {
+            const float WX[9] = {-kSobA, 0.f, kSobA, -kSobB, 0.f, kSobB, -kSobA, 0.f, kSobA};
+            const float WY[9] = {-kSobA, -kSobB, -kSobA, 0.f, 0.f, 0.f, kSobA, kSobB, kSobA};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) G3[s2][k] = gown[k];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) G3[s2][4 + k] = __shfl_down_sync(0xffffffffu, G3[s2][k], 1);
+            if (lane == 31) halo(G3[s2][4], G3[s2][5], G3[s2][6], G3[s2][7]);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+                const float ix = conv9_exact(WX, G3[s0][k], G3[s0][k + 1], G3[s0][k + 2], G3[s1][k], G3[s1][k + 1],
+                                             G3[s1][k + 2], G3[s2][k], G3[s2][k + 1], G3[s2][k + 2]);
+                const float iy = conv9_exact(WY, G3[s0][k], G3[s0][k + 1], G3[s0][k + 2], G3[s1][k], G3[s1][k + 1],
+                                             G3[s1][k + 2], G3[s2][k], G3[s2][k + 1], G3[s2][k + 2]);
+                P[s2][k] = __fmul_rn(ix, ix);
+                P[s2][6 + k] = __fmul_rn(ix, iy);
+                P[s2][12 + k] = __fmul_rn(iy, iy);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                float sq[3];
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const int o = q * 6 + j;
+                    sq[q] = sum9_exact(P[s0][o], P[s0][o + 1], P[s0][o + 2], P[s1][o], P[s1][o + 1], P[s1][o + 2],
+                                       P[s2][o], P[s2][o + 1], P[s2][o + 2]);
+                }
+                out[j] = coarsity_exact(sq[0], sq[1], sq[2], kappa);
+            }
+        }
+    }
+};
+
+// gray in the arithmetic of the core: FAST pre-scales by 1/12, EXACT is Appendix B
+template <bool EXACT>
+__device__ __forceinline__ float gray_of(float r, float g, float b) {
+    if constexpr (EXACT)
+        return gray_exact(r, g, b);
+    else
+        return fmaf(kGrayB12, b, fmaf(kGrayG12, g, kGrayR12 * r));
+}
+
+// ------------------------------------------------------------ planar RGB f32
+template <bool EXACT, int CH>
+struct HarrisF32Op {
+    static_assert(CH % 3 == 0, "row rotation needs CH % 3 == 0");
+    static constexpr int kRowsPerStage = CH;
+    static constexpr int kHaloRows = 4;
+    static constexpr uint32_t kTxBytes = 3u * CH * kBoxCols * 4u;
+    static constexpr uint32_t kStageBytes = (kTxBytes + 127u) / 128u * 128u;
+    struct Params {
+        float kappa;
+    };
+    HarrisCore<EXACT> core;
+
+    __device__ __forceinline__ explicit HarrisF32Op(const Params& p) : core(p.kappa) {}
+
+    __device__ __forceinline__ static void load(void* smem, const CUtensorMap* tmap, uint64_t* bar, int col0,
+                                                int row0, int image, uint64_t policy) {
+        tma_load_4d(smem, tmap, bar, col0, row0, 0, image, policy);
+    }
+
+    template <int R>
+    __device__ __forceinline__ void row(const unsigned char* stage, int lane, float (&out)[4]) {
+        const float* sm = reinterpret_cast<const float*>(stage);
+        const float* pr = sm + (0 * CH + R) * kBoxCols;
+        const float* pg = sm + (1 * CH + R) * kBoxCols;
+        const float* pb = sm + (2 * CH + R) * kBoxCols;
+        const float4 r = lds128(pr + lane * 4), g = lds128(pg + lane * 4), b = lds128(pb + lane * 4);
+        const float gown[4] = {gray_of<EXACT>(r.x, g.x, b.x), gray_of<EXACT>(r.y, g.y, b.y),
+                               gray_of<EXACT>(r.z, g.z, b.z), gray_of<EXACT>(r.w, g.w, b.w)};
+        core.template step<R>(gown, lane, [&](float& h0, float& h1, float& h2, float& h3) {
+            const float4 r2 = lds128(pr + kWarpCols), g2 = lds128(pg + kWarpCols), b2 = lds128(pb + kWarpCols);
+            h0 = gray_of<EXACT>(r2.x, g2.x, b2.x);
+            h1 = gray_of<EXACT>(r2.y, g2.y, b2.y);
+            h2 = gray_of<EXACT>(r2.z, g2.z, b2.z);
+            h3 = gray_of<EXACT>(r2.w, g2.w, b2.w);
+        }, out);
+    }
+};
+
+// --------------------------------------------------- interleaved RGB u8 (HWC)
+// byte k of w as an exact float: 0x4B0000bb is 2^23 + b, minus 2^23 (PRMT + FADD)
+__device__ __forceinline__ float u8f(uint32_t w, int k) {
+    return __int_as_float(__byte_perm(w, 0x4B000000u, 0x7440u | uint32_t(k))) - 8388608.0f;
+}
+
+// FAST gray of raw bytes: weights pre-scaled by 1/(12*255); EXACT: Appendix-B gray of
+// the IEEE quotients v/255 (the same f32 values the planar path sees for u8/255 data)
+template <bool EXACT>
+__device__ __forceinline__ float gray_u8(float r, float g, float b) {
+    if constexpr (EXACT) {
+        return gray_exact(__fdiv_rn(r, 255.0f), __fdiv_rn(g, 255.0f), __fdiv_rn(b, 255.0f));
+    } else {
+        constexpr float kR = 0.299f / (12.0f * 255.0f), kG = 0.587f / (12.0f * 255.0f),
+                        kB = 0.114f / (12.0f * 255.0f);
+        return fmaf(kB, b, fmaf(kG, g, kR * r));
+    }
+}
+
+// 4 pixels = 12 bytes = 3 words: w0 = R0 G0 B0 R1, w1 = G1 B1 R2 G2, w2 = B2 R3 G3 B3
+template <bool EXACT>
+__device__ __forceinline__ void gray4_u8(uint32_t w0, uint32_t w1, uint32_t w2, float& g0, float& g1, float& g2,
+                                         float& g3) {
+    g0 = gray_u8<EXACT>(u8f(w0, 0), u8f(w0, 1), u8f(w0, 2));
+    g1 = gray_u8<EXACT>(u8f(w0, 3), u8f(w1, 0), u8f(w1, 1));
+    g2 = gray_u8<EXACT>(u8f(w1, 2), u8f(w1, 3), u8f(w2, 0));
+    g3 = gray_u8<EXACT>(u8f(w2, 1), u8f(w2, 2), u8f(w2, 3));
+}
+
+template <bool EXACT, int CH>
+struct HarrisU8Op {
+    static_assert(CH % 3 == 0, "row rotation needs CH % 3 == 0");
+    static constexpr int kRowsPerStage = CH;
+    static constexpr int kHaloRows = 4;
+    static constexpr uint32_t kTxBytes = uint32_t(CH) * kU8BoxWords * 4u;
+    static constexpr uint32_t kStageBytes = (kTxBytes + 127u) / 128u * 128u;
+    struct Params {
+        float kappa;
+    };
+    HarrisCore<EXACT> core;
+
+    __device__ __forceinline__ explicit HarrisU8Op(const Params& p) : core(p.kappa) {}
+
+    // tensor map over 32-bit words: {ceil(3W/4) words, H rows, B images}
+    __device__ __forceinline__ static void load(void* smem, const CUtensorMap* tmap, uint64_t* bar, int col0,
+                                                int row0, int image, uint64_t policy) {
+        tma_load_3d(smem, tmap, bar, (col0 / kWarpCols) * (kWarpCols * 3 / 4), row0, image, policy);
+    }
+
+    template <int R>
+    __device__ __forceinline__ void row(const unsigned char* stage, int lane, float (&out)[4]) {
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(stage) + R * kU8BoxWords;
+        float gown[4];
+        gray4_u8<EXACT>(w[3 * lane], w[3 * lane + 1], w[3 * lane + 2], gown[0], gown[1], gown[2], gown[3]);
+        core.template step<R>(gown, lane, [&](float& h0, float& h1, float& h2, float& h3) {
+            gray4_u8<EXACT>(w[96], w[97], w[98], h0, h1, h2, h3);
+        }, out);
+    }
+};
+
+}  // namespace harris

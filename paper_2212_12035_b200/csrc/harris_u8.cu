@@ -1,0 +1,120 @@
+// harris_u8.cu — fused Harris on interleaved 8-bit RGB (HWC, e.g. a decoded
+// rgb.png): the u8 -> f32 (value/255) conversion is fused
+// into the TMA-staged row step, so HBM sees 3 B per
+// input pixel instead of 12 and no separate conversion pass exists.  Same strip
+// engine (strip_pipeline.cuh) and Harris core (harris_ops.cuh) as the f32 path;
+// results equal the f32 path on the planar image u8/255 (bit-for-bit in EXACT
+// order).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "harris_common.cuh"
+#include "harris_internal.h"
+#include "harris_ops.cuh"
+#include "strip_pipeline.cuh"
+
+namespace harris {
+
+const TmaConfig kU8Configs[kNumU8Configs] = {
+    {8, 4, 6},  // 0: default, 2 CTAs (16 warps) per SM (registers capped at 128)
+    {8, 4, 6},  // 1: same ring, 1 CTA per SM (no register cap)
+    {8, 3, 3},  // 2
+};
+
+template <int CFG>
+struct U8Cfg;
+template <>
+struct U8Cfg<0> {
+    static constexpr int NW = 8, NS = 4, CH = 6, MINB = 2;
+};
+template <>
+struct U8Cfg<1> {
+    static constexpr int NW = 8, NS = 4, CH = 6, MINB = 1;
+};
+template <>
+struct U8Cfg<2> {
+    static constexpr int NW = 8, NS = 3, CH = 3, MINB = 1;
+};
+
+template <int CFG, bool EXACT>
+static constexpr auto u8_kernel() {
+    using C = U8Cfg<CFG>;
+    return strip_kernel<HarrisU8Op<EXACT, C::CH>, C::NW, C::NS, C::MINB>;
+}
+
+template <int CFG>
+static constexpr size_t u8_smem() {
+    using C = U8Cfg<CFG>;
+    return StripShape<C::NW, C::NS, HarrisU8Op<false, C::CH>>::kSmemBytes;
+}
+
+template <int CFG>
+static cudaError_t u8_configure_one() {
+    cudaError_t e = cudaFuncSetAttribute(u8_kernel<CFG, false>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(u8_smem<CFG>()));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(u8_kernel<CFG, true>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(u8_smem<CFG>()));
+}
+
+template <int CFG>
+static cudaError_t u8_launch_one(bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid,
+                                 cudaStream_t stream) {
+    using C = U8Cfg<CFG>;
+    const dim3 block{unsigned(C::NW * 32)}, gridd{unsigned(grid)};
+    if (exact) {
+        const typename HarrisU8Op<true, C::CH>::Params p{tg.kappa};
+        u8_kernel<CFG, true>()<<<gridd, block, u8_smem<CFG>(), stream>>>(tmap, tg, p);
+    } else {
+        const typename HarrisU8Op<false, C::CH>::Params p{tg.kappa};
+        u8_kernel<CFG, false>()<<<gridd, block, u8_smem<CFG>(), stream>>>(tmap, tg, p);
+    }
+    return cudaGetLastError();
+}
+
+template <int CFG>
+static cudaError_t u8_occupancy_one(int* n) {
+    using C = U8Cfg<CFG>;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(n, u8_kernel<CFG, false>(), C::NW * 32, u8_smem<CFG>());
+}
+
+size_t u8_smem_bytes(int cfg) {
+    switch (cfg) {
+        case 0: return u8_smem<0>();
+        case 1: return u8_smem<1>();
+        case 2: return u8_smem<2>();
+        default: return 0;
+    }
+}
+
+cudaError_t u8_configure(int cfg) {
+    switch (cfg) {
+        case 0: return u8_configure_one<0>();
+        case 1: return u8_configure_one<1>();
+        case 2: return u8_configure_one<2>();
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t u8_occupancy(int cfg, int* ctas_per_sm) {
+    switch (cfg) {
+        case 0: return u8_occupancy_one<0>(ctas_per_sm);
+        case 1: return u8_occupancy_one<1>(ctas_per_sm);
+        case 2: return u8_occupancy_one<2>(ctas_per_sm);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_tma_u8(int cfg, bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid,
+                          cudaStream_t stream) {
+    switch (cfg) {
+        case 0: return u8_launch_one<0>(exact, tmap, tg, grid, stream);
+        case 1: return u8_launch_one<1>(exact, tmap, tg, grid, stream);
+        case 2: return u8_launch_one<2>(exact, tmap, tg, grid, stream);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace harris

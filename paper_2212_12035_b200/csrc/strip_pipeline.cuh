@@ -1,0 +1,158 @@
+// strip_pipeline.cuh — the warp-strip TMA engine shared by every fused stencil
+// in this library (Harris f32, Harris u8-ingest, separable 3x3).
+//
+// Work decomposition: a *tile* is one 128-output-column warp strip x
+// `band_rows` output rows of one image (TileGeom).  A persistent grid of
+// NW-warp CTAs strides its warps over tiles; each warp is independent (no
+// CTA-wide barrier anywhere): it owns an NS-stage shared-memory ring, and its
+// lane 0 issues one TMA box per stage (Op::load) completing on the stage's
+// mbarrier.  The producer cursor runs NS stages ahead of the consumer and keeps
+// going across tile boundaries, so the pipeline never drains between tiles.
+//
+// The consumer calls Op::row<R>() once per input row (R = row within the stage,
+// a compile-time constant: the row loop is fully unrolled and the stage height
+// is a multiple of the op's register-rotation period, so rolling-window state
+// lives in registers with static slot indices — the thesis's register rotation,
+// PAPER.md:4814-4815) and stores the 4 outputs of each lane once the window is
+// full (input row i >= Op::kHaloRows).
+//
+// Op concept:
+//   kRowsPerStage, kHaloRows, kStageBytes (multiple of 128), kTxBytes
+//   struct Params;  explicit Op(const Params&)
+//   static void load(void* smem, const CUtensorMap*, uint64_t* bar, int strip_col0, int in_row0, int image,
+//                    uint64_t l2_policy)                       // lane 0 only
+//   template <int R> void row(const unsigned char* stage, int lane, float (&out)[4])
+#pragma once
+#include <cuda.h>
+
+#include <cstdint>
+#include <utility>
+
+#include "harris_common.cuh"
+#include "harris_internal.h"
+
+namespace harris {
+
+struct TileCoord {
+    int b, band, cs;
+};
+
+__device__ __forceinline__ TileCoord decode_tile(int64_t t, const TileGeom& g) {
+    TileCoord c;
+    const int64_t q = t / g.colsegs;
+    c.cs = int(t - q * g.colsegs);
+    const int64_t b = q / g.bands;
+    c.band = int(q - b * g.bands);
+    c.b = int(b);
+    return c;
+}
+
+__device__ __forceinline__ int band_rows_out(int band, const TileGeom& g) {
+    const int r = g.n - band * g.band_rows;
+    return r < g.band_rows ? r : g.band_rows;
+}
+
+template <class F, int... Rs>
+__device__ __forceinline__ void static_for(F&& f, std::integer_sequence<int, Rs...>) {
+    (f(std::integral_constant<int, Rs>{}), ...);
+}
+
+template <int NW, int NS, class Op>
+struct StripShape {
+    static_assert(Op::kStageBytes % 128 == 0, "TMA destinations must be 128-byte aligned");
+    static constexpr size_t kSmemBytes = size_t(NW) * NS * Op::kStageBytes + size_t(NW) * NS * 8 + 128;
+};
+
+template <class Op, int NW, int NS, int MINB = 1>
+__global__ void __launch_bounds__(NW * 32, MINB)
+    strip_kernel(const __grid_constant__ CUtensorMap tmap, const TileGeom g, const typename Op::Params p) {
+    constexpr int CH = Op::kRowsPerStage;
+    constexpr int HALO = Op::kHaloRows;
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* base =
+        reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    unsigned char* ring = base + size_t(warp) * NS * Op::kStageBytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(base + size_t(NW) * NS * Op::kStageBytes) + warp * NS;
+
+    const int64_t GW = int64_t(gridDim.x) * NW;
+    const int64_t gw = int64_t(blockIdx.x) * NW + warp;
+    if (gw >= g.tiles) return;  // warps are independent: no CTA-wide barrier below
+
+    if (lane == 0) {
+        prefetch_tmap(&tmap);
+#pragma unroll
+        for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+        fence_barrier_init();
+    }
+    __syncwarp();
+    const uint64_t policy = l2_policy(g.l2_policy);
+
+    // ---- producer cursor (warp-uniform; lane 0 issues) ----
+    int64_t pt = gw;
+    int pc = 0;
+    int pn = (band_rows_out(decode_tile(pt, g).band, g) + HALO + CH - 1) / CH;
+    auto issue = [&](int s) {
+        if (pt < g.tiles) {
+            if (lane == 0) {
+                const TileCoord c = decode_tile(pt, g);
+                mbar_arrive_expect_tx(&bars[s], Op::kTxBytes);
+                Op::load(ring + s * Op::kStageBytes, &tmap, &bars[s], c.cs * kWarpCols,
+                         c.band * g.band_rows + pc * CH, c.b, policy);
+            }
+            if (++pc == pn) {
+                pc = 0;
+                pt += GW;
+                if (pt < g.tiles) pn = (band_rows_out(decode_tile(pt, g).band, g) + HALO + CH - 1) / CH;
+            }
+        }
+    };
+#pragma unroll
+    for (int s = 0; s < NS; ++s) issue(s);
+
+    Op op(p);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t t = gw; t < g.tiles; t += GW) {
+        const TileCoord tc = decode_tile(t, g);
+        const int rows_out = band_rows_out(tc.band, g);
+        const int nch = (rows_out + HALO + CH - 1) / CH;
+        const int col0 = tc.cs * kWarpCols + lane * kColsPerLane;
+        const bool col_ok = col0 < g.m;
+        float* orow = g.out + int64_t(tc.b) * g.out_image_stride + int64_t(tc.band) * g.band_rows * g.out_pitch +
+                      col0;
+
+        for (int c = 0; c < nch; ++c) {
+            mbar_wait(&bars[stage], phase);
+            const unsigned char* sm = ring + stage * Op::kStageBytes;
+            static_for(
+                [&](auto rc) {
+                    constexpr int R = decltype(rc)::value;
+                    const int i = c * CH + R;  // input row within the tile
+                    float out4[4];
+                    op.template row<R>(sm, lane, out4);
+                    if (i >= HALO && i - HALO < rows_out && col_ok) {
+                        float* po = orow + int64_t(i - HALO) * g.out_pitch;
+                        if (g.vec_store && col0 + kColsPerLane <= g.m) {
+                            stg128_cs(po, out4[0], out4[1], out4[2], out4[3]);
+                        } else {  // unaligned output rows, or the ragged right edge
+#pragma unroll
+                            for (int k = 0; k < kColsPerLane; ++k)
+                                if (col0 + k < g.m) po[k] = out4[k];
+                        }
+                    }
+                },
+                std::make_integer_sequence<int, CH>{});
+            __syncwarp();  // every lane is done with this stage: refill it
+            issue(stage);
+            if (++stage == NS) {
+                stage = 0;
+                phase ^= 1u;
+            }
+        }
+    }
+}
+
+}  // namespace harris

@@ -188,6 +188,51 @@ def harris(rgb, kappa: float = KAPPA, *, out: Optional[torch.Tensor] = None, exa
     return out
 
 
+def harris_u8(rgb8, kappa: float = KAPPA, *, out: Optional[torch.Tensor] = None, exact: bool = False,
+              force_generic: bool = False, force_tma: bool = False, stream: Optional[torch.cuda.Stream] = None):
+    """Fused Harris on interleaved 8-bit RGB: ``(H, W, 3)`` or ``(B, H, W, 3)`` uint8
+    (value/255), CUDA (device path) or CPU/numpy (host path through the device).
+    Returns ``(H-4, W-4)`` / ``(B, H-4, W-4)`` float32, equal to ``harris`` on the planar
+    image ``rgb8/255`` (bit-for-bit with ``exact=True``)."""
+    flags = _flags(exact, force_generic, force_tma)
+    shape = tuple(rgb8.shape)
+    if rgb8.dtype not in (torch.uint8, np.uint8):
+        raise TypeError("harris_u8 expects uint8 interleaved RGB")
+    if len(shape) not in (3, 4) or shape[-1] != 3:
+        raise ValueError("rgb8 must be (H, W, 3) or (B, H, W, 3)")
+    H, W = shape[-3], shape[-2]
+    if H < 5 or W < 5:
+        raise ValueError(f"harris needs an input of at least 5x5, got {H}x{W}")
+    B = shape[0] if len(shape) == 4 else 1
+    n, m = H - 4, W - 4
+    batched = len(shape) == 4
+    if isinstance(rgb8, np.ndarray) or not rgb8.is_cuda:
+        arr = np.ascontiguousarray(rgb8 if isinstance(rgb8, np.ndarray) else rgb8.numpy())
+        res = np.empty((B, n, m) if batched else (n, m), dtype=np.float32)
+        ctx = context(torch.cuda.current_device())
+        rc = lib().harris_run_host_u8(ctx.handle, res.ctypes.data, m, n, m, arr.ctypes.data, B, kappa, flags)
+        check(rc, "harris_run_host_u8", ctx.handle)
+        return res if isinstance(rgb8, np.ndarray) else torch.from_numpy(res)
+    if rgb8.stride(-1) != 1 or rgb8.stride(-2) != 3:
+        rgb8 = rgb8.contiguous()
+    if out is None:
+        out = torch.empty((B, n, m) if batched else (n, m), dtype=torch.float32, device=rgb8.device)
+    elif tuple(out.shape) != ((B, n, m) if batched else (n, m)) or out.stride(-1) != 1 or \
+            out.dtype != torch.float32 or out.device != rgb8.device:
+        raise ValueError("out has the wrong shape, dtype, device or column stride")
+    in_pitch = rgb8.stride(-3)
+    in_image = rgb8.stride(0) if batched else H * in_pitch
+    out_pitch = out.stride(-2)
+    out_image = out.stride(0) if batched else n * out_pitch
+    dev = rgb8.device.index if rgb8.device.index is not None else torch.cuda.current_device()
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    ctx = context(dev)
+    rc = lib().harris_run_u8(ctx.handle, out.data_ptr(), out_pitch, out_image, n, m, rgb8.data_ptr(), in_pitch,
+                             in_image, B, kappa, flags, st.cuda_stream)
+    check(rc, "harris_run_u8", ctx.handle)
+    return out
+
+
 GROUPINGS = {
     1: "[Sx],[Sy],[x],[+],[coarsity]",
     2: "[Sx,Sy,x],[+,coarsity]",
@@ -257,5 +302,5 @@ def algorithmic_bytes(n: int, m: int, batch: int = 1) -> int:
     return batch * (12 * (n + 4) * (m + 4) + 4 * n * m)
 
 
-__all__ = ["HarrisContext", "context", "harris", "harris_grouping", "grouping_hbm_bytes", "GROUPINGS", "synth_",
+__all__ = ["HarrisContext", "context", "harris", "harris_u8", "harris_grouping", "grouping_hbm_bytes", "GROUPINGS", "synth_",
            "algorithmic_bytes", "KAPPA", "_lib"]

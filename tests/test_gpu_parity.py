@@ -252,3 +252,56 @@ def test_grouping_scratch_contract(cuda_ctx):
     rc = L.harris_run_grouping(cuda_ctx.handle, 1, out.data_ptr(), 16, 16, rgb.data_ptr(), small.data_ptr(), 32,
                                0.04, 0, None)
     assert rc == _lib.HARRIS_ERR_INVALID_ARGUMENT
+
+
+def _u8_image(B, H, W, seed):
+    """u8 HWC image from the synthetic generator's dist-1 bytes, plus its planar f32 /255 twin."""
+    planes = synth.synth_numpy(3 * B, H, W, seed=seed, dist=1)          # (3B, H, W) = byte/255
+    u8 = np.rint(planes * 255.0).astype(np.uint8).reshape(B, 3, H, W)
+    hwc = np.ascontiguousarray(u8.transpose(0, 2, 3, 1))
+    f32 = (u8.astype(np.float32) / np.float32(255.0)).astype(np.float32)
+    assert np.array_equal(f32.reshape(3 * B, H, W), planes)
+    return hwc, f32
+
+
+@pytest.mark.parametrize("H,W", [(5, 16), (9, 128), (37, 144), (70, 272), (133, 528), (300, 2048)])
+def test_u8_tma_exact_equals_f32_path(cuda_ctx, H, W):
+    hwc, f32 = _u8_image(1, H, W, seed=H + W)
+    got = hb.harris_u8(torch.from_numpy(hwc[0]).cuda(), exact=True, force_tma=True)
+    assert cuda_ctx.last_path == _lib.PATH_TMA
+    torch.cuda.synchronize()
+    assert np.array_equal(got.cpu().numpy(), cref.harris_f32(f32[0]))
+
+
+@pytest.mark.parametrize("H,W", [(5, 5), (13, 17), (40, 130), (64, 200)])
+def test_u8_generic_exact_equals_f32_path(cuda_ctx, H, W):
+    hwc, f32 = _u8_image(1, H, W, seed=3 * H + W)
+    got = hb.harris_u8(torch.from_numpy(hwc[0]).cuda(), exact=True, force_generic=True)
+    assert cuda_ctx.last_path == _lib.PATH_GENERIC
+    torch.cuda.synchronize()
+    assert np.array_equal(got.cpu().numpy(), cref.harris_f32(f32[0]))
+
+
+@pytest.mark.parametrize("H,W", [(9, 128), (70, 272), (517, 1040), (64, 200)])
+def test_u8_fast_within_tolerance(cuda_ctx, H, W):
+    hwc, f32 = _u8_image(1, H, W, seed=5 * H + W)
+    got = hb.harris_u8(torch.from_numpy(hwc[0]).cuda())
+    torch.cuda.synchronize()
+    ok, m = synth.within_tolerance(got.cpu().numpy(), cref.harris_f64(f32[0]))
+    assert ok, m
+
+
+def test_u8_batched_and_host(cuda_ctx):
+    B, H, W = 3, 60, 400
+    hwc, f32 = _u8_image(B, H, W, seed=77)
+    dev = hb.harris_u8(torch.from_numpy(hwc).cuda(), exact=True)
+    assert cuda_ctx.last_path == _lib.PATH_TMA
+    torch.cuda.synchronize()
+    for i in range(B):
+        assert np.array_equal(dev[i].cpu().numpy(), cref.harris_f32(f32[i]))
+    host = hb.harris_u8(hwc, exact=True)
+    assert np.array_equal(host, dev.cpu().numpy())
+    big, bigf = _u8_image(1, 2100, 4096, seed=78)   # banded host pipeline (> 48 MB chunk? no: 25 MB) + fast order
+    fast = hb.harris_u8(big[0])
+    ok, m = synth.within_tolerance(fast, cref.harris_f64(bigf[0]))
+    assert ok, m

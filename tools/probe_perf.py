@@ -60,15 +60,59 @@ print(json.dumps(res))
     return json.loads(r.stdout.strip().splitlines()[-1])
 
 
+def time_u8(cfg, workloads, iters):
+    env = dict(os.environ, HARRIS_U8_CONFIG=str(cfg))
+    code = f"""
+import sys, torch, json
+sys.path.insert(0, {ROOT!r})
+import paper_2212_12035_b200 as hb
+res = []
+g = torch.Generator(device='cuda'); g.manual_seed(12035)
+for (B, H, W) in {workloads!r}:
+    x = torch.randint(0, 256, (B, H, W, 3), dtype=torch.uint8, device='cuda', generator=g)
+    out = torch.empty((B, H - 4, W - 4), device='cuda')
+    for _ in range(3):
+        hb.harris_u8(x, out=out)
+    torch.cuda.synchronize()
+    evs = []
+    for _ in range({iters}):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(); hb.harris_u8(x, out=out); e1.record()
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    ts = sorted(a.elapsed_time(b) for a, b in evs)
+    res.append(dict(B=B, H=H, W=W, ms=ts[len(ts) // 2], min_ms=ts[0], path=hb.context().last_path))
+    del x, out
+    torch.cuda.empty_cache()
+print(json.dumps(res))
+"""
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+    if r.returncode != 0:
+        print(r.stderr[-2000:])
+        return []
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="0,1,2,3")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--exact", action="store_true")
     ap.add_argument("--generic", action="store_true")
+    ap.add_argument("--u8", action="store_true")
     a = ap.parse_args()
     workloads = [(1, 8192, 8192), (1024, 1080, 1920), (1, 1536, 2560)]
     pk = peak()
+    if a.u8:
+        for cfg in [int(c) for c in a.configs.split(",")]:
+            for r in time_u8(cfg, workloads, a.iters):
+                B, H, W = r["B"], r["H"], r["W"]
+                nbytes = B * (3 * H * W + 4 * (H - 4) * (W - 4))
+                gbs = nbytes / (r["ms"] * 1e-3) / 1e9
+                mps = B * (H - 4) * (W - 4) / (r["ms"] * 1e-3) / 1e6
+                print(f"u8 cfg{cfg} {B}x{H}x{W}: {r['ms']:.4f} ms (min {r['min_ms']:.4f}) {mps:,.0f} MP/s "
+                      f"{gbs:,.0f} GB/s frac={gbs / pk:.3f} path={r['path']}", flush=True)
+        return
     for cfg in [int(c) for c in a.configs.split(",")]:
         for r in time_cfg(cfg, workloads, a.iters, a.exact, a.generic):
             B, H, W = r["B"], r["H"], r["W"]
