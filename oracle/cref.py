@@ -43,6 +43,10 @@ def lib() -> ctypes.CDLL:
         L.oracle_harris_f32_rrot.restype = ctypes.c_int
         L.oracle_harris_f32_rrot_batched.argtypes = [vp, i64, i64, vp, i64, ctypes.c_float, ctypes.c_int]
         L.oracle_harris_f32_rrot_batched.restype = ctypes.c_int
+        L.oracle_sep3x3_f32.argtypes = [vp, i64, i64, i64, vp, i64, vp, vp, ctypes.c_int]
+        L.oracle_sep3x3_f32.restype = ctypes.c_int
+        L.oracle_sep3x3_f64.argtypes = [vp, i64, i64, i64, vp, i64, vp, vp, ctypes.c_int, ctypes.c_int]
+        L.oracle_sep3x3_f64.restype = ctypes.c_int
         L.oracle_synth_fill.argtypes = [vp, i64, i64, i64, i64, i64, i64, i64, i64, ctypes.c_uint64, ctypes.c_int]
         L.oracle_synth_fill.restype = None
         L.oracle_max_threads.argtypes = []
@@ -125,6 +129,35 @@ def harris_batched(rgb: np.ndarray, variant: str = "cbuf", kappa: float = 0.04, 
     rc = lib().oracle_harris_f32_rrot_batched(_ptr(out), H - 4, W - 4, _ptr(rgb), B, kappa, nthreads)
     if rc:
         raise RuntimeError(f"oracle_harris_f32_rrot_batched failed ({rc})")
+    return out
+
+
+def sep3x3_f32(img: np.ndarray, wv=(1.0, 2.0, 1.0), wh=(1.0, 2.0, 1.0), nthreads: int = 0) -> np.ndarray:
+    """Separable 3x3 stencil, f32, vertical-then-horizontal order: (n+2, m+2) -> (n, m)."""
+    img = np.ascontiguousarray(img, dtype=np.float32)
+    if img.ndim != 2 or img.shape[0] < 3 or img.shape[1] < 3:
+        raise ValueError("img must be 2-D and at least 3x3")
+    n, m = img.shape[0] - 2, img.shape[1] - 2
+    out = np.empty((n, m), dtype=np.float32)
+    a = np.asarray(wv, dtype=np.float32)
+    b = np.asarray(wh, dtype=np.float32)
+    rc = lib().oracle_sep3x3_f32(_ptr(out), m, n, m, _ptr(img), m + 2, _ptr(a), _ptr(b), nthreads)
+    if rc:
+        raise RuntimeError(f"oracle_sep3x3_f32 failed ({rc})")
+    return out
+
+
+def sep3x3_f64(img: np.ndarray, wv=(1.0, 2.0, 1.0), wh=(1.0, 2.0, 1.0), form: int = 1,
+               nthreads: int = 0) -> np.ndarray:
+    """f64 in the reference evaluator's order: form 0 direct 2-D dot, form 1 vertical-then-horizontal."""
+    img = np.ascontiguousarray(img, dtype=np.float32)
+    n, m = img.shape[0] - 2, img.shape[1] - 2
+    out = np.empty((n, m), dtype=np.float64)
+    a = np.asarray(wv, dtype=np.float64)
+    b = np.asarray(wh, dtype=np.float64)
+    rc = lib().oracle_sep3x3_f64(_ptr(out), m, n, m, _ptr(img), m + 2, _ptr(a), _ptr(b), form, nthreads)
+    if rc:
+        raise RuntimeError(f"oracle_sep3x3_f64 failed ({rc})")
     return out
 
 

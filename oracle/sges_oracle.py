@@ -114,6 +114,25 @@ def harris_sges(rgb: np.ndarray) -> np.ndarray:
     return np.asarray(out, dtype=np.float64)
 
 
+BINOMIAL_INITIAL = "map (map (dot (join weights2d))) (map (map join) (map transpose (slide 3 1 (map (slide 3 1) input))))"
+BINOMIAL_SEPARATED = r"map (\l. map (dot weightsH) (slide 3 1 (map (dot weightsV) (transpose l)))) (slide 3 1 input)"
+
+
+def binomial_sges(img: np.ndarray, form: str = "separated") -> np.ndarray:
+    """The reference's binomial rewrite goal (Fig. binom-rewrite),
+    initial (direct 2-D) or separated (vertical then horizontal) program, evaluated by
+    ``evalref.eval_term`` in f64 with the reference's weights (evalref.py:112-115)."""
+    parser, types, nat, infer, evalref = _sges()
+    img = np.asarray(img, dtype=np.float32)
+    H, W = img.shape
+    n, m = nat.var("n"), nat.var("m")
+    env = {"input": _arr(types, nat, nat.add(n, nat.const(2)), nat.add(m, nat.const(2)))}
+    src = BINOMIAL_INITIAL if form == "initial" else BINOMIAL_SEPARATED
+    term = infer.from_named(parser.parse_term(src), env=env, sizes={"n", "m"})
+    out = evalref.eval_term(term, (), {"input": img.astype(np.float64).tolist()}, {"n": H - 2, "m": W - 2})
+    return np.asarray(out, dtype=np.float64)
+
+
 def register_ambient_harris(env: dict, amb: dict, impl: Callable[[np.ndarray], np.ndarray]):
     """Register ``harris`` as an ambient Rise primitive.
 
