@@ -119,6 +119,17 @@ HARRIS_API int harris_run_u8(harris_ctx* ctx, float* out, int64_t out_pitch, int
 HARRIS_API int harris_run_host_u8(harris_ctx* ctx, float* out_host, int64_t out_pitch, int64_t n, int64_t m,
                                   const uint8_t* rgb8_host, int64_t batch, float kappa, uint32_t flags);
 
+/* Separable 3x3 stencil on f32 planes (the reference's binomial
+ * filter is wv = wh = {1,2,1}):
+ *   out[b][y][x] = sum_j wh[j] * (sum_i wv[i] * in[b][y+i][x+j])   (vertical then horizontal)
+ * in: batch x (n+2) x (m+2) at in[b*in_image_stride + y*in_pitch + x]; out: batch x n x m.
+ * Same strip/TMA engine as harris_run; HARRIS_FLAG_EXACT_ORDER rounds every product
+ * and sum in that order (bit-exact with the oracle). wv, wh: 3 host floats each. */
+HARRIS_API int harris_stencil3x3_sep(harris_ctx* ctx, float* out, int64_t out_pitch, int64_t out_image_stride,
+                                     int64_t n, int64_t m, const float* in, int64_t in_pitch,
+                                     int64_t in_image_stride, int64_t batch, const float* wv, const float* wh,
+                                     uint32_t flags, void* cuda_stream);
+
 /* Device synthetic-image generator used by the bench (bit-identical to
  * oracle_synth_fill): dst (p, y, x) at dst[p*dst_plane_stride + y*dst_pitch + x] =
  * value of global plane plane0+p, row row0+y of a planes x H_global x W stack.

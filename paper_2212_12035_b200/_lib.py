@@ -37,7 +37,7 @@ EXPORTED_SYMBOLS = (
     "harris_run_host", "harris_synth_fill", "harris_plan", "harris_last_path", "harris_device",
     "harris_num_sms", "harris_strerror", "harris_last_cuda_error", "harris_abi_version",
     "harris_grouping_scratch_bytes", "harris_grouping_launches", "harris_run_grouping",
-    "harris_run_u8", "harris_run_host_u8",
+    "harris_run_u8", "harris_run_host_u8", "harris_stencil3x3_sep",
 )
 
 GROUPING_UNFUSED, GROUPING_SOBEL_PROD, GROUPING_SOBEL, GROUPING_FUSED = 1, 2, 3, 4
@@ -104,6 +104,8 @@ def lib() -> ctypes.CDLL:
         "harris_run_grouping": ([vp, i32, vp, i64, i64, vp, vp, i64, f32, u32, vp], i32),
         "harris_run_u8": ([vp, vp, i64, i64, i64, i64, vp, i64, i64, i64, f32, u32, vp], i32),
         "harris_run_host_u8": ([vp, vp, i64, i64, i64, vp, i64, f32, u32], i32),
+        "harris_stencil3x3_sep": ([vp, vp, i64, i64, i64, i64, vp, i64, i64, i64, ctypes.POINTER(f32),
+                                   ctypes.POINTER(f32), u32, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

@@ -30,6 +30,7 @@ struct harris_ctx {
     int cc_major = 0, cc_minor = 0;
     int tma_cfg = 0;
     int u8_cfg = 0;
+    int occ_sep = 0;
     int occ_u8[kNumU8Configs] = {0};
     int l2_policy = 1;  // evict_normal: the 4-column halo sectors are re-read by the neighbouring strip
     int64_t force_band_rows = 0;  // dev knob (HARRIS_BAND_ROWS): override the planner
@@ -120,7 +121,7 @@ bool tma_eligible(const Call& c) {
 // Pick the band height that minimises (waves x rows-per-tile) for a persistent
 // grid of `gw` warps: tiles = batch x bands x col_segments.
 void plan_tiles(int64_t n, int64_t m, int64_t batch, int64_t gw, int rows_per_stage, int64_t force_rows,
-                TileGeom& tg) {
+                TileGeom& tg, int halo = 4) {
     const int64_t colsegs = (m + kWarpCols - 1) / kWarpCols;
     if (force_rows > 0) {
         const int64_t rows = std::min(force_rows, n);
@@ -141,7 +142,7 @@ void plan_tiles(int64_t n, int64_t m, int64_t batch, int64_t gw, int rows_per_st
         if (bands != nb) continue;  // same split as a smaller nb
         const int64_t tiles = batch * colsegs * bands;
         const int64_t waves = (tiles + gw - 1) / gw;
-        const int64_t rows_in = ((rows + 4 + rows_per_stage - 1) / rows_per_stage) * rows_per_stage;
+        const int64_t rows_in = ((rows + halo + rows_per_stage - 1) / rows_per_stage) * rows_per_stage;
         const int64_t cost = waves * (rows_in + kTileOverheadRows);
         if (cost < best_cost) {
             best_cost = cost;
@@ -346,6 +347,12 @@ int harris_init(harris_ctx** out_ctx, int cuda_device) {
             return rc;
         }
     }
+    e = sep_configure(&ctx->occ_sep);
+    if (e != cudaSuccess) {
+        int rc = cuda_fail(ctx, e, "configure stencil kernel");
+        delete ctx;
+        return rc;
+    }
     for (int k = 0; k < kNumU8Configs; ++k) {
         e = u8_configure(k);
         if (e == cudaSuccess) e = u8_occupancy(k, &ctx->occ_u8[k]);
@@ -406,6 +413,59 @@ int harris_run_u8(harris_ctx* ctx, float* out, int64_t out_pitch, int64_t out_im
     c.fmt = kU8Interleaved;
     if (!rgb8) return HARRIS_ERR_INVALID_ARGUMENT;
     return run(ctx, c, static_cast<cudaStream_t>(stream));
+}
+
+int harris_stencil3x3_sep(harris_ctx* ctx, float* out, int64_t out_pitch, int64_t out_image_stride, int64_t n,
+                          int64_t m, const float* in, int64_t in_pitch, int64_t in_image_stride, int64_t batch,
+                          const float* wv, const float* wh, uint32_t flags, void* stream_) {
+    if (!ctx || !out || !in || !wv || !wh) return HARRIS_ERR_INVALID_ARGUMENT;
+    if (n < 1 || m < 1) return HARRIS_ERR_SIZE;
+    if (n + 2 > INT32_MAX || m + 2 > INT32_MAX) return HARRIS_ERR_SIZE;
+    if (batch < 1 || in_pitch < m + 2 || out_pitch < m) return HARRIS_ERR_INVALID_ARGUMENT;
+    if (batch > 1 && (in_image_stride < (n + 2) * in_pitch || out_image_stride < n * out_pitch))
+        return HARRIS_ERR_INVALID_ARGUMENT;
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    const bool exact = (flags & HARRIS_FLAG_EXACT_ORDER) != 0;
+    const int64_t img_stride = batch > 1 ? in_image_stride : (n + 2) * in_pitch;
+    const bool tma = !(flags & HARRIS_FLAG_FORCE_GENERIC) && aligned16(in) && (in_pitch & 3) == 0 &&
+                     (batch == 1 || (in_image_stride & 3) == 0) && batch <= INT32_MAX;
+    if (!tma && (flags & HARRIS_FLAG_FORCE_TMA)) return HARRIS_ERR_ALIGNMENT;
+    DeviceGuard guard(ctx->device);
+    if (!guard.ok) return cuda_fail(ctx, cudaGetLastError(), "cudaSetDevice");
+    cudaError_t e;
+    if (tma) {
+        CUtensorMap tmap;
+        cuuint64_t dims[3] = {cuuint64_t(m + 2), cuuint64_t(n + 2), cuuint64_t(batch)};
+        cuuint64_t strides[2] = {cuuint64_t(in_pitch) * 4, cuuint64_t((img_stride + 3) / 4 * 4) * 4};
+        cuuint32_t box[3] = {cuuint32_t(kBoxCols), cuuint32_t(kSepConfig.rows), 1};
+        cuuint32_t estr[3] = {1, 1, 1};
+        CUresult r = ctx->encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(in), dims, strides,
+                                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            std::snprintf(ctx->last_err, sizeof(ctx->last_err), "cuTensorMapEncodeTiled (stencil) failed (%d)", int(r));
+            return HARRIS_ERR_TMA;
+        }
+        TileGeom tg;
+        const int64_t resident = int64_t(ctx->num_sms) * std::max(1, ctx->occ_sep);
+        plan_tiles(n, m, batch, resident * kSepConfig.warps, kSepConfig.rows, ctx->force_band_rows, tg, 2);
+        const int64_t grid = std::min<int64_t>((tg.tiles + kSepConfig.warps - 1) / kSepConfig.warps, resident);
+        tg.out = out;
+        tg.out_pitch = out_pitch;
+        tg.out_image_stride = batch > 1 ? out_image_stride : n * out_pitch;
+        tg.kappa = 0.f;
+        tg.l2_policy = ctx->l2_policy;
+        tg.vec_store = aligned16(out) && (out_pitch & 3) == 0 && (batch == 1 || (out_image_stride & 3) == 0);
+        tg.pad_ = 0;
+        e = launch_tma_sep(exact, tmap, tg, grid, wv, wh, stream);
+    } else {
+        e = launch_generic_sep(exact, in, in_pitch, img_stride, out, out_pitch,
+                               batch > 1 ? out_image_stride : n * out_pitch, n, m, batch, wv, wh, ctx->num_sms,
+                               stream);
+    }
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "launch stencil");
+    ctx->last_path = tma ? HARRIS_PATH_TMA : HARRIS_PATH_GENERIC;
+    return HARRIS_OK;
 }
 
 int harris_plan(harris_ctx* ctx, int64_t n, int64_t m, int64_t batch, const float* rgb, int64_t in_pitch,

@@ -58,6 +58,15 @@ cudaError_t launch_tma_u8(int cfg, bool exact, const CUtensorMap& tmap, const Ti
                           cudaStream_t stream);
 cudaError_t launch_generic_u8(bool exact, const Geom& g, cudaStream_t stream);
 
+// separable 3x3 stencil on one f32 plane (stencil_sep.cu)
+extern const TmaConfig kSepConfig;
+cudaError_t sep_configure(int* ctas_per_sm);
+cudaError_t launch_tma_sep(bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid, const float* wv,
+                           const float* wh, cudaStream_t stream);
+cudaError_t launch_generic_sep(bool exact, const float* in, int64_t in_pitch, int64_t in_image_stride, float* out,
+                               int64_t out_pitch, int64_t out_image_stride, int64_t n, int64_t m, int64_t batch,
+                               const float* wv, const float* wh, int num_sms, cudaStream_t stream);
+
 int64_t grouping_scratch_floats(int grouping, int64_t n, int64_t m);
 int grouping_launches(int grouping);
 cudaError_t launch_grouping(int grouping, float* out, int64_t n, int64_t m, const float* rgb, float* scratch,

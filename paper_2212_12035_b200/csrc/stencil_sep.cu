@@ -1,0 +1,174 @@
+// stencil_sep.cu — separable 3x3 stencil on the strip engine (SURVEY.md §8(f)
+// row 3): out[y][x] = sum_i sum_j wv[i] wh[j] in[y+i][x+j] on one f32 plane,
+// valid region (n+2) x (m+2) -> n x m.  This is the reference package's own
+// stencil workload, the binomial filter weightsV = weightsH = [1,2,1]
+// (evalref.py:112-115; rewrite goal PAPER.md:3935-4016, binomial.rules:26-27),
+// evaluated in the goal's *separated* order: a vertical 3-tap per column, then a
+// horizontal 3-tap over the column results.
+//
+// Each lane owns 4 output columns; it reads its float4 plus the next 2 columns of
+// the TMA box (so no shuffles and no divergent halo branch), keeps the last 3
+// input rows of those 6 columns in registers (slot = row % 3) and emits one
+// float4 per row.  EXACT: every product/sum rounded in listing order (bit-exact
+// with oracle/stencil_oracle.c); FAST: FMA chains.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "harris_common.cuh"
+#include "harris_internal.h"
+#include "strip_pipeline.cuh"
+
+namespace harris {
+
+template <bool EXACT, int CH>
+struct Sep3x3Op {
+    static_assert(CH % 3 == 0, "row rotation needs CH % 3 == 0");
+    static constexpr int kRowsPerStage = CH;
+    static constexpr int kHaloRows = 2;
+    static constexpr uint32_t kTxBytes = uint32_t(CH) * kBoxCols * 4u;
+    static constexpr uint32_t kStageBytes = (kTxBytes + 127u) / 128u * 128u;
+    struct Params {
+        float wv[3], wh[3];
+    };
+    float wv0, wv1, wv2, wh0, wh1, wh2;
+    float X[3][6];
+
+    __device__ __forceinline__ explicit Sep3x3Op(const Params& p)
+        : wv0(p.wv[0]), wv1(p.wv[1]), wv2(p.wv[2]), wh0(p.wh[0]), wh1(p.wh[1]), wh2(p.wh[2]) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int k = 0; k < 6; ++k) X[a][k] = 0.f;
+    }
+
+    __device__ __forceinline__ static void load(void* smem, const CUtensorMap* tmap, uint64_t* bar, int col0,
+                                                int row0, int image, uint64_t policy) {
+        tma_load_3d(smem, tmap, bar, col0, row0, image, policy);
+    }
+
+    template <int R>
+    __device__ __forceinline__ void row(const unsigned char* stage, int lane, float (&out)[4]) {
+        constexpr int s2 = R % 3, s0 = (R + 1) % 3, s1 = (R + 2) % 3;
+        const float* rp = reinterpret_cast<const float*>(stage) + R * kBoxCols + lane * 4;
+        const float4 a = lds128(rp);
+        const float2 b = *reinterpret_cast<const float2*>(rp + 4);
+        X[s2][0] = a.x;
+        X[s2][1] = a.y;
+        X[s2][2] = a.z;
+        X[s2][3] = a.w;
+        X[s2][4] = b.x;
+        X[s2][5] = b.y;
+        float v[6];
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+            if constexpr (EXACT) {
+                float t = __fadd_rn(0.0f, __fmul_rn(wv0, X[s0][j]));
+                t = __fadd_rn(t, __fmul_rn(wv1, X[s1][j]));
+                v[j] = __fadd_rn(t, __fmul_rn(wv2, X[s2][j]));
+            } else {
+                v[j] = fmaf(wv2, X[s2][j], fmaf(wv1, X[s1][j], wv0 * X[s0][j]));
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if constexpr (EXACT) {
+                float t = __fadd_rn(0.0f, __fmul_rn(wh0, v[k]));
+                t = __fadd_rn(t, __fmul_rn(wh1, v[k + 1]));
+                out[k] = __fadd_rn(t, __fmul_rn(wh2, v[k + 2]));
+            } else {
+                out[k] = fmaf(wh2, v[k + 2], fmaf(wh1, v[k + 1], wh0 * v[k]));
+            }
+        }
+    }
+};
+
+constexpr int kSepNW = 8, kSepNS = 4, kSepCH = 6;
+
+template <bool EXACT>
+static constexpr auto sep_kernel() {
+    return strip_kernel<Sep3x3Op<EXACT, kSepCH>, kSepNW, kSepNS, 1>;
+}
+
+static constexpr size_t sep_smem() { return StripShape<kSepNW, kSepNS, Sep3x3Op<false, kSepCH>>::kSmemBytes; }
+
+const TmaConfig kSepConfig = {kSepNW, kSepNS, kSepCH};
+
+cudaError_t sep_configure(int* ctas_per_sm) {
+    cudaError_t e = cudaFuncSetAttribute(sep_kernel<false>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(sep_smem()));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(sep_kernel<true>(), cudaFuncAttributeMaxDynamicSharedMemorySize, int(sep_smem()));
+    if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, sep_kernel<false>(), kSepNW * 32, sep_smem());
+    return e;
+}
+
+cudaError_t launch_tma_sep(bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid, const float* wv,
+                           const float* wh, cudaStream_t stream) {
+    const dim3 block{unsigned(kSepNW * 32)}, gridd{unsigned(grid)};
+    if (exact) {
+        typename Sep3x3Op<true, kSepCH>::Params p{{wv[0], wv[1], wv[2]}, {wh[0], wh[1], wh[2]}};
+        sep_kernel<true>()<<<gridd, block, sep_smem(), stream>>>(tmap, tg, p);
+    } else {
+        typename Sep3x3Op<false, kSepCH>::Params p{{wv[0], wv[1], wv[2]}, {wh[0], wh[1], wh[2]}};
+        sep_kernel<false>()<<<gridd, block, sep_smem(), stream>>>(tmap, tg, p);
+    }
+    return cudaGetLastError();
+}
+
+// generic fallback: one thread per output pixel, same two orders
+template <bool EXACT>
+__global__ void sep_generic_kernel(const float* __restrict__ in, int64_t in_pitch, int64_t in_image_stride,
+                                   float* __restrict__ out, int64_t out_pitch, int64_t out_image_stride, int64_t n,
+                                   int64_t m, int64_t batch, float wv0, float wv1, float wv2, float wh0, float wh1,
+                                   float wh2) {
+    const int64_t total = batch * n * m;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t x = e % m, yb = e / m, y = yb % n, b = yb / n;
+        const float* p = in + b * in_image_stride + y * in_pitch + x;
+        float v[3];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const float r0 = __ldg(p + j), r1 = __ldg(p + in_pitch + j), r2 = __ldg(p + 2 * in_pitch + j);
+            if (EXACT) {
+                float t = __fadd_rn(0.0f, __fmul_rn(wv0, r0));
+                t = __fadd_rn(t, __fmul_rn(wv1, r1));
+                v[j] = __fadd_rn(t, __fmul_rn(wv2, r2));
+            } else {
+                v[j] = fmaf(wv2, r2, fmaf(wv1, r1, wv0 * r0));
+            }
+        }
+        float o;
+        if (EXACT) {
+            float t = __fadd_rn(0.0f, __fmul_rn(wh0, v[0]));
+            t = __fadd_rn(t, __fmul_rn(wh1, v[1]));
+            o = __fadd_rn(t, __fmul_rn(wh2, v[2]));
+        } else {
+            o = fmaf(wh2, v[2], fmaf(wh1, v[1], wh0 * v[0]));
+        }
+        out[b * out_image_stride + y * out_pitch + x] = o;
+    }
+}
+
+cudaError_t launch_generic_sep(bool exact, const float* in, int64_t in_pitch, int64_t in_image_stride, float* out,
+                               int64_t out_pitch, int64_t out_image_stride, int64_t n, int64_t m, int64_t batch,
+                               const float* wv, const float* wh, int num_sms, cudaStream_t stream) {
+    const int64_t total = batch * n * m;
+    int64_t blocks = (total + 255) / 256;
+    const int64_t cap = int64_t(num_sms) * 16;
+    if (blocks > cap) blocks = cap;
+    if (exact)
+        sep_generic_kernel<true><<<unsigned(blocks), 256, 0, stream>>>(in, in_pitch, in_image_stride, out, out_pitch,
+                                                                       out_image_stride, n, m, batch, wv[0], wv[1],
+                                                                       wv[2], wh[0], wh[1], wh[2]);
+    else
+        sep_generic_kernel<false><<<unsigned(blocks), 256, 0, stream>>>(in, in_pitch, in_image_stride, out,
+                                                                        out_pitch, out_image_stride, n, m, batch,
+                                                                        wv[0], wv[1], wv[2], wh[0], wh[1], wh[2]);
+    return cudaGetLastError();
+}
+
+}  // namespace harris

@@ -68,9 +68,10 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     strip_kernel(const __grid_constant__ CUtensorMap tmap, const TileGeom g, const typename Op::Params p) {
     constexpr int CH = Op::kRowsPerStage;
     constexpr int HALO = Op::kHaloRows;
-    extern __shared__ unsigned char smem_raw[];
-    unsigned char* base =
-        reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    // align by offsetting the __shared__ array itself (an integer round trip would turn
+    // every stage read into a generic LD instead of LDS)
+    unsigned char* base = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;

@@ -233,6 +233,42 @@ def harris_u8(rgb8, kappa: float = KAPPA, *, out: Optional[torch.Tensor] = None,
     return out
 
 
+BINOMIAL = (1.0, 2.0, 1.0)  # weightsV = weightsH of the reference (evalref.py:112-115)
+
+
+def stencil3x3_sep(img: torch.Tensor, wv=BINOMIAL, wh=BINOMIAL, *, out: Optional[torch.Tensor] = None,
+                   exact: bool = False, force_generic: bool = False, force_tma: bool = False,
+                   stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """Separable 3x3 stencil ``(H, W)`` / ``(B, H, W)`` float32 CUDA -> ``(H-2, W-2)`` /
+    ``(B, H-2, W-2)``: vertical ``wv`` then horizontal ``wh`` (the separated form of the
+    reference's binomial rewrite goal)."""
+    if img.dtype != torch.float32 or not img.is_cuda or img.dim() not in (2, 3):
+        raise ValueError("img must be a (H, W) or (B, H, W) float32 CUDA tensor")
+    H, W = img.shape[-2:]
+    if H < 3 or W < 3:
+        raise ValueError("stencil3x3 needs at least 3x3")
+    if img.stride(-1) != 1:
+        img = img.contiguous()
+    batched = img.dim() == 3
+    B = img.shape[0] if batched else 1
+    n, m = H - 2, W - 2
+    if out is None:
+        out = torch.empty((B, n, m) if batched else (n, m), dtype=torch.float32, device=img.device)
+    elif tuple(out.shape) != ((B, n, m) if batched else (n, m)) or out.stride(-1) != 1:
+        raise ValueError("out has the wrong shape or column stride")
+    fwv = (ctypes.c_float * 3)(*[float(v) for v in wv])
+    fwh = (ctypes.c_float * 3)(*[float(v) for v in wh])
+    dev = img.device.index if img.device.index is not None else torch.cuda.current_device()
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    ctx = context(dev)
+    rc = lib().harris_stencil3x3_sep(ctx.handle, out.data_ptr(), out.stride(-2),
+                                     out.stride(0) if batched else n * out.stride(-2), n, m, img.data_ptr(),
+                                     img.stride(-2), img.stride(0) if batched else H * img.stride(-2), B,
+                                     fwv, fwh, _flags(exact, force_generic, force_tma), st.cuda_stream)
+    check(rc, "harris_stencil3x3_sep", ctx.handle)
+    return out
+
+
 GROUPINGS = {
     1: "[Sx],[Sy],[x],[+],[coarsity]",
     2: "[Sx,Sy,x],[+,coarsity]",
@@ -302,5 +338,5 @@ def algorithmic_bytes(n: int, m: int, batch: int = 1) -> int:
     return batch * (12 * (n + 4) * (m + 4) + 4 * n * m)
 
 
-__all__ = ["HarrisContext", "context", "harris", "harris_u8", "harris_grouping", "grouping_hbm_bytes", "GROUPINGS", "synth_",
+__all__ = ["HarrisContext", "context", "harris", "harris_u8", "stencil3x3_sep", "BINOMIAL", "harris_grouping", "grouping_hbm_bytes", "GROUPINGS", "synth_",
            "algorithmic_bytes", "KAPPA", "_lib"]

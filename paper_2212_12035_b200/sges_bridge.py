@@ -72,6 +72,40 @@ def register(env: dict, amb: dict, impl: Optional[Callable[[np.ndarray], np.ndar
     return env, amb
 
 
+BINOMIAL_SCHEME = "(?n+2).(?m+2).f32 -> ?n.?m.f32"
+
+
+def gpu_binomial_impl() -> Callable[[np.ndarray], np.ndarray]:
+    import torch
+
+    from .harris import stencil3x3_sep
+
+    def run(img: np.ndarray) -> np.ndarray:
+        t = torch.from_numpy(np.ascontiguousarray(img, dtype=np.float32)).cuda()
+        return stencil3x3_sep(t).cpu().numpy()
+
+    return run
+
+
+def register_binomial(env: dict, amb: dict, impl: Optional[Callable[[np.ndarray], np.ndarray]] = None,
+                      reference_src: Optional[str] = None) -> tuple[dict, dict]:
+    """Register ``binomial`` (the reference's separated binomial goal as one primitive,
+    PAPER.md:3935-4016) with scheme ``(?n+2).(?m+2).f32 -> ?n.?m.f32``; ``impl`` defaults
+    to the separable-stencil kernel on the B200."""
+    parser, _, _ = _sges(reference_src)
+    fn = impl or gpu_binomial_impl()
+    env["binomial"] = parser.parse_type(BINOMIAL_SCHEME)
+
+    def _call(img_lists):
+        arr = np.asarray(img_lists, dtype=np.float32)
+        if arr.ndim != 2 or arr.shape[0] < 3 or arr.shape[1] < 3:
+            raise ValueError(f"binomial needs an (n+2) x (m+2) input with n, m >= 1, got {arr.shape}")
+        return np.asarray(fn(arr), dtype=np.float64).tolist()
+
+    amb["binomial"] = _call
+    return env, amb
+
+
 def evaluate(src: str, env: dict, amb: dict, sizes=(), nenv: Optional[dict] = None,
              reference_src: Optional[str] = None):
     """Parse, type and evaluate a Rise program that may call ``harris``."""

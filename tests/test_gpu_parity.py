@@ -305,3 +305,61 @@ def test_u8_batched_and_host(cuda_ctx):
     fast = hb.harris_u8(big[0])
     ok, m = synth.within_tolerance(fast, cref.harris_f64(bigf[0]))
     assert ok, m
+
+
+# ------------------------------------------------ separable 3x3 (binomial) stencil
+@pytest.mark.parametrize("H,W", [(3, 4), (5, 9), (7, 132), (40, 130), (133, 520), (300, 1030)])
+@pytest.mark.parametrize("generic", [False, True])
+def test_stencil_exact_bitexact(cuda_ctx, H, W, generic):
+    img = synth.synth_numpy(1, H, W, seed=H * 7 + W)[0]
+    got = hb.stencil3x3_sep(_dev(img), exact=True, force_generic=generic)
+    assert cuda_ctx.last_path == (_lib.PATH_GENERIC if generic or (W % 4) else _lib.PATH_TMA)
+    torch.cuda.synchronize()
+    assert np.array_equal(got.cpu().numpy(), cref.sep3x3_f32(img))
+
+
+@pytest.mark.parametrize("H,W", [(40, 132), (517, 1036)])
+def test_stencil_fast_and_weights(cuda_ctx, H, W):
+    img = synth.synth_numpy(1, H, W, seed=H + W)[0]
+    for wv, wh in (((1, 2, 1), (1, 2, 1)), ((0.25, 0.5, 0.25), (-1.0, 0.0, 1.0))):
+        got = hb.stencil3x3_sep(_dev(img), wv, wh)
+        torch.cuda.synchronize()
+        ref = cref.sep3x3_f64(img, wv, wh)
+        assert np.max(np.abs(got.cpu().numpy() - ref)) <= 1e-6 * max(1.0, np.max(np.abs(ref)))
+        ex = hb.stencil3x3_sep(_dev(img), wv, wh, exact=True)
+        torch.cuda.synchronize()
+        assert np.array_equal(ex.cpu().numpy(), cref.sep3x3_f32(img, wv, wh))
+
+
+def test_stencil_golden_and_integer_exact(cuda_ctx):
+    import json
+    import os
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    meta = json.load(open(os.path.join(here, "binomial_golden.json")))
+    arrays = dict(np.load(os.path.join(here, "binomial_golden.npz")))
+    for case in meta["cases"]:
+        if case["kind"] != "synth" or f"{case['name']}_separated" not in arrays:
+            continue
+        img = synth.synth_numpy(1, case["H"], case["W"], seed=case["seed"], dist=case["dist"])[0]
+        got = hb.stencil3x3_sep(_dev(img))
+        torch.cuda.synchronize()
+        assert synth.norm_linf(got.cpu().numpy(), arrays[f"{case['name']}_separated"]) <= 1e-6, case["name"]
+    img = arrays["binom_int_input"]
+    for kw in ({}, {"exact": True}, {"force_generic": True}):
+        got = hb.stencil3x3_sep(_dev(img), **kw)
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy(), arrays["binom_int_initial"]), kw
+
+
+def test_stencil_batched_and_views(cuda_ctx):
+    B, H, W = 4, 50, 260
+    imgs = synth.synth_numpy(B, H, W, seed=31)
+    x = _dev(imgs)
+    got = hb.stencil3x3_sep(x, exact=True)
+    assert cuda_ctx.last_path == _lib.PATH_TMA
+    torch.cuda.synchronize()
+    for b in range(B):
+        assert np.array_equal(got[b].cpu().numpy(), cref.sep3x3_f32(imgs[b]))
+    band = hb.stencil3x3_sep(x[1, 10:30], exact=True)
+    torch.cuda.synchronize()
+    assert torch.equal(band, got[1, 10:28])
