@@ -30,7 +30,8 @@ struct harris_ctx {
     int cc_major = 0, cc_minor = 0;
     int tma_cfg = 0;
     int u8_cfg = 0;
-    int occ_sep = 0;
+    int sep_cfg = 0;
+    int occ_sep[kNumSepConfigs] = {0};
     int occ_u8[kNumU8Configs] = {0};
     int l2_policy = 1;  // evict_normal: the 4-column halo sectors are re-read by the neighbouring strip
     int64_t force_band_rows = 0;  // dev knob (HARRIS_BAND_ROWS): override the planner
@@ -121,8 +122,9 @@ bool tma_eligible(const Call& c) {
 // Pick the band height that minimises (waves x rows-per-tile) for a persistent
 // grid of `gw` warps: tiles = batch x bands x col_segments.
 void plan_tiles(int64_t n, int64_t m, int64_t batch, int64_t gw, int rows_per_stage, int64_t force_rows,
-                TileGeom& tg, int halo = 4) {
-    const int64_t colsegs = (m + kWarpCols - 1) / kWarpCols;
+                TileGeom& tg, int halo = 4, int groups = 1) {
+    const int64_t strip = int64_t(kWarpCols) * groups;
+    const int64_t colsegs = (m + strip - 1) / strip;
     if (force_rows > 0) {
         const int64_t rows = std::min(force_rows, n);
         tg.n = int32_t(n);
@@ -168,7 +170,8 @@ void plan_launch(const harris_ctx* ctx, const Call& c, TileGeom& tg, int64_t& gr
     const TmaConfig& cfg = u8 ? kU8Configs[ctx->u8_cfg] : kTmaConfigs[ctx->tma_cfg];
     const int occ = std::max(1, u8 ? ctx->occ_u8[ctx->u8_cfg] : ctx->occ[ctx->tma_cfg]);
     const int64_t resident_ctas = int64_t(ctx->num_sms) * occ;
-    plan_tiles(c.g.n, c.g.m, c.g.batch, resident_ctas * cfg.warps, cfg.rows, ctx->force_band_rows, tg);
+    plan_tiles(c.g.n, c.g.m, c.g.batch, resident_ctas * cfg.warps, cfg.rows, ctx->force_band_rows, tg, 4,
+               cfg.groups);
     grid = std::min<int64_t>((tg.tiles + cfg.warps - 1) / cfg.warps, resident_ctas);
     tg.out = c.g.out;
     tg.out_pitch = c.g.out_pitch;
@@ -185,7 +188,7 @@ int encode_tmap_u8(harris_ctx* ctx, const Call& c, CUtensorMap* tmap) {
     cuuint64_t dims[3] = {cuuint64_t((3 * (g.m + 4) + 3) / 4), cuuint64_t(g.n + 4), cuuint64_t(g.batch)};
     const int64_t img_stride = g.batch > 1 ? g.in_image_stride : (g.n + 4) * g.in_pitch;
     cuuint64_t strides[2] = {cuuint64_t(g.in_pitch), cuuint64_t((img_stride + 15) / 16 * 16)};
-    cuuint32_t box[3] = {cuuint32_t(kU8BoxWords), cuuint32_t(cfg.rows), 1};
+    cuuint32_t box[3] = {cuuint32_t(cfg.groups == 2 ? 196 : kU8BoxWords), cuuint32_t(cfg.rows), 1};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = ctx->encode(tmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<float*>(g.rgb), dims, strides, box,
                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -322,6 +325,11 @@ int harris_init(harris_ctx** out_ctx, int cuda_device) {
         int v = std::atoi(env);
         if (v >= 0 && v < kNumU8Configs) ctx->u8_cfg = v;
     }
+    env = std::getenv("HARRIS_SEP_CONFIG");
+    if (env) {
+        int v = std::atoi(env);
+        if (v >= 0 && v < kNumSepConfigs) ctx->sep_cfg = v;
+    }
     env = std::getenv("HARRIS_BAND_ROWS");
     if (env) ctx->force_band_rows = std::atoll(env);
     env = std::getenv("HARRIS_L2_POLICY");
@@ -347,11 +355,13 @@ int harris_init(harris_ctx** out_ctx, int cuda_device) {
             return rc;
         }
     }
-    e = sep_configure(&ctx->occ_sep);
-    if (e != cudaSuccess) {
-        int rc = cuda_fail(ctx, e, "configure stencil kernel");
-        delete ctx;
-        return rc;
+    for (int k = 0; k < kNumSepConfigs; ++k) {
+        e = sep_configure(k, &ctx->occ_sep[k]);
+        if (e != cudaSuccess) {
+            int rc = cuda_fail(ctx, e, "configure stencil kernel");
+            delete ctx;
+            return rc;
+        }
     }
     for (int k = 0; k < kNumU8Configs; ++k) {
         e = u8_configure(k);
@@ -437,7 +447,8 @@ int harris_stencil3x3_sep(harris_ctx* ctx, float* out, int64_t out_pitch, int64_
         CUtensorMap tmap;
         cuuint64_t dims[3] = {cuuint64_t(m + 2), cuuint64_t(n + 2), cuuint64_t(batch)};
         cuuint64_t strides[2] = {cuuint64_t(in_pitch) * 4, cuuint64_t((img_stride + 3) / 4 * 4) * 4};
-        cuuint32_t box[3] = {cuuint32_t(kBoxCols), cuuint32_t(kSepConfig.rows), 1};
+        const TmaConfig& scfg = kSepConfigs[ctx->sep_cfg];
+        cuuint32_t box[3] = {cuuint32_t(kBoxCols), cuuint32_t(scfg.rows), 1};
         cuuint32_t estr[3] = {1, 1, 1};
         CUresult r = ctx->encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(in), dims, strides,
                                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -447,9 +458,9 @@ int harris_stencil3x3_sep(harris_ctx* ctx, float* out, int64_t out_pitch, int64_
             return HARRIS_ERR_TMA;
         }
         TileGeom tg;
-        const int64_t resident = int64_t(ctx->num_sms) * std::max(1, ctx->occ_sep);
-        plan_tiles(n, m, batch, resident * kSepConfig.warps, kSepConfig.rows, ctx->force_band_rows, tg, 2);
-        const int64_t grid = std::min<int64_t>((tg.tiles + kSepConfig.warps - 1) / kSepConfig.warps, resident);
+        const int64_t resident = int64_t(ctx->num_sms) * std::max(1, ctx->occ_sep[ctx->sep_cfg]);
+        plan_tiles(n, m, batch, resident * scfg.warps, scfg.rows, ctx->force_band_rows, tg, 2);
+        const int64_t grid = std::min<int64_t>((tg.tiles + scfg.warps - 1) / scfg.warps, resident);
         tg.out = out;
         tg.out_pitch = out_pitch;
         tg.out_image_stride = batch > 1 ? out_image_stride : n * out_pitch;
@@ -457,7 +468,7 @@ int harris_stencil3x3_sep(harris_ctx* ctx, float* out, int64_t out_pitch, int64_
         tg.l2_policy = ctx->l2_policy;
         tg.vec_store = aligned16(out) && (out_pitch & 3) == 0 && (batch == 1 || (out_image_stride & 3) == 0);
         tg.pad_ = 0;
-        e = launch_tma_sep(exact, tmap, tg, grid, wv, wh, stream);
+        e = launch_tma_sep(ctx->sep_cfg, exact, tmap, tg, grid, wv, wh, stream);
     } else {
         e = launch_generic_sep(exact, in, in_pitch, img_stride, out, out_pitch,
                                batch > 1 ? out_image_stride : n * out_pitch, n, m, batch, wv, wh, ctx->num_sms,

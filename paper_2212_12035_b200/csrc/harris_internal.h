@@ -35,8 +35,9 @@ struct TileGeom {
 // per stage).  Index 0 is the default; HARRIS_TMA_CONFIG selects another one.
 struct TmaConfig {
     int warps, stages, rows;
+    int groups = 1;  // 128-column strips per tile (2: packed FP32x2 dual-strip op)
 };
-constexpr int kNumTmaConfigs = 4;
+constexpr int kNumTmaConfigs = 8;
 extern const TmaConfig kTmaConfigs[kNumTmaConfigs];
 
 size_t tma_smem_bytes(int cfg);
@@ -49,7 +50,7 @@ cudaError_t launch_generic(bool exact, const Geom& g, cudaStream_t stream);
 
 // interleaved RGB u8 (HWC) input: TMA configs + generic fallback (Geom.rgb is then the
 // byte base pointer; in_pitch / in_image_stride are in BYTES, in_chan_stride unused)
-constexpr int kNumU8Configs = 3;
+constexpr int kNumU8Configs = 5;
 extern const TmaConfig kU8Configs[kNumU8Configs];
 size_t u8_smem_bytes(int cfg);
 cudaError_t u8_configure(int cfg);
@@ -59,10 +60,11 @@ cudaError_t launch_tma_u8(int cfg, bool exact, const CUtensorMap& tmap, const Ti
 cudaError_t launch_generic_u8(bool exact, const Geom& g, cudaStream_t stream);
 
 // separable 3x3 stencil on one f32 plane (stencil_sep.cu)
-extern const TmaConfig kSepConfig;
-cudaError_t sep_configure(int* ctas_per_sm);
-cudaError_t launch_tma_sep(bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid, const float* wv,
-                           const float* wh, cudaStream_t stream);
+constexpr int kNumSepConfigs = 3;
+extern const TmaConfig kSepConfigs[kNumSepConfigs];
+cudaError_t sep_configure(int cfg, int* ctas_per_sm);
+cudaError_t launch_tma_sep(int cfg, bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid,
+                           const float* wv, const float* wh, cudaStream_t stream);
 cudaError_t launch_generic_sep(bool exact, const float* in, int64_t in_pitch, int64_t in_image_stride, float* out,
                                int64_t out_pitch, int64_t out_image_stride, int64_t n, int64_t m, int64_t batch,
                                const float* wv, const float* wh, int num_sms, cudaStream_t stream);

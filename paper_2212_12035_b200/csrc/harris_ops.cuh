@@ -136,6 +136,7 @@ __device__ __forceinline__ float gray_of(float r, float g, float b) {
 template <bool EXACT, int CH>
 struct HarrisF32Op {
     static_assert(CH % 3 == 0, "row rotation needs CH % 3 == 0");
+    static constexpr int kGroups = 1;
     static constexpr int kRowsPerStage = CH;
     static constexpr int kHaloRows = 4;
     static constexpr uint32_t kTxBytes = 3u * CH * kBoxCols * 4u;
@@ -153,7 +154,7 @@ struct HarrisF32Op {
     }
 
     template <int R>
-    __device__ __forceinline__ void row(const unsigned char* stage, int lane, float (&out)[4]) {
+    __device__ __forceinline__ void row(const unsigned char* stage, int lane, float (&out)[1][4]) {
         const float* sm = reinterpret_cast<const float*>(stage);
         const float* pr = sm + (0 * CH + R) * kBoxCols;
         const float* pg = sm + (1 * CH + R) * kBoxCols;
@@ -167,7 +168,7 @@ struct HarrisF32Op {
             h1 = gray_of<EXACT>(r2.y, g2.y, b2.y);
             h2 = gray_of<EXACT>(r2.z, g2.z, b2.z);
             h3 = gray_of<EXACT>(r2.w, g2.w, b2.w);
-        }, out);
+        }, out[0]);
     }
 };
 
@@ -203,6 +204,7 @@ __device__ __forceinline__ void gray4_u8(uint32_t w0, uint32_t w1, uint32_t w2, 
 template <bool EXACT, int CH>
 struct HarrisU8Op {
     static_assert(CH % 3 == 0, "row rotation needs CH % 3 == 0");
+    static constexpr int kGroups = 1;
     static constexpr int kRowsPerStage = CH;
     static constexpr int kHaloRows = 4;
     static constexpr uint32_t kTxBytes = uint32_t(CH) * kU8BoxWords * 4u;
@@ -221,13 +223,13 @@ struct HarrisU8Op {
     }
 
     template <int R>
-    __device__ __forceinline__ void row(const unsigned char* stage, int lane, float (&out)[4]) {
+    __device__ __forceinline__ void row(const unsigned char* stage, int lane, float (&out)[1][4]) {
         const uint32_t* w = reinterpret_cast<const uint32_t*>(stage) + R * kU8BoxWords;
         float gown[4];
         gray4_u8<EXACT>(w[3 * lane], w[3 * lane + 1], w[3 * lane + 2], gown[0], gown[1], gown[2], gown[3]);
         core.template step<R>(gown, lane, [&](float& h0, float& h1, float& h2, float& h3) {
             gray4_u8<EXACT>(w[96], w[97], w[98], h0, h1, h2, h3);
-        }, out);
+        }, out[0]);
     }
 };
 

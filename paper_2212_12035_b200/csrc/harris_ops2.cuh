@@ -1,0 +1,309 @@
+// harris_ops2.cuh — dual-strip Harris ops with packed FP32x2 arithmetic.
+//
+// A tile is TWO adjacent 128-column strips (kGroups = 2): lane l owns columns
+// [4l, 4l+4) of strip A and the same columns of strip B.  Every operation of the
+// Harris row step is identical for A and B, so the pair (A, B) is carried in one
+// float2 and evaluated with sm_100's packed instructions (__ffma2_rn /
+// __fadd2_rn / __fmul2_rn -> FFMA2 / FADD2 / FMUL2): half the FP instructions per
+// pixel of the scalar core, which keeps the kernel HBM-bound even when the SM
+// clock drops under the power cap (the scalar core becomes per-warp-latency
+// bound there; tools/variance.py).
+//
+// Arithmetic is the same contract as harris_ops.cuh:
+//   FAST : separable Sobel, fused product+pair-sum box rows, FMAs.
+//   EXACT: Appendix-B 9-tap orders with packed *_rn ops (each element rounded
+//          exactly like the scalar __fmul_rn/__fadd_rn), bit-exact with the oracle.
+// a - b is evaluated as fma(b, -1, a): one rounding of the exact difference, i.e.
+// identical to FSUB.
+#pragma once
+#include <cuda.h>
+
+#include <cstdint>
+
+#include "harris_common.cuh"
+#include "harris_ops.cuh"
+
+namespace harris {
+
+__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __ffma2_rn(b, f2(-1.0f), a); }
+
+__device__ __forceinline__ float2 shfl_down2(float2 v) {
+    return make_float2(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1));
+}
+
+// exact Appendix-B pieces on pairs
+__device__ __forceinline__ float2 gray_exact2(float2 r, float2 g, float2 b) {
+    float2 t = add2(f2(0.0f), mul2(f2(kGrayR), r));
+    t = add2(t, mul2(f2(kGrayG), g));
+    return add2(t, mul2(f2(kGrayB), b));
+}
+
+__device__ __forceinline__ float2 conv9_exact2(const float (&w)[9], float2 a0, float2 a1, float2 a2, float2 b0,
+                                               float2 b1, float2 b2, float2 c0, float2 c1, float2 c2) {
+    float2 t = f2(0.0f);
+    t = add2(t, mul2(f2(w[0]), a0));
+    t = add2(t, mul2(f2(w[1]), a1));
+    t = add2(t, mul2(f2(w[2]), a2));
+    t = add2(t, mul2(f2(w[3]), b0));
+    t = add2(t, mul2(f2(w[4]), b1));
+    t = add2(t, mul2(f2(w[5]), b2));
+    t = add2(t, mul2(f2(w[6]), c0));
+    t = add2(t, mul2(f2(w[7]), c1));
+    t = add2(t, mul2(f2(w[8]), c2));
+    return t;
+}
+
+__device__ __forceinline__ float2 sum9_exact2(float2 a0, float2 a1, float2 a2, float2 b0, float2 b1, float2 b2,
+                                              float2 c0, float2 c1, float2 c2) {
+    float2 s = add2(f2(0.0f), a0);
+    s = add2(s, a1);
+    s = add2(s, a2);
+    s = add2(s, b0);
+    s = add2(s, b1);
+    s = add2(s, b2);
+    s = add2(s, c0);
+    s = add2(s, c1);
+    return add2(s, c2);
+}
+
+__device__ __forceinline__ float2 coarsity_exact2(float2 sxx, float2 sxy, float2 syy, float k) {
+    const float2 det = sub2(mul2(sxx, syy), mul2(sxy, sxy));
+    const float2 tr = add2(sxx, syy);
+    return sub2(det, mul2(mul2(f2(k), tr), tr));
+}
+
+template <bool EXACT>
+struct HarrisCore2 {
+    float kappa;
+    float2 D[3][6], Hs[3][6], HB[3][12];   // FAST
+    float2 G3[3][8], P[3][18];             // EXACT
+
+    __device__ __forceinline__ explicit HarrisCore2(float k) : kappa(k) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+#pragma unroll
+            for (int j = 0; j < 6; ++j) D[a][j] = Hs[a][j] = f2(0.f);
+#pragma unroll
+            for (int j = 0; j < 12; ++j) HB[a][j] = f2(0.f);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) G3[a][j] = f2(0.f);
+#pragma unroll
+            for (int j = 0; j < 18; ++j) P[a][j] = f2(0.f);
+        }
+    }
+
+    // products a*b of 6 columns folded into 4 horizontal 3-sums (shared pairs)
+    __device__ __forceinline__ static void prodsum4(const float2 (&a)[6], const float2 (&b)[6], float2& o0,
+                                                    float2& o1, float2& o2, float2& o3) {
+        const float2 q1 = fma2(a[1], b[1], mul2(a[2], b[2]));
+        const float2 q3 = fma2(a[3], b[3], mul2(a[4], b[4]));
+        o0 = fma2(a[0], b[0], q1);
+        o1 = fma2(a[3], b[3], q1);
+        o2 = fma2(a[2], b[2], q3);
+        o3 = fma2(a[5], b[5], q3);
+    }
+
+    // gown: (A, B) gray of this lane's 4 columns; halo(h0..h3) fills the right halo of
+    // both strips for lane 31
+    template <int R, class HaloFn>
+    __device__ __forceinline__ void step(const float2 (&gown)[4], int lane, HaloFn&& halo, float (&out)[2][4]) {
+        constexpr int s2 = R % 3, s0 = (R + 1) % 3, s1 = (R + 2) % 3;
+        float2 g[8];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) g[k] = gown[k];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) g[4 + k] = shfl_down2(g[k]);
+        if (lane == 31) halo(g[4], g[5], g[6], g[7]);
+        if constexpr (!EXACT) {
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+                D[s2][k] = sub2(g[k + 2], g[k]);
+                Hs[s2][k] = add2(fma2(f2(2.f), g[k + 1], g[k]), g[k + 2]);
+            }
+            float2 ix[6], iy[6];
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+                ix[k] = fma2(f2(2.f), D[s1][k], add2(D[s0][k], D[s2][k]));
+                iy[k] = sub2(Hs[s2][k], Hs[s0][k]);
+            }
+            prodsum4(ix, ix, HB[s2][0], HB[s2][1], HB[s2][2], HB[s2][3]);
+            prodsum4(ix, iy, HB[s2][4], HB[s2][5], HB[s2][6], HB[s2][7]);
+            prodsum4(iy, iy, HB[s2][8], HB[s2][9], HB[s2][10], HB[s2][11]);
+            const float2 kk = f2(kappa);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float2 sxx = add2(add2(HB[s0][0 + j], HB[s1][0 + j]), HB[s2][0 + j]);
+                const float2 sxy = add2(add2(HB[s0][4 + j], HB[s1][4 + j]), HB[s2][4 + j]);
+                const float2 syy = add2(add2(HB[s0][8 + j], HB[s1][8 + j]), HB[s2][8 + j]);
+                const float2 tr = add2(sxx, syy);
+                const float2 t2 = fma2(sxy, sxy, mul2(mul2(kk, tr), tr));
+                const float2 o = sub2(mul2(sxx, syy), t2);
+                out[0][j] = o.x;
+                out[1][j] = o.y;
+            }
+        } else {
+            const float WX[9] = {-kSobA, 0.f, kSobA, -kSobB, 0.f, kSobB, -kSobA, 0.f, kSobA};
+            const float WY[9] = {-kSobA, -kSobB, -kSobA, 0.f, 0.f, 0.f, kSobA, kSobB, kSobA};
+#pragma unroll
+            for (int k = 0; k < 8; ++k) G3[s2][k] = g[k];
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+                const float2 ix = conv9_exact2(WX, G3[s0][k], G3[s0][k + 1], G3[s0][k + 2], G3[s1][k],
+                                               G3[s1][k + 1], G3[s1][k + 2], G3[s2][k], G3[s2][k + 1], G3[s2][k + 2]);
+                const float2 iy = conv9_exact2(WY, G3[s0][k], G3[s0][k + 1], G3[s0][k + 2], G3[s1][k],
+                                               G3[s1][k + 1], G3[s1][k + 2], G3[s2][k], G3[s2][k + 1], G3[s2][k + 2]);
+                P[s2][k] = mul2(ix, ix);
+                P[s2][6 + k] = mul2(ix, iy);
+                P[s2][12 + k] = mul2(iy, iy);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                float2 sq[3];
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const int o = q * 6 + j;
+                    sq[q] = sum9_exact2(P[s0][o], P[s0][o + 1], P[s0][o + 2], P[s1][o], P[s1][o + 1], P[s1][o + 2],
+                                        P[s2][o], P[s2][o + 1], P[s2][o + 2]);
+                }
+                const float2 o = coarsity_exact2(sq[0], sq[1], sq[2], kappa);
+                out[0][j] = o.x;
+                out[1][j] = o.y;
+            }
+        }
+    }
+};
+
+template <bool EXACT>
+__device__ __forceinline__ float2 gray2_of(float2 r, float2 g, float2 b) {
+    if constexpr (EXACT)
+        return gray_exact2(r, g, b);
+    else
+        return fma2(f2(kGrayB12), b, fma2(f2(kGrayG12), g, mul2(f2(kGrayR12), r)));
+}
+
+// ------------------------------------------------------------ planar RGB f32
+// Two TMA boxes per stage ({132 cols, CH rows, 3 channels, 1 image} at x and x+128).
+template <bool EXACT, int CH>
+struct HarrisF32x2Op {
+    static_assert(CH % 3 == 0, "row rotation needs CH % 3 == 0");
+    static constexpr int kGroups = 2;
+    static constexpr int kRowsPerStage = CH;
+    static constexpr int kHaloRows = 4;
+    static constexpr uint32_t kBoxBytes = 3u * CH * kBoxCols * 4u;
+    static constexpr uint32_t kBoxStride = (kBoxBytes + 127u) / 128u * 128u;
+    static constexpr uint32_t kTxBytes = 2u * kBoxBytes;
+    static constexpr uint32_t kStageBytes = 2u * kBoxStride;
+    struct Params {
+        float kappa;
+    };
+    HarrisCore2<EXACT> core;
+
+    __device__ __forceinline__ explicit HarrisF32x2Op(const Params& p) : core(p.kappa) {}
+
+    __device__ __forceinline__ static void load(void* smem, const CUtensorMap* tmap, uint64_t* bar, int col0,
+                                                int row0, int image, uint64_t policy) {
+        tma_load_4d(smem, tmap, bar, col0, row0, 0, image, policy);
+        tma_load_4d(static_cast<unsigned char*>(smem) + kBoxStride, tmap, bar, col0 + kWarpCols, row0, 0, image,
+                    policy);
+    }
+
+    template <int R>
+    __device__ __forceinline__ void row(const unsigned char* stage, int lane, float (&out)[2][4]) {
+        const float* a = reinterpret_cast<const float*>(stage);
+        const float* b = reinterpret_cast<const float*>(stage + kBoxStride);
+        const int o_r = (0 * CH + R) * kBoxCols, o_g = (1 * CH + R) * kBoxCols, o_b = (2 * CH + R) * kBoxCols;
+        const float4 ra = lds128(a + o_r + lane * 4), ga = lds128(a + o_g + lane * 4), ba = lds128(a + o_b + lane * 4);
+        const float4 rb = lds128(b + o_r + lane * 4), gb = lds128(b + o_g + lane * 4), bb = lds128(b + o_b + lane * 4);
+        const float2 gown[4] = {
+            gray2_of<EXACT>(make_float2(ra.x, rb.x), make_float2(ga.x, gb.x), make_float2(ba.x, bb.x)),
+            gray2_of<EXACT>(make_float2(ra.y, rb.y), make_float2(ga.y, gb.y), make_float2(ba.y, bb.y)),
+            gray2_of<EXACT>(make_float2(ra.z, rb.z), make_float2(ga.z, gb.z), make_float2(ba.z, bb.z)),
+            gray2_of<EXACT>(make_float2(ra.w, rb.w), make_float2(ga.w, gb.w), make_float2(ba.w, bb.w))};
+        core.template step<R>(gown, lane, [&](float2& h0, float2& h1, float2& h2, float2& h3) {
+            const float4 r2a = lds128(a + o_r + kWarpCols), g2a = lds128(a + o_g + kWarpCols),
+                         b2a = lds128(a + o_b + kWarpCols);
+            const float4 r2b = lds128(b + o_r + kWarpCols), g2b = lds128(b + o_g + kWarpCols),
+                         b2b = lds128(b + o_b + kWarpCols);
+            h0 = gray2_of<EXACT>(make_float2(r2a.x, r2b.x), make_float2(g2a.x, g2b.x), make_float2(b2a.x, b2b.x));
+            h1 = gray2_of<EXACT>(make_float2(r2a.y, r2b.y), make_float2(g2a.y, g2b.y), make_float2(b2a.y, b2b.y));
+            h2 = gray2_of<EXACT>(make_float2(r2a.z, r2b.z), make_float2(g2a.z, g2b.z), make_float2(b2a.z, b2b.z));
+            h3 = gray2_of<EXACT>(make_float2(r2a.w, r2b.w), make_float2(g2a.w, g2b.w), make_float2(b2a.w, b2b.w));
+        }, out);
+    }
+};
+
+// --------------------------------------------------- interleaved RGB u8 (HWC)
+constexpr int kU8x2BoxWords = 196;  // 784 bytes >= 260 px * 3 B; <= 256 TMA elements
+
+// (byte k of wa, byte k of wb) as exact floats: PRMT each, one FADD2 for both
+__device__ __forceinline__ float2 u8f2(uint32_t wa, uint32_t wb, int k) {
+    const float2 m = make_float2(__int_as_float(__byte_perm(wa, 0x4B000000u, 0x7440u | uint32_t(k))),
+                                 __int_as_float(__byte_perm(wb, 0x4B000000u, 0x7440u | uint32_t(k))));
+    return add2(m, f2(-8388608.0f));
+}
+
+template <bool EXACT>
+__device__ __forceinline__ float2 gray2_u8(float2 r, float2 g, float2 b) {
+    if constexpr (EXACT) {
+        const float2 q255 = f2(255.0f);
+        return gray_exact2(make_float2(__fdiv_rn(r.x, q255.x), __fdiv_rn(r.y, q255.y)),
+                           make_float2(__fdiv_rn(g.x, q255.x), __fdiv_rn(g.y, q255.y)),
+                           make_float2(__fdiv_rn(b.x, q255.x), __fdiv_rn(b.y, q255.y)));
+    } else {
+        constexpr float kR = 0.299f / (12.0f * 255.0f), kG = 0.587f / (12.0f * 255.0f),
+                        kB = 0.114f / (12.0f * 255.0f);
+        return fma2(f2(kB), b, fma2(f2(kG), g, mul2(f2(kR), r)));
+    }
+}
+
+// 4 pixels of strips A and B from their 3 words each
+template <bool EXACT>
+__device__ __forceinline__ void gray4_u8x2(const uint32_t (&a)[3], const uint32_t (&b)[3], float2& g0, float2& g1,
+                                           float2& g2, float2& g3) {
+    g0 = gray2_u8<EXACT>(u8f2(a[0], b[0], 0), u8f2(a[0], b[0], 1), u8f2(a[0], b[0], 2));
+    g1 = gray2_u8<EXACT>(u8f2(a[0], b[0], 3), u8f2(a[1], b[1], 0), u8f2(a[1], b[1], 1));
+    g2 = gray2_u8<EXACT>(u8f2(a[1], b[1], 2), u8f2(a[1], b[1], 3), u8f2(a[2], b[2], 0));
+    g3 = gray2_u8<EXACT>(u8f2(a[2], b[2], 1), u8f2(a[2], b[2], 2), u8f2(a[2], b[2], 3));
+}
+
+template <bool EXACT, int CH>
+struct HarrisU8x2Op {
+    static_assert(CH % 3 == 0, "row rotation needs CH % 3 == 0");
+    static constexpr int kGroups = 2;
+    static constexpr int kRowsPerStage = CH;
+    static constexpr int kHaloRows = 4;
+    static constexpr uint32_t kTxBytes = uint32_t(CH) * kU8x2BoxWords * 4u;
+    static constexpr uint32_t kStageBytes = (kTxBytes + 127u) / 128u * 128u;
+    struct Params {
+        float kappa;
+    };
+    HarrisCore2<EXACT> core;
+
+    __device__ __forceinline__ explicit HarrisU8x2Op(const Params& p) : core(p.kappa) {}
+
+    // tensor map over 32-bit words; a 256-column tile starts at word 192 * (col0 / 256)
+    __device__ __forceinline__ static void load(void* smem, const CUtensorMap* tmap, uint64_t* bar, int col0,
+                                                int row0, int image, uint64_t policy) {
+        tma_load_3d(smem, tmap, bar, (col0 / (2 * kWarpCols)) * (2 * kWarpCols * 3 / 4), row0, image, policy);
+    }
+
+    template <int R>
+    __device__ __forceinline__ void row(const unsigned char* stage, int lane, float (&out)[2][4]) {
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(stage) + R * kU8x2BoxWords;
+        const uint32_t a[3] = {w[3 * lane], w[3 * lane + 1], w[3 * lane + 2]};
+        const uint32_t b[3] = {w[96 + 3 * lane], w[97 + 3 * lane], w[98 + 3 * lane]};
+        float2 gown[4];
+        gray4_u8x2<EXACT>(a, b, gown[0], gown[1], gown[2], gown[3]);
+        core.template step<R>(gown, lane, [&](float2& h0, float2& h1, float2& h2, float2& h3) {
+            const uint32_t ha[3] = {w[96], w[97], w[98]};
+            const uint32_t hb[3] = {w[192], w[193], w[194]};
+            gray4_u8x2<EXACT>(ha, hb, h0, h1, h2, h3);
+        }, out);
+    }
+};
+
+}  // namespace harris

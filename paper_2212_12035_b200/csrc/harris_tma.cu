@@ -42,95 +42,124 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "harris_common.cuh"
 #include "harris_internal.h"
 #include "harris_ops.cuh"
+#include "harris_ops2.cuh"
 #include "strip_pipeline.cuh"
 
 namespace harris {
 
+// (warps per CTA, stages per warp, rows per stage, min CTAs per SM); index 0 is the
+// default, HARRIS_TMA_CONFIG selects another (tools/probe_perf.py sweeps them)
+template <int CFG>
+struct F32Cfg;
+// scalar single-strip core
+template <> struct F32Cfg<0> { static constexpr int NW = 8, NS = 3, CH = 3, MINB = 1, G = 1; };
+template <> struct F32Cfg<1> { static constexpr int NW = 8, NS = 2, CH = 3, MINB = 2, G = 1; };
+template <> struct F32Cfg<2> { static constexpr int NW = 4, NS = 3, CH = 3, MINB = 3, G = 1; };
+template <> struct F32Cfg<3> { static constexpr int NW = 4, NS = 4, CH = 3, MINB = 1, G = 1; };
+template <> struct F32Cfg<4> { static constexpr int NW = 4, NS = 3, CH = 6, MINB = 1, G = 1; };
+// packed FP32x2 dual-strip core (harris_ops2.cuh)
+template <> struct F32Cfg<5> { static constexpr int NW = 6, NS = 3, CH = 3, MINB = 1, G = 2; };
+template <> struct F32Cfg<6> { static constexpr int NW = 8, NS = 2, CH = 3, MINB = 1, G = 2; };
+template <> struct F32Cfg<7> { static constexpr int NW = 4, NS = 4, CH = 3, MINB = 1, G = 2; };
+
+template <int CFG, bool EXACT>
+using F32OpOf = std::conditional_t<F32Cfg<CFG>::G == 2, HarrisF32x2Op<EXACT, F32Cfg<CFG>::CH>,
+                                   HarrisF32Op<EXACT, F32Cfg<CFG>::CH>>;
+
+#define HARRIS_CFG_ROW(k) {F32Cfg<k>::NW, F32Cfg<k>::NS, F32Cfg<k>::CH, F32Cfg<k>::G}
 const TmaConfig kTmaConfigs[kNumTmaConfigs] = {
-    {8, 3, 3},  // 0: default, 117 KB smem / CTA, 1 CTA (8 warps) per SM
-    {2, 4, 3},  // 1
-    {4, 3, 6},  // 2
-    {4, 4, 3},  // 3
+    HARRIS_CFG_ROW(0), HARRIS_CFG_ROW(1), HARRIS_CFG_ROW(2), HARRIS_CFG_ROW(3),
+    HARRIS_CFG_ROW(4), HARRIS_CFG_ROW(5), HARRIS_CFG_ROW(6), HARRIS_CFG_ROW(7),
 };
+#undef HARRIS_CFG_ROW
 
-// ------------------------------------------------------------------ host side
-template <int NW, int NS, int CH>
-static constexpr size_t smem_of() {
-    return StripShape<NW, NS, HarrisF32Op<false, CH>>::kSmemBytes;
+template <int CFG, bool EXACT>
+static constexpr auto f32_kernel() {
+    using C = F32Cfg<CFG>;
+    return strip_kernel<F32OpOf<CFG, EXACT>, C::NW, C::NS, C::MINB>;
 }
 
-template <int NW, int NS, int CH>
+template <int CFG>
+static constexpr size_t f32_smem() {
+    using C = F32Cfg<CFG>;
+    return StripShape<C::NW, C::NS, F32OpOf<CFG, false>>::kSmemBytes;
+}
+
+template <int CFG>
 static cudaError_t configure_one() {
-    cudaError_t e = cudaFuncSetAttribute(strip_kernel<HarrisF32Op<false, CH>, NW, NS>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_of<NW, NS, CH>()));
+    cudaError_t e = cudaFuncSetAttribute(f32_kernel<CFG, false>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(f32_smem<CFG>()));
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(strip_kernel<HarrisF32Op<true, CH>, NW, NS>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_of<NW, NS, CH>()));
+    return cudaFuncSetAttribute(f32_kernel<CFG, true>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(f32_smem<CFG>()));
 }
 
-template <int NW, int NS, int CH>
+template <int CFG>
 static cudaError_t launch_one(bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid,
                               cudaStream_t stream) {
-    const dim3 block{unsigned(NW * 32)}, gridd{unsigned(grid)};
+    using C = F32Cfg<CFG>;
+    const dim3 block{unsigned(C::NW * 32)}, gridd{unsigned(grid)};
     if (exact) {
-        const typename HarrisF32Op<true, CH>::Params p{tg.kappa};
-        strip_kernel<HarrisF32Op<true, CH>, NW, NS><<<gridd, block, smem_of<NW, NS, CH>(), stream>>>(tmap, tg, p);
+        const typename F32OpOf<CFG, true>::Params p{tg.kappa};
+        f32_kernel<CFG, true>()<<<gridd, block, f32_smem<CFG>(), stream>>>(tmap, tg, p);
     } else {
-        const typename HarrisF32Op<false, CH>::Params p{tg.kappa};
-        strip_kernel<HarrisF32Op<false, CH>, NW, NS><<<gridd, block, smem_of<NW, NS, CH>(), stream>>>(tmap, tg, p);
+        const typename F32OpOf<CFG, false>::Params p{tg.kappa};
+        f32_kernel<CFG, false>()<<<gridd, block, f32_smem<CFG>(), stream>>>(tmap, tg, p);
     }
     return cudaGetLastError();
 }
 
-template <int NW, int NS, int CH>
+template <int CFG>
 static cudaError_t occupancy_one(int* n) {
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(n, strip_kernel<HarrisF32Op<false, CH>, NW, NS>, NW * 32,
-                                                         smem_of<NW, NS, CH>());
+    using C = F32Cfg<CFG>;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(n, f32_kernel<CFG, false>(), C::NW * 32, f32_smem<CFG>());
 }
 
-size_t tma_smem_bytes(int cfg) {
-    switch (cfg) {
-        case 0: return smem_of<8, 3, 3>();
-        case 1: return smem_of<2, 4, 3>();
-        case 2: return smem_of<4, 3, 6>();
-        case 3: return smem_of<4, 4, 3>();
-        default: return 0;
+#define HARRIS_F32_SWITCH(EXPR_T)       \
+    switch (cfg) {                      \
+        case 0: return EXPR_T(0);       \
+        case 1: return EXPR_T(1);       \
+        case 2: return EXPR_T(2);       \
+        case 3: return EXPR_T(3);       \
+        case 4: return EXPR_T(4);       \
+        case 5: return EXPR_T(5);       \
+        case 6: return EXPR_T(6);       \
+        case 7: return EXPR_T(7);       \
+        default: break;                 \
     }
+
+size_t tma_smem_bytes(int cfg) {
+#define E(k) f32_smem<k>()
+    HARRIS_F32_SWITCH(E)
+#undef E
+    return 0;
 }
 
 cudaError_t tma_configure(int cfg) {
-    switch (cfg) {
-        case 0: return configure_one<8, 3, 3>();
-        case 1: return configure_one<2, 4, 3>();
-        case 2: return configure_one<4, 3, 6>();
-        case 3: return configure_one<4, 4, 3>();
-        default: return cudaErrorInvalidValue;
-    }
+#define E(k) configure_one<k>()
+    HARRIS_F32_SWITCH(E)
+#undef E
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t tma_occupancy(int cfg, int* ctas_per_sm) {
-    switch (cfg) {
-        case 0: return occupancy_one<8, 3, 3>(ctas_per_sm);
-        case 1: return occupancy_one<2, 4, 3>(ctas_per_sm);
-        case 2: return occupancy_one<4, 3, 6>(ctas_per_sm);
-        case 3: return occupancy_one<4, 4, 3>(ctas_per_sm);
-        default: return cudaErrorInvalidValue;
-    }
+#define E(k) occupancy_one<k>(ctas_per_sm)
+    HARRIS_F32_SWITCH(E)
+#undef E
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_tma(int cfg, bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid,
                        cudaStream_t stream) {
-    switch (cfg) {
-        case 0: return launch_one<8, 3, 3>(exact, tmap, tg, grid, stream);
-        case 1: return launch_one<2, 4, 3>(exact, tmap, tg, grid, stream);
-        case 2: return launch_one<4, 3, 6>(exact, tmap, tg, grid, stream);
-        case 3: return launch_one<4, 4, 3>(exact, tmap, tg, grid, stream);
-        default: return cudaErrorInvalidValue;
-    }
+#define E(k) launch_one<k>(exact, tmap, tg, grid, stream)
+    HARRIS_F32_SWITCH(E)
+#undef E
+    return cudaErrorInvalidValue;
 }
 
 }  // namespace harris

@@ -9,18 +9,22 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "harris_common.cuh"
 #include "harris_internal.h"
 #include "harris_ops.cuh"
+#include "harris_ops2.cuh"
 #include "strip_pipeline.cuh"
 
 namespace harris {
 
 const TmaConfig kU8Configs[kNumU8Configs] = {
-    {8, 4, 6},  // 0: default, 2 CTAs (16 warps) per SM (registers capped at 128)
-    {8, 4, 6},  // 1: same ring, 1 CTA per SM (no register cap)
-    {8, 3, 3},  // 2
+    {8, 4, 6, 1},  // 0: scalar core, 2 CTAs (16 warps) per SM (registers capped at 128)
+    {8, 4, 6, 1},  // 1: scalar core, 1 CTA per SM
+    {8, 3, 3, 1},  // 2: scalar core
+    {8, 4, 6, 2},  // 3: packed FP32x2 dual-strip core
+    {8, 3, 3, 2},  // 4: packed FP32x2 dual-strip core
 };
 
 template <int CFG>
@@ -37,17 +41,34 @@ template <>
 struct U8Cfg<2> {
     static constexpr int NW = 8, NS = 3, CH = 3, MINB = 1;
 };
+template <>
+struct U8Cfg<3> {
+    static constexpr int NW = 8, NS = 4, CH = 6, MINB = 1, G = 2;
+};
+template <>
+struct U8Cfg<4> {
+    static constexpr int NW = 8, NS = 3, CH = 3, MINB = 1, G = 2;
+};
+
+template <class C, class = void>
+struct GroupsOf : std::integral_constant<int, 1> {};
+template <class C>
+struct GroupsOf<C, std::void_t<decltype(C::G)>> : std::integral_constant<int, C::G> {};
+
+template <int CFG, bool EXACT>
+using U8OpOf = std::conditional_t<GroupsOf<U8Cfg<CFG>>::value == 2, HarrisU8x2Op<EXACT, U8Cfg<CFG>::CH>,
+                                  HarrisU8Op<EXACT, U8Cfg<CFG>::CH>>;
 
 template <int CFG, bool EXACT>
 static constexpr auto u8_kernel() {
     using C = U8Cfg<CFG>;
-    return strip_kernel<HarrisU8Op<EXACT, C::CH>, C::NW, C::NS, C::MINB>;
+    return strip_kernel<U8OpOf<CFG, EXACT>, C::NW, C::NS, C::MINB>;
 }
 
 template <int CFG>
 static constexpr size_t u8_smem() {
     using C = U8Cfg<CFG>;
-    return StripShape<C::NW, C::NS, HarrisU8Op<false, C::CH>>::kSmemBytes;
+    return StripShape<C::NW, C::NS, U8OpOf<CFG, false>>::kSmemBytes;
 }
 
 template <int CFG>
@@ -65,10 +86,10 @@ static cudaError_t u8_launch_one(bool exact, const CUtensorMap& tmap, const Tile
     using C = U8Cfg<CFG>;
     const dim3 block{unsigned(C::NW * 32)}, gridd{unsigned(grid)};
     if (exact) {
-        const typename HarrisU8Op<true, C::CH>::Params p{tg.kappa};
+        const typename U8OpOf<CFG, true>::Params p{tg.kappa};
         u8_kernel<CFG, true>()<<<gridd, block, u8_smem<CFG>(), stream>>>(tmap, tg, p);
     } else {
-        const typename HarrisU8Op<false, C::CH>::Params p{tg.kappa};
+        const typename U8OpOf<CFG, false>::Params p{tg.kappa};
         u8_kernel<CFG, false>()<<<gridd, block, u8_smem<CFG>(), stream>>>(tmap, tg, p);
     }
     return cudaGetLastError();
@@ -85,6 +106,8 @@ size_t u8_smem_bytes(int cfg) {
         case 0: return u8_smem<0>();
         case 1: return u8_smem<1>();
         case 2: return u8_smem<2>();
+        case 3: return u8_smem<3>();
+        case 4: return u8_smem<4>();
         default: return 0;
     }
 }
@@ -94,6 +117,8 @@ cudaError_t u8_configure(int cfg) {
         case 0: return u8_configure_one<0>();
         case 1: return u8_configure_one<1>();
         case 2: return u8_configure_one<2>();
+        case 3: return u8_configure_one<3>();
+        case 4: return u8_configure_one<4>();
         default: return cudaErrorInvalidValue;
     }
 }
@@ -103,6 +128,8 @@ cudaError_t u8_occupancy(int cfg, int* ctas_per_sm) {
         case 0: return u8_occupancy_one<0>(ctas_per_sm);
         case 1: return u8_occupancy_one<1>(ctas_per_sm);
         case 2: return u8_occupancy_one<2>(ctas_per_sm);
+        case 3: return u8_occupancy_one<3>(ctas_per_sm);
+        case 4: return u8_occupancy_one<4>(ctas_per_sm);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -113,6 +140,8 @@ cudaError_t launch_tma_u8(int cfg, bool exact, const CUtensorMap& tmap, const Ti
         case 0: return u8_launch_one<0>(exact, tmap, tg, grid, stream);
         case 1: return u8_launch_one<1>(exact, tmap, tg, grid, stream);
         case 2: return u8_launch_one<2>(exact, tmap, tg, grid, stream);
+        case 3: return u8_launch_one<3>(exact, tmap, tg, grid, stream);
+        case 4: return u8_launch_one<4>(exact, tmap, tg, grid, stream);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -25,6 +25,7 @@ namespace harris {
 template <bool EXACT, int CH>
 struct Sep3x3Op {
     static_assert(CH % 3 == 0, "row rotation needs CH % 3 == 0");
+    static constexpr int kGroups = 1;
     static constexpr int kRowsPerStage = CH;
     static constexpr int kHaloRows = 2;
     static constexpr uint32_t kTxBytes = uint32_t(CH) * kBoxCols * 4u;
@@ -49,7 +50,8 @@ struct Sep3x3Op {
     }
 
     template <int R>
-    __device__ __forceinline__ void row(const unsigned char* stage, int lane, float (&out)[4]) {
+    __device__ __forceinline__ void row(const unsigned char* stage, int lane, float (&out4)[1][4]) {
+        float(&out)[4] = out4[0];
         constexpr int s2 = R % 3, s0 = (R + 1) % 3, s1 = (R + 2) % 3;
         const float* rp = reinterpret_cast<const float*>(stage) + R * kBoxCols + lane * 4;
         const float4 a = lds128(rp);
@@ -84,38 +86,82 @@ struct Sep3x3Op {
     }
 };
 
-constexpr int kSepNW = 8, kSepNS = 4, kSepCH = 6;
+// configs (warps, stages, rows/stage, min CTAs/SM); HARRIS_SEP_CONFIG selects one
+template <int CFG>
+struct SepCfg;
+template <>
+struct SepCfg<0> {
+    static constexpr int NW = 8, NS = 8, CH = 6, MINB = 1;
+};
+template <>
+struct SepCfg<1> {
+    static constexpr int NW = 8, NS = 4, CH = 6, MINB = 2;
+};
+template <>
+struct SepCfg<2> {
+    static constexpr int NW = 8, NS = 4, CH = 6, MINB = 1;
+};
 
-template <bool EXACT>
+const TmaConfig kSepConfigs[kNumSepConfigs] = {{8, 8, 6}, {8, 4, 6}, {8, 4, 6}};
+
+template <int CFG, bool EXACT>
 static constexpr auto sep_kernel() {
-    return strip_kernel<Sep3x3Op<EXACT, kSepCH>, kSepNW, kSepNS, 1>;
+    using C = SepCfg<CFG>;
+    return strip_kernel<Sep3x3Op<EXACT, C::CH>, C::NW, C::NS, C::MINB>;
 }
 
-static constexpr size_t sep_smem() { return StripShape<kSepNW, kSepNS, Sep3x3Op<false, kSepCH>>::kSmemBytes; }
+template <int CFG>
+static constexpr size_t sep_smem() {
+    using C = SepCfg<CFG>;
+    return StripShape<C::NW, C::NS, Sep3x3Op<false, C::CH>>::kSmemBytes;
+}
 
-const TmaConfig kSepConfig = {kSepNW, kSepNS, kSepCH};
-
-cudaError_t sep_configure(int* ctas_per_sm) {
-    cudaError_t e = cudaFuncSetAttribute(sep_kernel<false>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(sep_smem()));
+template <int CFG>
+static cudaError_t sep_configure_one(int* ctas_per_sm) {
+    using C = SepCfg<CFG>;
+    cudaError_t e = cudaFuncSetAttribute(sep_kernel<CFG, false>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(sep_smem<CFG>()));
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(sep_kernel<true>(), cudaFuncAttributeMaxDynamicSharedMemorySize, int(sep_smem()));
+        e = cudaFuncSetAttribute(sep_kernel<CFG, true>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(sep_smem<CFG>()));
     if (e == cudaSuccess)
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, sep_kernel<false>(), kSepNW * 32, sep_smem());
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, sep_kernel<CFG, false>(), C::NW * 32,
+                                                          sep_smem<CFG>());
     return e;
 }
 
-cudaError_t launch_tma_sep(bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid, const float* wv,
-                           const float* wh, cudaStream_t stream) {
-    const dim3 block{unsigned(kSepNW * 32)}, gridd{unsigned(grid)};
+cudaError_t sep_configure(int cfg, int* ctas_per_sm) {
+    switch (cfg) {
+        case 0: return sep_configure_one<0>(ctas_per_sm);
+        case 1: return sep_configure_one<1>(ctas_per_sm);
+        case 2: return sep_configure_one<2>(ctas_per_sm);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <int CFG>
+static cudaError_t sep_launch_one(bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid,
+                                  const float* wv, const float* wh, cudaStream_t stream) {
+    using C = SepCfg<CFG>;
+    const dim3 block{unsigned(C::NW * 32)}, gridd{unsigned(grid)};
     if (exact) {
-        typename Sep3x3Op<true, kSepCH>::Params p{{wv[0], wv[1], wv[2]}, {wh[0], wh[1], wh[2]}};
-        sep_kernel<true>()<<<gridd, block, sep_smem(), stream>>>(tmap, tg, p);
+        typename Sep3x3Op<true, C::CH>::Params p{{wv[0], wv[1], wv[2]}, {wh[0], wh[1], wh[2]}};
+        sep_kernel<CFG, true>()<<<gridd, block, sep_smem<CFG>(), stream>>>(tmap, tg, p);
     } else {
-        typename Sep3x3Op<false, kSepCH>::Params p{{wv[0], wv[1], wv[2]}, {wh[0], wh[1], wh[2]}};
-        sep_kernel<false>()<<<gridd, block, sep_smem(), stream>>>(tmap, tg, p);
+        typename Sep3x3Op<false, C::CH>::Params p{{wv[0], wv[1], wv[2]}, {wh[0], wh[1], wh[2]}};
+        sep_kernel<CFG, false>()<<<gridd, block, sep_smem<CFG>(), stream>>>(tmap, tg, p);
     }
     return cudaGetLastError();
+}
+
+cudaError_t launch_tma_sep(int cfg, bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid,
+                           const float* wv, const float* wh, cudaStream_t stream) {
+    switch (cfg) {
+        case 0: return sep_launch_one<0>(exact, tmap, tg, grid, wv, wh, stream);
+        case 1: return sep_launch_one<1>(exact, tmap, tg, grid, wv, wh, stream);
+        case 2: return sep_launch_one<2>(exact, tmap, tg, grid, wv, wh, stream);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 // generic fallback: one thread per output pixel, same two orders

@@ -17,11 +17,13 @@
 // full (input row i >= Op::kHaloRows).
 //
 // Op concept:
+//   kGroups (1 or 2: 128-column strips per tile; with 2 a lane owns the same 4
+//            columns of two adjacent strips, so the op can run packed f32x2 math),
 //   kRowsPerStage, kHaloRows, kStageBytes (multiple of 128), kTxBytes
 //   struct Params;  explicit Op(const Params&)
 //   static void load(void* smem, const CUtensorMap*, uint64_t* bar, int strip_col0, int in_row0, int image,
 //                    uint64_t l2_policy)                       // lane 0 only
-//   template <int R> void row(const unsigned char* stage, int lane, float (&out)[4])
+//   template <int R> void row(const unsigned char* stage, int lane, float (&out)[kGroups][4])
 #pragma once
 #include <cuda.h>
 
@@ -68,6 +70,8 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     strip_kernel(const __grid_constant__ CUtensorMap tmap, const TileGeom g, const typename Op::Params p) {
     constexpr int CH = Op::kRowsPerStage;
     constexpr int HALO = Op::kHaloRows;
+    constexpr int G = Op::kGroups;
+    constexpr int SW = kWarpCols * G;  // tile width in output columns
     extern __shared__ __align__(128) unsigned char smem_raw[];
     // align by offsetting the __shared__ array itself (an integer round trip would turn
     // every stage read into a generic LD instead of LDS)
@@ -100,7 +104,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
             if (lane == 0) {
                 const TileCoord c = decode_tile(pt, g);
                 mbar_arrive_expect_tx(&bars[s], Op::kTxBytes);
-                Op::load(ring + s * Op::kStageBytes, &tmap, &bars[s], c.cs * kWarpCols,
+                Op::load(ring + s * Op::kStageBytes, &tmap, &bars[s], c.cs * SW,
                          c.band * g.band_rows + pc * CH, c.b, policy);
             }
             if (++pc == pn) {
@@ -120,8 +124,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
         const TileCoord tc = decode_tile(t, g);
         const int rows_out = band_rows_out(tc.band, g);
         const int nch = (rows_out + HALO + CH - 1) / CH;
-        const int col0 = tc.cs * kWarpCols + lane * kColsPerLane;
-        const bool col_ok = col0 < g.m;
+        const int col0 = tc.cs * SW + lane * kColsPerLane;
         float* orow = g.out + int64_t(tc.b) * g.out_image_stride + int64_t(tc.band) * g.band_rows * g.out_pitch +
                       col0;
 
@@ -132,16 +135,21 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                 [&](auto rc) {
                     constexpr int R = decltype(rc)::value;
                     const int i = c * CH + R;  // input row within the tile
-                    float out4[4];
+                    float out4[G][4];
                     op.template row<R>(sm, lane, out4);
-                    if (i >= HALO && i - HALO < rows_out && col_ok) {
-                        float* po = orow + int64_t(i - HALO) * g.out_pitch;
-                        if (g.vec_store && col0 + kColsPerLane <= g.m) {
-                            stg128_cs(po, out4[0], out4[1], out4[2], out4[3]);
-                        } else {  // unaligned output rows, or the ragged right edge
+                    if (i >= HALO && i - HALO < rows_out) {
 #pragma unroll
-                            for (int k = 0; k < kColsPerLane; ++k)
-                                if (col0 + k < g.m) po[k] = out4[k];
+                        for (int gi = 0; gi < G; ++gi) {
+                            const int cg = col0 + gi * kWarpCols;
+                            if (cg >= g.m) continue;
+                            float* po = orow + int64_t(i - HALO) * g.out_pitch + gi * kWarpCols;
+                            if (g.vec_store && cg + kColsPerLane <= g.m) {
+                                stg128_cs(po, out4[gi][0], out4[gi][1], out4[gi][2], out4[gi][3]);
+                            } else {  // unaligned output rows, or the ragged right edge
+#pragma unroll
+                                for (int k = 0; k < kColsPerLane; ++k)
+                                    if (cg + k < g.m) po[k] = out4[gi][k];
+                            }
                         }
                     }
                 },

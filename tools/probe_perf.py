@@ -93,6 +93,38 @@ print(json.dumps(res))
     return json.loads(r.stdout.strip().splitlines()[-1])
 
 
+def time_stencil(workloads, iters):
+    code = f"""
+import sys, torch, json
+sys.path.insert(0, {ROOT!r})
+import paper_2212_12035_b200 as hb
+res = []
+for (B, H, W) in {workloads!r}:
+    x = torch.empty((B, H, W), device='cuda')
+    hb.synth_(x, seed=12035)
+    out = torch.empty((B, H - 2, W - 2), device='cuda')
+    for _ in range(3):
+        hb.stencil3x3_sep(x, out=out)
+    torch.cuda.synchronize()
+    evs = []
+    for _ in range({iters}):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(); hb.stencil3x3_sep(x, out=out); e1.record()
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    ts = sorted(a.elapsed_time(b) for a, b in evs)
+    res.append(dict(B=B, H=H, W=W, ms=ts[len(ts) // 2], min_ms=ts[0], path=hb.context().last_path))
+    del x, out
+    torch.cuda.empty_cache()
+print(json.dumps(res))
+"""
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
+    if r.returncode != 0:
+        print(r.stderr[-2000:])
+        return []
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="0,1,2,3")
@@ -100,9 +132,19 @@ def main():
     ap.add_argument("--exact", action="store_true")
     ap.add_argument("--generic", action="store_true")
     ap.add_argument("--u8", action="store_true")
+    ap.add_argument("--stencil", action="store_true")
     a = ap.parse_args()
     workloads = [(1, 8192, 8192), (1024, 1080, 1920), (1, 1536, 2560)]
     pk = peak()
+    if a.stencil:
+        for r in time_stencil(workloads, a.iters):
+            B, H, W = r["B"], r["H"], r["W"]
+            nbytes = B * (4 * H * W + 4 * (H - 2) * (W - 2))
+            gbs = nbytes / (r["ms"] * 1e-3) / 1e9
+            mps = B * (H - 2) * (W - 2) / (r["ms"] * 1e-3) / 1e6
+            print(f"stencil3x3 {B}x{H}x{W}: {r['ms']:.4f} ms (min {r['min_ms']:.4f}) {mps:,.0f} MP/s "
+                  f"{gbs:,.0f} GB/s frac={gbs / pk:.3f} path={r['path']}", flush=True)
+        return
     if a.u8:
         for cfg in [int(c) for c in a.configs.split(",")]:
             for r in time_u8(cfg, workloads, a.iters):
