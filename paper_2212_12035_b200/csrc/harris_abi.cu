@@ -121,18 +121,22 @@ bool tma_eligible(const Call& c) {
 
 // Pick the band height that minimises (waves x rows-per-tile) for a persistent
 // grid of `gw` warps: tiles = batch x bands x col_segments.
+// Pick the band height that minimises (waves x rows-per-tile) for a persistent grid
+// of `gw` warps.  A tile is `groups` 128-column strips: with groups == 2 the strips
+// of one band row of all images are paired consecutively (strip_pipeline.cuh).
 void plan_tiles(int64_t n, int64_t m, int64_t batch, int64_t gw, int rows_per_stage, int64_t force_rows,
                 TileGeom& tg, int halo = 4, int groups = 1) {
-    const int64_t strip = int64_t(kWarpCols) * groups;
-    const int64_t colsegs = (m + strip - 1) / strip;
+    const int64_t colsegs = (m + kWarpCols - 1) / kWarpCols;
+    const int64_t units_per_band = groups == 2 ? (batch * colsegs + 1) / 2 : batch * colsegs;
+    tg.n = int32_t(n);
+    tg.m = int32_t(m);
+    tg.colsegs = int32_t(colsegs);
+    tg.batch = int32_t(batch);
     if (force_rows > 0) {
         const int64_t rows = std::min(force_rows, n);
-        tg.n = int32_t(n);
-        tg.m = int32_t(m);
         tg.band_rows = int32_t(rows);
         tg.bands = int32_t((n + rows - 1) / rows);
-        tg.colsegs = int32_t(colsegs);
-        tg.tiles = batch * colsegs * tg.bands;
+        tg.tiles = units_per_band * tg.bands;
         return;
     }
     const int64_t kTileOverheadRows = 6;  // pipeline/tile switch cost in row-equivalents
@@ -142,7 +146,7 @@ void plan_tiles(int64_t n, int64_t m, int64_t batch, int64_t gw, int rows_per_st
         const int64_t rows = (n + nb - 1) / nb;
         const int64_t bands = (n + rows - 1) / rows;
         if (bands != nb) continue;  // same split as a smaller nb
-        const int64_t tiles = batch * colsegs * bands;
+        const int64_t tiles = units_per_band * bands;
         const int64_t waves = (tiles + gw - 1) / gw;
         const int64_t rows_in = ((rows + halo + rows_per_stage - 1) / rows_per_stage) * rows_per_stage;
         const int64_t cost = waves * (rows_in + kTileOverheadRows);
@@ -152,12 +156,9 @@ void plan_tiles(int64_t n, int64_t m, int64_t batch, int64_t gw, int rows_per_st
             best_bands = bands;
         }
     }
-    tg.n = int32_t(n);
-    tg.m = int32_t(m);
     tg.band_rows = int32_t(best_rows);
     tg.bands = int32_t(best_bands);
-    tg.colsegs = int32_t(colsegs);
-    tg.tiles = batch * colsegs * best_bands;
+    tg.tiles = units_per_band * best_bands;
 }
 
 int choose_path(const Call& c) {
@@ -188,7 +189,7 @@ int encode_tmap_u8(harris_ctx* ctx, const Call& c, CUtensorMap* tmap) {
     cuuint64_t dims[3] = {cuuint64_t((3 * (g.m + 4) + 3) / 4), cuuint64_t(g.n + 4), cuuint64_t(g.batch)};
     const int64_t img_stride = g.batch > 1 ? g.in_image_stride : (g.n + 4) * g.in_pitch;
     cuuint64_t strides[2] = {cuuint64_t(g.in_pitch), cuuint64_t((img_stride + 15) / 16 * 16)};
-    cuuint32_t box[3] = {cuuint32_t(cfg.groups == 2 ? 196 : kU8BoxWords), cuuint32_t(cfg.rows), 1};
+    cuuint32_t box[3] = {cuuint32_t(kU8BoxWords), cuuint32_t(cfg.rows), 1};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = ctx->encode(tmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<float*>(g.rgb), dims, strides, box,
                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,

@@ -21,7 +21,8 @@ struct Geom {
 // `band_rows` output rows of one image.
 struct TileGeom {
     int32_t n, m;
-    int32_t band_rows, bands, colsegs;
+    int32_t band_rows, bands, colsegs;  // colsegs: 128-column strips per image
+    int32_t batch;
     int32_t l2_policy;  // 0 evict_first, 1 evict_normal (default), 2 evict_last
     int32_t vec_store;  // 1: output rows 16-byte aligned -> float4 streaming stores
     int32_t pad_;

@@ -33,6 +33,17 @@ __device__ __forceinline__ void hsum4(const float (&p)[6], float& o0, float& o1,
     o3 = q3 + p[5];
 }
 
+// products a*b of 6 columns folded into 4 horizontal 3-sums (shared pairs): 8 ops
+__device__ __forceinline__ void prodsum4(const float (&a)[6], const float (&b)[6], float& o0, float& o1, float& o2,
+                                         float& o3) {
+    const float q1 = fmaf(a[1], b[1], a[2] * b[2]);
+    const float q3 = fmaf(a[3], b[3], a[4] * b[4]);
+    o0 = fmaf(a[0], b[0], q1);
+    o1 = fmaf(a[3], b[3], q1);
+    o2 = fmaf(a[2], b[2], q3);
+    o3 = fmaf(a[5], b[5], q3);
+}
+
 template <bool EXACT>
 struct HarrisCore {
     float kappa;
@@ -71,18 +82,16 @@ struct HarrisCore {
                 D[s2][k] = gr[k + 2] - gr[k];
                 Hs[s2][k] = fmaf(2.f, gr[k + 1], gr[k]) + gr[k + 2];
             }
-            float pxx[6], pxy[6], pyy[6];
+            float ix[6], iy[6];
 #pragma unroll
             for (int k = 0; k < 6; ++k) {
-                const float ix = fmaf(2.f, D[s1][k], D[s0][k] + D[s2][k]);
-                const float iy = Hs[s2][k] - Hs[s0][k];
-                pxx[k] = ix * ix;
-                pxy[k] = ix * iy;
-                pyy[k] = iy * iy;
+                ix[k] = fmaf(2.f, D[s1][k], D[s0][k] + D[s2][k]);
+                iy[k] = Hs[s2][k] - Hs[s0][k];
             }
-            hsum4(pxx, HB[s2][0], HB[s2][1], HB[s2][2], HB[s2][3]);
-            hsum4(pxy, HB[s2][4], HB[s2][5], HB[s2][6], HB[s2][7]);
-            hsum4(pyy, HB[s2][8], HB[s2][9], HB[s2][10], HB[s2][11]);
+            // products folded into the shared-pair horizontal 3-sums with explicit FMAs
+            prodsum4(ix, ix, HB[s2][0], HB[s2][1], HB[s2][2], HB[s2][3]);
+            prodsum4(ix, iy, HB[s2][4], HB[s2][5], HB[s2][6], HB[s2][7]);
+            prodsum4(iy, iy, HB[s2][8], HB[s2][9], HB[s2][10], HB[s2][11]);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const float sxx = (HB[s0][0 + j] + HB[s1][0 + j]) + HB[s2][0 + j];
@@ -148,9 +157,10 @@ struct HarrisF32Op {
 
     __device__ __forceinline__ explicit HarrisF32Op(const Params& p) : core(p.kappa) {}
 
-    __device__ __forceinline__ static void load(void* smem, const CUtensorMap* tmap, uint64_t* bar, int col0,
-                                                int row0, int image, uint64_t policy) {
-        tma_load_4d(smem, tmap, bar, col0, row0, 0, image, policy);
+    __device__ __forceinline__ static void load(void* smem, const CUtensorMap* tmap, uint64_t* bar,
+                                                const int (&col0)[1], int row0, const int (&image)[1],
+                                                uint64_t policy) {
+        tma_load_4d(smem, tmap, bar, col0[0], row0, 0, image[0], policy);
     }
 
     template <int R>
@@ -217,9 +227,10 @@ struct HarrisU8Op {
     __device__ __forceinline__ explicit HarrisU8Op(const Params& p) : core(p.kappa) {}
 
     // tensor map over 32-bit words: {ceil(3W/4) words, H rows, B images}
-    __device__ __forceinline__ static void load(void* smem, const CUtensorMap* tmap, uint64_t* bar, int col0,
-                                                int row0, int image, uint64_t policy) {
-        tma_load_3d(smem, tmap, bar, (col0 / kWarpCols) * (kWarpCols * 3 / 4), row0, image, policy);
+    __device__ __forceinline__ static void load(void* smem, const CUtensorMap* tmap, uint64_t* bar,
+                                                const int (&col0)[1], int row0, const int (&image)[1],
+                                                uint64_t policy) {
+        tma_load_3d(smem, tmap, bar, (col0[0] / kWarpCols) * (kWarpCols * 3 / 4), row0, image[0], policy);
     }
 
     template <int R>

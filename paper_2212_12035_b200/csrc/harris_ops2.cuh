@@ -11,10 +11,10 @@
 //
 // Arithmetic is the same contract as harris_ops.cuh:
 //   FAST : separable Sobel, fused product+pair-sum box rows, FMAs.
-//   EXACT: Appendix-B 9-tap orders with packed *_rn ops (each element rounded
-//          exactly like the scalar __fmul_rn/__fadd_rn), bit-exact with the oracle.
-// a - b is evaluated as fma(b, -1, a): one rounding of the exact difference, i.e.
-// identical to FSUB.
+//   EXACT: Appendix-B 9-tap orders, component-wise scalar __fmul_rn/__fadd_rn
+//          (see xadd2 below for why not the packed forms), bit-exact with the oracle.
+// In FAST, a - b is evaluated as fma(b, -1, a): one rounding of the exact
+// difference, i.e. identical to FSUB.
 #pragma once
 #include <cuda.h>
 
@@ -35,45 +35,62 @@ __device__ __forceinline__ float2 shfl_down2(float2 v) {
     return make_float2(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1));
 }
 
-// exact Appendix-B pieces on pairs
+// exact Appendix-B pieces on pairs.  ptxas (CUDA 12.9, sm_100a) packs paired
+// mul.rn/add.rn into FMUL2/FADD2 and then contracts them into FFMA2 despite the
+// explicit rounding modifier (observed in SASS), which breaks bit-exactness.  The
+// multiplies are therefore written as fma(a, b, -0), which is bit-identical to a
+// rounded product and cannot be fused with the following add.  EXACT is the parity
+// path, so its speed is irrelevant.
+__device__ __forceinline__ float2 xadd2(float2 a, float2 b) {
+    return make_float2(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y));
+}
+// a*b as fma(a, b, -0): bit-identical to round(a*b) (adding -0 preserves every value
+// and sign), and an fma can never be contracted with the following add
+__device__ __forceinline__ float2 xmul2(float2 a, float2 b) {
+    return make_float2(__fmaf_rn(a.x, b.x, -0.0f), __fmaf_rn(a.y, b.y, -0.0f));
+}
+__device__ __forceinline__ float2 xsub2(float2 a, float2 b) {
+    return make_float2(__fsub_rn(a.x, b.x), __fsub_rn(a.y, b.y));
+}
+
 __device__ __forceinline__ float2 gray_exact2(float2 r, float2 g, float2 b) {
-    float2 t = add2(f2(0.0f), mul2(f2(kGrayR), r));
-    t = add2(t, mul2(f2(kGrayG), g));
-    return add2(t, mul2(f2(kGrayB), b));
+    float2 t = xadd2(f2(0.0f), xmul2(f2(kGrayR), r));
+    t = xadd2(t, xmul2(f2(kGrayG), g));
+    return xadd2(t, xmul2(f2(kGrayB), b));
 }
 
 __device__ __forceinline__ float2 conv9_exact2(const float (&w)[9], float2 a0, float2 a1, float2 a2, float2 b0,
                                                float2 b1, float2 b2, float2 c0, float2 c1, float2 c2) {
     float2 t = f2(0.0f);
-    t = add2(t, mul2(f2(w[0]), a0));
-    t = add2(t, mul2(f2(w[1]), a1));
-    t = add2(t, mul2(f2(w[2]), a2));
-    t = add2(t, mul2(f2(w[3]), b0));
-    t = add2(t, mul2(f2(w[4]), b1));
-    t = add2(t, mul2(f2(w[5]), b2));
-    t = add2(t, mul2(f2(w[6]), c0));
-    t = add2(t, mul2(f2(w[7]), c1));
-    t = add2(t, mul2(f2(w[8]), c2));
+    t = xadd2(t, xmul2(f2(w[0]), a0));
+    t = xadd2(t, xmul2(f2(w[1]), a1));
+    t = xadd2(t, xmul2(f2(w[2]), a2));
+    t = xadd2(t, xmul2(f2(w[3]), b0));
+    t = xadd2(t, xmul2(f2(w[4]), b1));
+    t = xadd2(t, xmul2(f2(w[5]), b2));
+    t = xadd2(t, xmul2(f2(w[6]), c0));
+    t = xadd2(t, xmul2(f2(w[7]), c1));
+    t = xadd2(t, xmul2(f2(w[8]), c2));
     return t;
 }
 
 __device__ __forceinline__ float2 sum9_exact2(float2 a0, float2 a1, float2 a2, float2 b0, float2 b1, float2 b2,
                                               float2 c0, float2 c1, float2 c2) {
-    float2 s = add2(f2(0.0f), a0);
-    s = add2(s, a1);
-    s = add2(s, a2);
-    s = add2(s, b0);
-    s = add2(s, b1);
-    s = add2(s, b2);
-    s = add2(s, c0);
-    s = add2(s, c1);
-    return add2(s, c2);
+    float2 s = xadd2(f2(0.0f), a0);
+    s = xadd2(s, a1);
+    s = xadd2(s, a2);
+    s = xadd2(s, b0);
+    s = xadd2(s, b1);
+    s = xadd2(s, b2);
+    s = xadd2(s, c0);
+    s = xadd2(s, c1);
+    return xadd2(s, c2);
 }
 
 __device__ __forceinline__ float2 coarsity_exact2(float2 sxx, float2 sxy, float2 syy, float k) {
-    const float2 det = sub2(mul2(sxx, syy), mul2(sxy, sxy));
-    const float2 tr = add2(sxx, syy);
-    return sub2(det, mul2(mul2(f2(k), tr), tr));
+    const float2 det = xsub2(xmul2(sxx, syy), xmul2(sxy, sxy));
+    const float2 tr = xadd2(sxx, syy);
+    return xsub2(det, xmul2(xmul2(f2(k), tr), tr));
 }
 
 template <bool EXACT>
@@ -156,9 +173,9 @@ struct HarrisCore2 {
                                                G3[s1][k + 1], G3[s1][k + 2], G3[s2][k], G3[s2][k + 1], G3[s2][k + 2]);
                 const float2 iy = conv9_exact2(WY, G3[s0][k], G3[s0][k + 1], G3[s0][k + 2], G3[s1][k],
                                                G3[s1][k + 1], G3[s1][k + 2], G3[s2][k], G3[s2][k + 1], G3[s2][k + 2]);
-                P[s2][k] = mul2(ix, ix);
-                P[s2][6 + k] = mul2(ix, iy);
-                P[s2][12 + k] = mul2(iy, iy);
+                P[s2][k] = xmul2(ix, ix);
+                P[s2][6 + k] = xmul2(ix, iy);
+                P[s2][12 + k] = xmul2(iy, iy);
             }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -204,11 +221,12 @@ struct HarrisF32x2Op {
 
     __device__ __forceinline__ explicit HarrisF32x2Op(const Params& p) : core(p.kappa) {}
 
-    __device__ __forceinline__ static void load(void* smem, const CUtensorMap* tmap, uint64_t* bar, int col0,
-                                                int row0, int image, uint64_t policy) {
-        tma_load_4d(smem, tmap, bar, col0, row0, 0, image, policy);
-        tma_load_4d(static_cast<unsigned char*>(smem) + kBoxStride, tmap, bar, col0 + kWarpCols, row0, 0, image,
-                    policy);
+    // one box per strip (the two strips may belong to different images)
+    __device__ __forceinline__ static void load(void* smem, const CUtensorMap* tmap, uint64_t* bar,
+                                                const int (&col0)[2], int row0, const int (&image)[2],
+                                                uint64_t policy) {
+        tma_load_4d(smem, tmap, bar, col0[0], row0, 0, image[0], policy);
+        tma_load_4d(static_cast<unsigned char*>(smem) + kBoxStride, tmap, bar, col0[1], row0, 0, image[1], policy);
     }
 
     template <int R>
@@ -237,8 +255,6 @@ struct HarrisF32x2Op {
 };
 
 // --------------------------------------------------- interleaved RGB u8 (HWC)
-constexpr int kU8x2BoxWords = 196;  // 784 bytes >= 260 px * 3 B; <= 256 TMA elements
-
 // (byte k of wa, byte k of wb) as exact floats: PRMT each, one FADD2 for both
 __device__ __forceinline__ float2 u8f2(uint32_t wa, uint32_t wb, int k) {
     const float2 m = make_float2(__int_as_float(__byte_perm(wa, 0x4B000000u, 0x7440u | uint32_t(k))),
@@ -276,8 +292,10 @@ struct HarrisU8x2Op {
     static constexpr int kGroups = 2;
     static constexpr int kRowsPerStage = CH;
     static constexpr int kHaloRows = 4;
-    static constexpr uint32_t kTxBytes = uint32_t(CH) * kU8x2BoxWords * 4u;
-    static constexpr uint32_t kStageBytes = (kTxBytes + 127u) / 128u * 128u;
+    static constexpr uint32_t kBoxBytes = uint32_t(CH) * kU8BoxWords * 4u;
+    static constexpr uint32_t kBoxStride = (kBoxBytes + 127u) / 128u * 128u;
+    static constexpr uint32_t kTxBytes = 2u * kBoxBytes;
+    static constexpr uint32_t kStageBytes = 2u * kBoxStride;
     struct Params {
         float kappa;
     };
@@ -285,22 +303,26 @@ struct HarrisU8x2Op {
 
     __device__ __forceinline__ explicit HarrisU8x2Op(const Params& p) : core(p.kappa) {}
 
-    // tensor map over 32-bit words; a 256-column tile starts at word 192 * (col0 / 256)
-    __device__ __forceinline__ static void load(void* smem, const CUtensorMap* tmap, uint64_t* bar, int col0,
-                                                int row0, int image, uint64_t policy) {
-        tma_load_3d(smem, tmap, bar, (col0 / (2 * kWarpCols)) * (2 * kWarpCols * 3 / 4), row0, image, policy);
+    // tensor map over 32-bit words; strip cs starts at word 96 * cs
+    __device__ __forceinline__ static void load(void* smem, const CUtensorMap* tmap, uint64_t* bar,
+                                                const int (&col0)[2], int row0, const int (&image)[2],
+                                                uint64_t policy) {
+        tma_load_3d(smem, tmap, bar, (col0[0] / kWarpCols) * (kWarpCols * 3 / 4), row0, image[0], policy);
+        tma_load_3d(static_cast<unsigned char*>(smem) + kBoxStride, tmap, bar,
+                    (col0[1] / kWarpCols) * (kWarpCols * 3 / 4), row0, image[1], policy);
     }
 
     template <int R>
     __device__ __forceinline__ void row(const unsigned char* stage, int lane, float (&out)[2][4]) {
-        const uint32_t* w = reinterpret_cast<const uint32_t*>(stage) + R * kU8x2BoxWords;
-        const uint32_t a[3] = {w[3 * lane], w[3 * lane + 1], w[3 * lane + 2]};
-        const uint32_t b[3] = {w[96 + 3 * lane], w[97 + 3 * lane], w[98 + 3 * lane]};
+        const uint32_t* wa = reinterpret_cast<const uint32_t*>(stage) + R * kU8BoxWords;
+        const uint32_t* wb = reinterpret_cast<const uint32_t*>(stage + kBoxStride) + R * kU8BoxWords;
+        const uint32_t a[3] = {wa[3 * lane], wa[3 * lane + 1], wa[3 * lane + 2]};
+        const uint32_t b[3] = {wb[3 * lane], wb[3 * lane + 1], wb[3 * lane + 2]};
         float2 gown[4];
         gray4_u8x2<EXACT>(a, b, gown[0], gown[1], gown[2], gown[3]);
         core.template step<R>(gown, lane, [&](float2& h0, float2& h1, float2& h2, float2& h3) {
-            const uint32_t ha[3] = {w[96], w[97], w[98]};
-            const uint32_t hb[3] = {w[192], w[193], w[194]};
+            const uint32_t ha[3] = {wa[96], wa[97], wa[98]};
+            const uint32_t hb[3] = {wb[96], wb[97], wb[98]};
             gray4_u8x2<EXACT>(ha, hb, h0, h1, h2, h3);
         }, out);
     }

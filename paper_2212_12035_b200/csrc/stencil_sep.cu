@@ -44,9 +44,10 @@ struct Sep3x3Op {
             for (int k = 0; k < 6; ++k) X[a][k] = 0.f;
     }
 
-    __device__ __forceinline__ static void load(void* smem, const CUtensorMap* tmap, uint64_t* bar, int col0,
-                                                int row0, int image, uint64_t policy) {
-        tma_load_3d(smem, tmap, bar, col0, row0, image, policy);
+    __device__ __forceinline__ static void load(void* smem, const CUtensorMap* tmap, uint64_t* bar,
+                                                const int (&col0)[1], int row0, const int (&image)[1],
+                                                uint64_t policy) {
+        tma_load_3d(smem, tmap, bar, col0[0], row0, image[0], policy);
     }
 
     template <int R>

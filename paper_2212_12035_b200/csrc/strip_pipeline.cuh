@@ -21,8 +21,8 @@
 //            columns of two adjacent strips, so the op can run packed f32x2 math),
 //   kRowsPerStage, kHaloRows, kStageBytes (multiple of 128), kTxBytes
 //   struct Params;  explicit Op(const Params&)
-//   static void load(void* smem, const CUtensorMap*, uint64_t* bar, int strip_col0, int in_row0, int image,
-//                    uint64_t l2_policy)                       // lane 0 only
+//   static void load(void* smem, const CUtensorMap*, uint64_t* bar, const int (&strip_col0)[kGroups],
+//                    int in_row0, const int (&image)[kGroups], uint64_t l2_policy)   // lane 0 only
 //   template <int R> void row(const unsigned char* stage, int lane, float (&out)[kGroups][4])
 #pragma once
 #include <cuda.h>
@@ -35,17 +35,43 @@
 
 namespace harris {
 
+// Tile -> coordinates.  G = 1: tile t = (image b, band, strip cs), strip-fastest.
+// G = 2: the strips of one band row of ALL images are numbered s = b * colsegs + cs and
+// paired (2p, 2p+1), so a pair may straddle two images and no group idles at the
+// right edge of an image; tile t = (band, pair p), pair-fastest.
+template <int G>
 struct TileCoord {
-    int b, band, cs;
+    int band;
+    int b[G], cs[G];
+    bool valid[G];
 };
 
-__device__ __forceinline__ TileCoord decode_tile(int64_t t, const TileGeom& g) {
-    TileCoord c;
-    const int64_t q = t / g.colsegs;
-    c.cs = int(t - q * g.colsegs);
-    const int64_t b = q / g.bands;
-    c.band = int(q - b * g.bands);
-    c.b = int(b);
+template <int G>
+__device__ __forceinline__ TileCoord<G> decode_tile(int64_t t, const TileGeom& g) {
+    TileCoord<G> c;
+    if constexpr (G == 1) {
+        const int64_t q = t / g.colsegs;
+        c.cs[0] = int(t - q * g.colsegs);
+        const int64_t b = q / g.bands;
+        c.band = int(q - b * g.bands);
+        c.b[0] = int(b);
+        c.valid[0] = true;
+    } else {
+        const int64_t strips = g.batch * g.colsegs;
+        const int64_t pairs = (strips + 1) / 2;
+        const int64_t band = t / pairs;
+        const int64_t p = t - band * pairs;
+        c.band = int(band);
+#pragma unroll
+        for (int k = 0; k < G; ++k) {
+            const int64_t sidx = 2 * p + k;
+            c.valid[k] = sidx < strips;
+            const int64_t s2 = c.valid[k] ? sidx : 0;
+            const int64_t b = s2 / g.colsegs;
+            c.b[k] = int(b);
+            c.cs[k] = int(s2 - b * g.colsegs);
+        }
+    }
     return c;
 }
 
@@ -71,7 +97,6 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     constexpr int CH = Op::kRowsPerStage;
     constexpr int HALO = Op::kHaloRows;
     constexpr int G = Op::kGroups;
-    constexpr int SW = kWarpCols * G;  // tile width in output columns
     extern __shared__ __align__(128) unsigned char smem_raw[];
     // align by offsetting the __shared__ array itself (an integer round trip would turn
     // every stage read into a generic LD instead of LDS)
@@ -98,19 +123,25 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     // ---- producer cursor (warp-uniform; lane 0 issues) ----
     int64_t pt = gw;
     int pc = 0;
-    int pn = (band_rows_out(decode_tile(pt, g).band, g) + HALO + CH - 1) / CH;
+    int pn = (band_rows_out(decode_tile<G>(pt, g).band, g) + HALO + CH - 1) / CH;
     auto issue = [&](int s) {
         if (pt < g.tiles) {
             if (lane == 0) {
-                const TileCoord c = decode_tile(pt, g);
+                const TileCoord<G> c = decode_tile<G>(pt, g);
+                int cols[G], imgs[G];
+#pragma unroll
+                for (int k = 0; k < G; ++k) {
+                    cols[k] = c.cs[k] * kWarpCols;
+                    imgs[k] = c.b[k];
+                }
                 mbar_arrive_expect_tx(&bars[s], Op::kTxBytes);
-                Op::load(ring + s * Op::kStageBytes, &tmap, &bars[s], c.cs * SW,
-                         c.band * g.band_rows + pc * CH, c.b, policy);
+                Op::load(ring + s * Op::kStageBytes, &tmap, &bars[s], cols, c.band * g.band_rows + pc * CH, imgs,
+                         policy);
             }
             if (++pc == pn) {
                 pc = 0;
                 pt += GW;
-                if (pt < g.tiles) pn = (band_rows_out(decode_tile(pt, g).band, g) + HALO + CH - 1) / CH;
+                if (pt < g.tiles) pn = (band_rows_out(decode_tile<G>(pt, g).band, g) + HALO + CH - 1) / CH;
             }
         }
     };
@@ -121,12 +152,17 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     int stage = 0;
     uint32_t phase = 0;
     for (int64_t t = gw; t < g.tiles; t += GW) {
-        const TileCoord tc = decode_tile(t, g);
+        const TileCoord<G> tc = decode_tile<G>(t, g);
         const int rows_out = band_rows_out(tc.band, g);
         const int nch = (rows_out + HALO + CH - 1) / CH;
-        const int col0 = tc.cs * SW + lane * kColsPerLane;
-        float* orow = g.out + int64_t(tc.b) * g.out_image_stride + int64_t(tc.band) * g.band_rows * g.out_pitch +
-                      col0;
+        int colg[G];
+        float* orow[G];
+#pragma unroll
+        for (int k = 0; k < G; ++k) {
+            colg[k] = tc.valid[k] ? tc.cs[k] * kWarpCols + lane * kColsPerLane : g.m;  // invalid: never stored
+            orow[k] = g.out + int64_t(tc.b[k]) * g.out_image_stride +
+                      int64_t(tc.band) * g.band_rows * g.out_pitch + (tc.valid[k] ? colg[k] : 0);
+        }
 
         for (int c = 0; c < nch; ++c) {
             mbar_wait(&bars[stage], phase);
@@ -140,9 +176,9 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                     if (i >= HALO && i - HALO < rows_out) {
 #pragma unroll
                         for (int gi = 0; gi < G; ++gi) {
-                            const int cg = col0 + gi * kWarpCols;
+                            const int cg = colg[gi];
                             if (cg >= g.m) continue;
-                            float* po = orow + int64_t(i - HALO) * g.out_pitch + gi * kWarpCols;
+                            float* po = orow[gi] + int64_t(i - HALO) * g.out_pitch;
                             if (g.vec_store && cg + kColsPerLane <= g.m) {
                                 stg128_cs(po, out4[gi][0], out4[gi][1], out4[gi][2], out4[gi][3]);
                             } else {  // unaligned output rows, or the ragged right edge

@@ -141,7 +141,8 @@ def _check_rgb(rgb) -> tuple[int, int, int]:
 
 
 def harris(rgb, kappa: float = KAPPA, *, out: Optional[torch.Tensor] = None, exact: bool = False,
-           force_generic: bool = False, force_tma: bool = False, stream: Optional[torch.cuda.Stream] = None):
+           force_generic: bool = False, force_tma: bool = False, stream: Optional[torch.cuda.Stream] = None,
+           ctx: Optional[HarrisContext] = None):
     """Fused Harris coarsity of planar RGB f32.
 
     rgb: ``(3, H, W)`` or ``(B, 3, H, W)`` float32; CUDA tensor (device path,
@@ -183,13 +184,14 @@ def harris(rgb, kappa: float = KAPPA, *, out: Optional[torch.Tensor] = None, exa
         out_image = n * out_pitch
     dev = rgb.device.index if rgb.device.index is not None else torch.cuda.current_device()
     st = stream if stream is not None else torch.cuda.current_stream(dev)
-    context(dev).run_strided(out.data_ptr(), out_pitch, out_image, n, m, rgb.data_ptr(), in_pitch, in_chan,
-                             in_image, B, kappa, flags, st.cuda_stream)
+    (ctx or context(dev)).run_strided(out.data_ptr(), out_pitch, out_image, n, m, rgb.data_ptr(), in_pitch,
+                                      in_chan, in_image, B, kappa, flags, st.cuda_stream)
     return out
 
 
 def harris_u8(rgb8, kappa: float = KAPPA, *, out: Optional[torch.Tensor] = None, exact: bool = False,
-              force_generic: bool = False, force_tma: bool = False, stream: Optional[torch.cuda.Stream] = None):
+              force_generic: bool = False, force_tma: bool = False, stream: Optional[torch.cuda.Stream] = None,
+              ctx: Optional[HarrisContext] = None):
     """Fused Harris on interleaved 8-bit RGB: ``(H, W, 3)`` or ``(B, H, W, 3)`` uint8
     (value/255), CUDA (device path) or CPU/numpy (host path through the device).
     Returns ``(H-4, W-4)`` / ``(B, H-4, W-4)`` float32, equal to ``harris`` on the planar
@@ -226,7 +228,7 @@ def harris_u8(rgb8, kappa: float = KAPPA, *, out: Optional[torch.Tensor] = None,
     out_image = out.stride(0) if batched else n * out_pitch
     dev = rgb8.device.index if rgb8.device.index is not None else torch.cuda.current_device()
     st = stream if stream is not None else torch.cuda.current_stream(dev)
-    ctx = context(dev)
+    ctx = ctx or context(dev)
     rc = lib().harris_run_u8(ctx.handle, out.data_ptr(), out_pitch, out_image, n, m, rgb8.data_ptr(), in_pitch,
                              in_image, B, kappa, flags, st.cuda_stream)
     check(rc, "harris_run_u8", ctx.handle)

@@ -363,3 +363,55 @@ def test_stencil_batched_and_views(cuda_ctx):
     band = hb.stencil3x3_sep(x[1, 10:30], exact=True)
     torch.cuda.synchronize()
     assert torch.equal(band, got[1, 10:28])
+
+
+def _ctx_with(env: dict):
+    import os
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update({k: str(v) for k, v in env.items()})
+    try:
+        return hb.HarrisContext(0)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("cfg", range(8))
+def test_every_f32_tma_config_bitexact(cuda_ctx, cfg):
+    """Every TMA kernel configuration (scalar and packed dual-strip cores), including a
+    batch whose strip pairs straddle images and a single image with ragged strips."""
+    ctx = _ctx_with({"HARRIS_TMA_CONFIG": cfg})
+    for B, H, W in [(1, 9, 132), (1, 70, 260), (3, 41, 388), (1, 300, 2564), (5, 21, 136)]:
+        rgb = synth.synth_numpy(3 * B, H, W, seed=cfg * 101 + H).reshape(B, 3, H, W)
+        x = _dev(rgb if B > 1 else rgb[0])
+        ex = hb.harris(x, exact=True, ctx=ctx)
+        assert ctx.last_path == _lib.PATH_TMA
+        fast = hb.harris(x, ctx=ctx)
+        torch.cuda.synchronize()
+        ex, fast = ex.cpu().numpy().reshape(B, H - 4, W - 4), fast.cpu().numpy().reshape(B, H - 4, W - 4)
+        for b in range(B):
+            assert np.array_equal(ex[b], cref.harris_f32(rgb[b])), (cfg, B, H, W, b)
+            ok, m = synth.within_tolerance(fast[b], cref.harris_f64(rgb[b]))
+            assert ok, (cfg, B, H, W, b, m)
+    ctx.close()
+
+
+@pytest.mark.parametrize("cfg", range(5))
+def test_every_u8_tma_config_bitexact(cuda_ctx, cfg):
+    ctx = _ctx_with({"HARRIS_U8_CONFIG": cfg})
+    for B, H, W in [(1, 9, 128), (3, 40, 400), (1, 133, 528)]:
+        hwc, f32 = _u8_image(B, H, W, seed=cfg * 7 + H)
+        x = torch.from_numpy(hwc if B > 1 else hwc[0]).cuda()
+        ex = hb.harris_u8(x, exact=True, ctx=ctx)
+        assert ctx.last_path == _lib.PATH_TMA
+        fast = hb.harris_u8(x, ctx=ctx)
+        torch.cuda.synchronize()
+        ex, fast = ex.cpu().numpy().reshape(B, H - 4, W - 4), fast.cpu().numpy().reshape(B, H - 4, W - 4)
+        for b in range(B):
+            assert np.array_equal(ex[b], cref.harris_f32(f32[b])), (cfg, B, H, W, b)
+            ok, m = synth.within_tolerance(fast[b], cref.harris_f64(f32[b]))
+            assert ok, (cfg, B, H, W, b, m)
+    ctx.close()
