@@ -166,6 +166,8 @@ typedef struct harris_plan_info {
     int64_t tiles;          /* batch * bands * col_segments */
     int64_t grid_ctas;
     int64_t smem_bytes;     /* dynamic shared memory per CTA */
+    int32_t groups;         /* 128-column strips per tile (2: packed FP32x2 dual-strip core) */
+    int32_t tma_config;     /* kernel configuration index (HARRIS_TMA_CONFIG) */
 } harris_plan_info;
 
 HARRIS_API int harris_plan(harris_ctx* ctx, int64_t n, int64_t m, int64_t batch, const float* rgb,

@@ -57,7 +57,7 @@ class PlanInfo(ctypes.Structure):
         ("path", ctypes.c_int32), ("warps_per_cta", ctypes.c_int32), ("stages", ctypes.c_int32),
         ("rows_per_stage", ctypes.c_int32), ("band_rows", ctypes.c_int64), ("bands", ctypes.c_int64),
         ("col_segments", ctypes.c_int64), ("tiles", ctypes.c_int64), ("grid_ctas", ctypes.c_int64),
-        ("smem_bytes", ctypes.c_int64),
+        ("smem_bytes", ctypes.c_int64), ("groups", ctypes.c_int32), ("tma_config", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:

@@ -28,7 +28,7 @@ struct harris_ctx {
     int device = 0;
     int num_sms = 0;
     int cc_major = 0, cc_minor = 0;
-    int tma_cfg = 0;
+    int tma_cfg = kDefaultTmaConfig;
     int u8_cfg = 0;
     int sep_cfg = 0;
     int occ_sep[kNumSepConfigs] = {0};
@@ -503,6 +503,8 @@ int harris_plan(harris_ctx* ctx, int64_t n, int64_t m, int64_t batch, const floa
     info->tiles = tg.tiles;
     info->grid_ctas = grid;
     info->smem_bytes = int64_t(tma_smem_bytes(ctx->tma_cfg));
+    info->groups = cfg.groups;
+    info->tma_config = ctx->tma_cfg;
     return HARRIS_OK;
 }
 

@@ -39,6 +39,7 @@ struct TmaConfig {
     int groups = 1;  // 128-column strips per tile (2: packed FP32x2 dual-strip op)
 };
 constexpr int kNumTmaConfigs = 8;
+constexpr int kDefaultTmaConfig = 6;  // packed FP32x2 dual-strip core, 8 warps x 2 stages (bench r01)
 extern const TmaConfig kTmaConfigs[kNumTmaConfigs];
 
 size_t tma_smem_bytes(int cfg);

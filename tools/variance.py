@@ -26,6 +26,14 @@ def main():
     out = torch.empty((B, H - 4, W - 4), device="cuda")
     pynvml.nvmlInit()
     h = pynvml.nvmlDeviceGetHandleByIndex(0)
+    limits = {}
+    for name, fn in (("enforced_w", "nvmlDeviceGetEnforcedPowerLimit"), ("mgmt_limit_w", "nvmlDeviceGetPowerManagementLimit"),
+                     ("default_w", "nvmlDeviceGetPowerManagementDefaultLimit")):
+        try:
+            limits[name] = getattr(pynvml, fn)(h) / 1000.0
+        except Exception as e:  # pragma: no cover
+            limits[name] = repr(e)
+    mode = os.environ.get("VARIANCE_MODE", "harris")
     samples = []
     stop = threading.Event()
 
@@ -43,8 +51,18 @@ def main():
                 pass
             time.sleep(0.002)
 
+    flat = x.view(-1)
+    half = flat.numel() // 2
+
+    def launch():
+        if mode == "copy":   # plain device copy of the same byte volume (read 25.5 GB, write 8.4 GB)
+            out.view(-1).copy_(flat[: out.numel()])
+            flat[out.numel(): out.numel() * 2].copy_(flat[2 * out.numel(): 3 * out.numel()])
+        else:
+            hb.harris(x, out=out)
+
     for _ in range(3):
-        hb.harris(x, out=out)
+        launch()
     torch.cuda.synchronize()
     th = threading.Thread(target=loop, daemon=True)
     th.start()
@@ -53,7 +71,7 @@ def main():
     for _ in range(n_launch):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        hb.harris(x, out=out)
+        launch()
         e1.record()
         evs.append((e0, e1))
     torch.cuda.synchronize()
@@ -66,7 +84,8 @@ def main():
                       "sm_mhz": sorted({s["sm"] for s in inside}), "mem_mhz": sorted({s["mem"] for s in inside}),
                       "power_w": [round(min(s["pw"] for s in inside)), round(max(s["pw"] for s in inside))],
                       "temp_c": [min(s["temp"] for s in inside), max(s["temp"] for s in inside)],
-                      "reasons_or": hex(sum({s["rsn"] for s in inside})), "samples": len(inside)}))
+                      "reasons_or": hex(sum({s["rsn"] for s in inside})), "samples": len(inside),
+                      "limits": limits, "mode": mode}))
 
 
 if __name__ == "__main__":
