@@ -236,20 +236,22 @@ struct HarrisF32x2Op {
         const int o_r = (0 * CH + R) * kBoxCols, o_g = (1 * CH + R) * kBoxCols, o_b = (2 * CH + R) * kBoxCols;
         const float4 ra = lds128(a + o_r + lane * 4), ga = lds128(a + o_g + lane * 4), ba = lds128(a + o_b + lane * 4);
         const float4 rb = lds128(b + o_r + lane * 4), gb = lds128(b + o_g + lane * 4), bb = lds128(b + o_b + lane * 4);
+        // gray in scalar form: the results can be allocated straight into the (A, B)
+        // register pairs, where packed gray would first need MOVs to pair the inputs
         const float2 gown[4] = {
-            gray2_of<EXACT>(make_float2(ra.x, rb.x), make_float2(ga.x, gb.x), make_float2(ba.x, bb.x)),
-            gray2_of<EXACT>(make_float2(ra.y, rb.y), make_float2(ga.y, gb.y), make_float2(ba.y, bb.y)),
-            gray2_of<EXACT>(make_float2(ra.z, rb.z), make_float2(ga.z, gb.z), make_float2(ba.z, bb.z)),
-            gray2_of<EXACT>(make_float2(ra.w, rb.w), make_float2(ga.w, gb.w), make_float2(ba.w, bb.w))};
+            make_float2(gray_of<EXACT>(ra.x, ga.x, ba.x), gray_of<EXACT>(rb.x, gb.x, bb.x)),
+            make_float2(gray_of<EXACT>(ra.y, ga.y, ba.y), gray_of<EXACT>(rb.y, gb.y, bb.y)),
+            make_float2(gray_of<EXACT>(ra.z, ga.z, ba.z), gray_of<EXACT>(rb.z, gb.z, bb.z)),
+            make_float2(gray_of<EXACT>(ra.w, ga.w, ba.w), gray_of<EXACT>(rb.w, gb.w, bb.w))};
         core.template step<R>(gown, lane, [&](float2& h0, float2& h1, float2& h2, float2& h3) {
             const float4 r2a = lds128(a + o_r + kWarpCols), g2a = lds128(a + o_g + kWarpCols),
                          b2a = lds128(a + o_b + kWarpCols);
             const float4 r2b = lds128(b + o_r + kWarpCols), g2b = lds128(b + o_g + kWarpCols),
                          b2b = lds128(b + o_b + kWarpCols);
-            h0 = gray2_of<EXACT>(make_float2(r2a.x, r2b.x), make_float2(g2a.x, g2b.x), make_float2(b2a.x, b2b.x));
-            h1 = gray2_of<EXACT>(make_float2(r2a.y, r2b.y), make_float2(g2a.y, g2b.y), make_float2(b2a.y, b2b.y));
-            h2 = gray2_of<EXACT>(make_float2(r2a.z, r2b.z), make_float2(g2a.z, g2b.z), make_float2(b2a.z, b2b.z));
-            h3 = gray2_of<EXACT>(make_float2(r2a.w, r2b.w), make_float2(g2a.w, g2b.w), make_float2(b2a.w, b2b.w));
+            h0 = make_float2(gray_of<EXACT>(r2a.x, g2a.x, b2a.x), gray_of<EXACT>(r2b.x, g2b.x, b2b.x));
+            h1 = make_float2(gray_of<EXACT>(r2a.y, g2a.y, b2a.y), gray_of<EXACT>(r2b.y, g2b.y, b2b.y));
+            h2 = make_float2(gray_of<EXACT>(r2a.z, g2a.z, b2a.z), gray_of<EXACT>(r2b.z, g2b.z, b2b.z));
+            h3 = make_float2(gray_of<EXACT>(r2a.w, g2a.w, b2a.w), gray_of<EXACT>(r2b.w, g2b.w, b2b.w));
         }, out);
     }
 };
