@@ -12,7 +12,7 @@ import os
 import subprocess
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libharris_b200.so")
+LIB_PATH = os.environ.get("HARRIS_LIB") or os.path.join(PKG_DIR, "libharris_b200.so")  # HARRIS_LIB: dev A/B only
 CSRC = os.path.join(PKG_DIR, "csrc")
 
 HARRIS_OK = 0

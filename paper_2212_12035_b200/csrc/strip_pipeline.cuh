@@ -155,22 +155,14 @@ __global__ void __launch_bounds__(NW * 32, MINB)
         const TileCoord<G> tc = decode_tile<G>(t, g);
         const int rows_out = band_rows_out(tc.band, g);
         const int nch = (rows_out + HALO + CH - 1) / CH;
-        // per-group store state, hoisted out of the row loop: a row pointer advanced by
-        // out_pitch per input row (it points at output row i - HALO), the vector-store
-        // and ragged-edge decisions
-        float* prow[G];
-        int ncols[G];      // valid output columns of this lane in the group (0..4)
-        bool vec[G];
+        int colg[G];
+        float* orow[G];
 #pragma unroll
         for (int k = 0; k < G; ++k) {
-            const int cg = tc.cs[k] * kWarpCols + lane * kColsPerLane;
-            const int left = tc.valid[k] ? g.m - cg : 0;
-            ncols[k] = left < 0 ? 0 : (left > kColsPerLane ? kColsPerLane : left);
-            vec[k] = g.vec_store && ncols[k] == kColsPerLane;
-            prow[k] = g.out + int64_t(tc.b[k]) * g.out_image_stride +
-                      (int64_t(tc.band) * g.band_rows - HALO) * g.out_pitch + (ncols[k] ? cg : 0);
+            colg[k] = tc.valid[k] ? tc.cs[k] * kWarpCols + lane * kColsPerLane : g.m;  // invalid: never stored
+            orow[k] = g.out + int64_t(tc.b[k]) * g.out_image_stride +
+                      int64_t(tc.band) * g.band_rows * g.out_pitch + (tc.valid[k] ? colg[k] : 0);
         }
-        const int out_end = rows_out + HALO;  // input rows i in [HALO, out_end) produce output
 
         for (int c = 0; c < nch; ++c) {
             mbar_wait(&bars[stage], phase);
@@ -181,21 +173,21 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                     const int i = c * CH + R;  // input row within the tile
                     float out4[G][4];
                     op.template row<R>(sm, lane, out4);
-                    if (i >= HALO && i < out_end) {
+                    if (i >= HALO && i - HALO < rows_out) {
 #pragma unroll
                         for (int gi = 0; gi < G; ++gi) {
-                            float* po = prow[gi];
-                            if (vec[gi]) {
+                            const int cg = colg[gi];
+                            if (cg >= g.m) continue;
+                            float* po = orow[gi] + int64_t(i - HALO) * g.out_pitch;
+                            if (g.vec_store && cg + kColsPerLane <= g.m) {
                                 stg128_cs(po, out4[gi][0], out4[gi][1], out4[gi][2], out4[gi][3]);
                             } else {  // unaligned output rows, or the ragged right edge
 #pragma unroll
                                 for (int k = 0; k < kColsPerLane; ++k)
-                                    if (k < ncols[gi]) po[k] = out4[gi][k];
+                                    if (cg + k < g.m) po[k] = out4[gi][k];
                             }
                         }
                     }
-#pragma unroll
-                    for (int gi = 0; gi < G; ++gi) prow[gi] += g.out_pitch;
                 },
                 std::make_integer_sequence<int, CH>{});
             __syncwarp();  // every lane is done with this stage: refill it
