@@ -35,6 +35,7 @@ struct harris_ctx {
     int occ_u8[kNumU8Configs] = {0};
     int l2_policy = 1;  // evict_normal: the 4-column halo sectors are re-read by the neighbouring strip
     int64_t force_band_rows = 0;  // dev knob (HARRIS_BAND_ROWS): override the planner
+    CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;  // dev knob HARRIS_L2_PROMO
     int occ[kNumTmaConfigs] = {0};
     PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     int last_path = HARRIS_PATH_NONE;
@@ -193,7 +194,7 @@ int encode_tmap_u8(harris_ctx* ctx, const Call& c, CUtensorMap* tmap) {
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = ctx->encode(tmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<float*>(g.rgb), dims, strides, box,
                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                             ctx->promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
         std::snprintf(ctx->last_err, sizeof(ctx->last_err), "cuTensorMapEncodeTiled (u8) failed (CUresult %d)",
                       int(r));
@@ -214,7 +215,7 @@ int encode_tmap(harris_ctx* ctx, const Call& c, CUtensorMap* tmap) {
     cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = ctx->encode(tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(g.rgb), dims, strides,
                              box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                             ctx->promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
         std::snprintf(ctx->last_err, sizeof(ctx->last_err), "cuTensorMapEncodeTiled failed (CUresult %d)", int(r));
         return HARRIS_ERR_TMA;
@@ -330,6 +331,13 @@ int harris_init(harris_ctx** out_ctx, int cuda_device) {
     if (env) {
         int v = std::atoi(env);
         if (v >= 0 && v < kNumSepConfigs) ctx->sep_cfg = v;
+    }
+    env = std::getenv("HARRIS_L2_PROMO");
+    if (env) {
+        const int v = std::atoi(env);
+        const CUtensorMapL2promotion tab[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
+                                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
+        if (v >= 0 && v < 4) ctx->promo = tab[v];
     }
     env = std::getenv("HARRIS_BAND_ROWS");
     if (env) ctx->force_band_rows = std::atoll(env);
@@ -453,7 +461,7 @@ int harris_stencil3x3_sep(harris_ctx* ctx, float* out, int64_t out_pitch, int64_
         cuuint32_t estr[3] = {1, 1, 1};
         CUresult r = ctx->encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(in), dims, strides,
                                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                                 ctx->promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) {
             std::snprintf(ctx->last_err, sizeof(ctx->last_err), "cuTensorMapEncodeTiled (stencil) failed (%d)", int(r));
             return HARRIS_ERR_TMA;
