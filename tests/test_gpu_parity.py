@@ -415,3 +415,27 @@ def test_every_u8_tma_config_bitexact(cuda_ctx, cfg):
             ok, m = synth.within_tolerance(fast[b], cref.harris_f64(f32[b]))
             assert ok, (cfg, B, H, W, b, m)
     ctx.close()
+
+
+def test_cuda_graph_capture_replay(cuda_ctx):
+    """harris_run* never allocates or synchronises, so a launch can be captured in a CUDA
+    graph (the TMA descriptor is a by-value kernel parameter) and replayed on new data."""
+    H, W = 70, 264
+    a = synth.synth_numpy(3, H, W, seed=1)
+    b = synth.synth_numpy(3, H, W, seed=2)
+    x = _dev(a)
+    out = torch.empty((H - 4, W - 4), device="cuda")
+    hb.harris(x, out=out)          # warm-up (context creation) outside capture
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            hb.harris(x, out=out, exact=True)
+    g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), cref.harris_f32(a))
+    x.copy_(_dev(b))
+    g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), cref.harris_f32(b))
