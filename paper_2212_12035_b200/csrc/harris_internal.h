@@ -38,7 +38,7 @@ struct TmaConfig {
     int warps, stages, rows;
     int groups = 1;  // 128-column strips per tile (2: packed FP32x2 dual-strip op)
 };
-constexpr int kNumTmaConfigs = 8;
+constexpr int kNumTmaConfigs = 9;
 constexpr int kDefaultTmaConfig = 6;  // packed FP32x2 dual-strip core, 8 warps x 2 stages (bench r01)
 extern const TmaConfig kTmaConfigs[kNumTmaConfigs];
 

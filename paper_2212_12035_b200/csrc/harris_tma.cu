@@ -66,6 +66,8 @@ template <> struct F32Cfg<4> { static constexpr int NW = 4, NS = 3, CH = 6, MINB
 template <> struct F32Cfg<5> { static constexpr int NW = 6, NS = 3, CH = 3, MINB = 1, G = 2; };
 template <> struct F32Cfg<6> { static constexpr int NW = 8, NS = 2, CH = 3, MINB = 1, G = 2; };
 template <> struct F32Cfg<7> { static constexpr int NW = 4, NS = 4, CH = 3, MINB = 1, G = 2; };
+// scalar core, deep ring (small images: more of each short tile in flight)
+template <> struct F32Cfg<8> { static constexpr int NW = 8, NS = 4, CH = 3, MINB = 1, G = 1; };
 
 template <int CFG, bool EXACT>
 using F32OpOf = std::conditional_t<F32Cfg<CFG>::G == 2, HarrisF32x2Op<EXACT, F32Cfg<CFG>::CH>,
@@ -74,7 +76,7 @@ using F32OpOf = std::conditional_t<F32Cfg<CFG>::G == 2, HarrisF32x2Op<EXACT, F32
 #define HARRIS_CFG_ROW(k) {F32Cfg<k>::NW, F32Cfg<k>::NS, F32Cfg<k>::CH, F32Cfg<k>::G}
 const TmaConfig kTmaConfigs[kNumTmaConfigs] = {
     HARRIS_CFG_ROW(0), HARRIS_CFG_ROW(1), HARRIS_CFG_ROW(2), HARRIS_CFG_ROW(3),
-    HARRIS_CFG_ROW(4), HARRIS_CFG_ROW(5), HARRIS_CFG_ROW(6), HARRIS_CFG_ROW(7),
+    HARRIS_CFG_ROW(4), HARRIS_CFG_ROW(5), HARRIS_CFG_ROW(6), HARRIS_CFG_ROW(7), HARRIS_CFG_ROW(8),
 };
 #undef HARRIS_CFG_ROW
 
@@ -130,6 +132,7 @@ static cudaError_t occupancy_one(int* n) {
         case 5: return EXPR_T(5);       \
         case 6: return EXPR_T(6);       \
         case 7: return EXPR_T(7);       \
+        case 8: return EXPR_T(8);       \
         default: break;                 \
     }
 

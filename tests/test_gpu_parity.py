@@ -379,7 +379,7 @@ def _ctx_with(env: dict):
                 os.environ[k] = v
 
 
-@pytest.mark.parametrize("cfg", range(8))
+@pytest.mark.parametrize("cfg", range(9))
 def test_every_f32_tma_config_bitexact(cuda_ctx, cfg):
     """Every TMA kernel configuration (scalar and packed dual-strip cores), including a
     batch whose strip pairs straddle images and a single image with ragged strips."""

@@ -36,6 +36,23 @@ def main():
         r = subprocess.run([sys.executable, "-c", CODE.replace("ROOT", repr(ROOT))], env=env, capture_output=True,
                            text=True)
         print("cfg", cfg, r.stdout.strip()[-400:] or r.stderr[-400:], flush=True)
+    # floor: the same byte volume as a plain copy (45 MB read + 15 MB written), same flush
+    code = r"""
+import torch
+a = torch.empty(3 * 1536 * 2560, device='cuda'); b = torch.empty(1532 * 2556, device='cuda')
+s1 = torch.empty(1 << 28, device='cuda'); s2 = torch.empty(1 << 28, device='cuda')
+for _ in range(10): b.copy_(a[: b.numel()])
+evs = []
+for _ in range(30):
+    s1.fill_(0.0); s2.sum()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(); a.sum(); b.copy_(a[: b.numel()]); e1.record(); evs.append((e0, e1))
+torch.cuda.synchronize()
+ts = sorted(x.elapsed_time(y) for x, y in evs)
+print('copy-floor ms', ts[len(ts)//2], 'min', ts[0])
+"""
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
+    print(r.stdout.strip() or r.stderr[-300:], flush=True)
     n = 4 << 30
     h = torch.empty(n // 4, dtype=torch.float32, pin_memory=True)
     d = torch.empty(n // 4, dtype=torch.float32, device="cuda")
