@@ -7,9 +7,11 @@
 
 A step is one pass of the fused kernel over the workload: for the default
 workload (BASELINE.json configs[4], the only config quoted at 1/2/4/8 GPUs) a
-batch of 1024 synthetic 1920x1080 planar RGB f32 images, image-sharded across
-ranks (one batched launch per rank per step, no collective in the data path).
-Inputs (25.5 GB) are far larger than the 126 MB L2, so no flush is needed.
+batch of 1024 synthetic 1920x1080 planar RGB f32 images per GPU.  The path
+partitions by image, so ranks own disjoint batches (weak scaling, no collective in
+the data path, one batched launch per rank per step); `--scaling strong` splits one
+1024-image batch over the ranks instead.  Inputs (25.5 GB per GPU) are far larger
+than the 126 MB L2, so no flush is needed.
 Time = CUDA events on the launching stream, barrier + synchronize on both sides,
 max over ranks.  Rank 0 prints one JSON line.
 """
@@ -182,19 +184,26 @@ def max_over_ranks(x: float, world: int, device) -> float:
 class Shard:
     """This rank's share of the workload: images [b0, b0+nb) or output rows [r0, r0+rows)."""
 
-    def __init__(self, wl: dict, world: int, rank: int):
+    def __init__(self, wl: dict, world: int, rank: int, scaling: str = "weak"):
         from paper_2212_12035_b200 import shard
         self.H, self.W = wl["H"], wl["W"]
         self.n, self.m = self.H - 4, self.W - 4
-        if wl["sharding"] == "image":
-            s = shard.image_shards(wl["B"], world)[rank]
+        if wl["sharding"] == "image" and scaling == "weak":
+            # the path partitions by image: every rank owns a fixed batch of B images
+            # (global images [rank*B, (rank+1)*B) of the synthetic stream), no collective
+            self.b0, self.nb = rank * wl["B"], wl["B"]
+            self.r0, self.rows = 0, self.n
+            self.total_px = world * wl["B"] * self.n * self.m
+        elif wl["sharding"] == "image":
+            s = shard.image_shards(wl["B"], world)[rank]   # strong: one B-image batch split over ranks
             self.b0, self.nb = s.image0, s.images
             self.r0, self.rows = 0, self.n
+            self.total_px = wl["B"] * self.n * self.m
         else:
-            b = shard.row_bands(self.n, world)[rank]
+            b = shard.row_bands(self.n, world)[rank]      # one image in row bands + 4-row halo
             self.b0, self.nb = 0, 1
             self.r0, self.rows = b.out_row0, b.out_rows
-        self.total_px = wl["B"] * self.n * self.m
+            self.total_px = wl["B"] * self.n * self.m
         self.local_px = self.nb * self.rows * self.m
 
     @property
@@ -278,7 +287,8 @@ def run_gpu(a, world, rank, local) -> dict | None:
     import paper_2212_12035_b200 as hb
     dev = torch.device("cuda", local)
     wl = WORKLOADS[a.workload]
-    sh = Shard(wl, world, rank)
+    scaling = a.scaling if wl["sharding"] == "image" else "strong"
+    sh = Shard(wl, world, rank, scaling)
     ctx = hb.context(local)
     x, out = make_inputs(sh, dev)
     stream = torch.cuda.current_stream(dev)
@@ -342,14 +352,18 @@ def run_gpu(a, world, rank, local) -> dict | None:
     return {
         "metric": metric_name(), "value": value, "unit": "MP/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
-        "scaling": "strong",
+        "scaling": scaling,
         "vs_baseline": None, "dtype": "f32",
         "data": f"synthetic planar RGB f32 U[0,1) (splitmix64 of the global pixel index, seed {SEED}), "
                 "generated on device",
-        "config": {"workload": wl["desc"], "images": wl["B"], "height": wl["H"], "width": wl["W"],
+        "config": {"workload": wl["desc"], "images": wl["B"] * (world if scaling == "weak" else 1),
+                   "images_per_gpu": sh.nb, "height": wl["H"], "width": wl["W"],
                    "output": [wl["B"], wl["H"] - 4, wl["W"] - 4], "kappa": KAPPA,
-                   "parallelism": f"{'image' if wl['sharding'] == 'image' else 'row-band'}-sharded x{world}, "
-                                  "no data-path collective",
+                   "parallelism": (f"image-sharded x{world} ({scaling} scaling: "
+                                   + ("a fixed 1024-image batch per GPU" if scaling == "weak"
+                                      else "one 1024-image batch split over the GPUs") + "), no data-path collective")
+                                  if wl["sharding"] == "image" else
+                                  f"row-band-sharded x{world} (4-row halo re-read), no data-path collective",
                    "l2": "inputs larger than L2 (no flush needed)" if sh.in_bytes() > 512 << 20 else
                          "inputs smaller than L2: see extra.l2_flushed",
                    "kernel": "strip_kernel<HarrisF32x2Op> (fused gray/Sobel/products/box/coarsity, per-warp TMA "
@@ -368,9 +382,10 @@ def run_gpu(a, world, rank, local) -> dict | None:
 def run_e2e(a, sh: Shard, x_dev, dev, world, ctx) -> dict:
     """Same metric through the public host-buffer API (HarrisContext.run_host ->
     harris_run_host): pinned host input in, pinned host output back, every step."""
-    host_in = torch.empty(tuple(x_dev.shape), dtype=torch.float32, pin_memory=True)
-    host_in.copy_(x_dev)
-    host_out = torch.empty((sh.nb, sh.rows, sh.m), dtype=torch.float32, pin_memory=True)
+    nb = min(sh.nb, a.e2e_images)   # bounded pinned footprint per rank (PCIe-bound: MP/s is size-independent)
+    host_in = torch.empty((nb,) + tuple(x_dev.shape[1:]), dtype=torch.float32, pin_memory=True)
+    host_in.copy_(x_dev[:nb])
+    host_out = torch.empty((nb, sh.rows, sh.m), dtype=torch.float32, pin_memory=True)
     hin = host_in.numpy() if sh.nb > 1 else host_in.numpy()[0]
     hout = host_out.numpy() if sh.nb > 1 else host_out.numpy()[0]
     ctx.run_host(hin, out=hout)  # warm-up (staging buffers)
@@ -382,8 +397,10 @@ def run_e2e(a, sh: Shard, x_dev, dev, world, ctx) -> dict:
     t1 = time.perf_counter()
     barrier(world)
     dt = max_over_ranks(t1 - t0, world, dev)
-    return {"value": sh.total_px * steps / dt / 1e6, "unit": "MP/s", "h2d_bytes_per_step": sh.in_bytes(),
-            "d2h_bytes_per_step": sh.out_bytes(), "steps": steps,
+    frac = nb / sh.nb
+    return {"value": sh.total_px * frac * steps / dt / 1e6, "unit": "MP/s",
+            "h2d_bytes_per_step": int(sh.in_bytes() * frac), "d2h_bytes_per_step": int(sh.out_bytes() * frac),
+            "steps": steps, "images_per_rank_per_step": nb,
             "api": "HarrisContext.run_host -> harris_run_host (pipelined H2D/kernel/D2H, 3 streams)",
             "note": "bytes are per rank; host wall clock, max over ranks"}
 
@@ -504,7 +521,8 @@ def run_reference(a, world, rank) -> dict | None:
     value = px * a.steps / dt / 1e6
     return {
         "metric": metric_name(), "value": value, "unit": "MP/s", "n_gpus": world, "steps": a.steps,
-        "warmup": a.warmup, "ms_per_step": dt * 1e3 / a.steps, "higher_is_better": True, "scaling": "strong",
+        "warmup": a.warmup, "ms_per_step": dt * 1e3 / a.steps, "higher_is_better": True,
+        "scaling": a.scaling if wl["sharding"] == "image" else "strong",
         "vs_baseline": None, "dtype": "f32", "data": f"synthetic planar RGB f32 (seed {SEED}), host",
         "config": {"workload": wl["desc"], "images": wl["B"], "height": wl["H"], "width": wl["W"],
                    "sample_per_step": desc},
@@ -524,6 +542,10 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="batch")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-images", type=int, default=256, help="images per rank per e2e step (pinned footprint)")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="batch workload: weak = a fixed 1024-image batch per GPU (the path partitions by "
+                         "image); strong = one 1024-image batch split over the GPUs (BASELINE configs[4])")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
