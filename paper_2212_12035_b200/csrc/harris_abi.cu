@@ -33,6 +33,7 @@ struct harris_ctx {
     int sep_cfg = 0;
     int occ_sep[kNumSepConfigs] = {0};
     int occ_u8[kNumU8Configs] = {0};
+    int sync_waves = 1;  // dev knob HARRIS_SYNC_WAVES=0 disables the per-tile CTA barrier
     int l2_policy = 1;  // evict_normal: the 4-column halo sectors are re-read by the neighbouring strip
     int64_t force_band_rows = 0;  // dev knob (HARRIS_BAND_ROWS): override the planner
     CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;  // dev knob HARRIS_L2_PROMO
@@ -181,7 +182,7 @@ void plan_launch(const harris_ctx* ctx, const Call& c, TileGeom& tg, int64_t& gr
     tg.kappa = c.g.kappa;
     tg.l2_policy = ctx->l2_policy;
     tg.vec_store = aligned16(c.g.out) && (c.g.out_pitch & 3) == 0 && (c.g.batch == 1 || (c.g.out_image_stride & 3) == 0);
-    tg.pad_ = 0;
+    tg.sync_waves = ctx->sync_waves;
 }
 
 int encode_tmap_u8(harris_ctx* ctx, const Call& c, CUtensorMap* tmap) {
@@ -332,6 +333,8 @@ int harris_init(harris_ctx** out_ctx, int cuda_device) {
         int v = std::atoi(env);
         if (v >= 0 && v < kNumSepConfigs) ctx->sep_cfg = v;
     }
+    env = std::getenv("HARRIS_SYNC_WAVES");
+    if (env) ctx->sync_waves = std::atoi(env) != 0;
     env = std::getenv("HARRIS_L2_PROMO");
     if (env) {
         const int v = std::atoi(env);
@@ -476,7 +479,7 @@ int harris_stencil3x3_sep(harris_ctx* ctx, float* out, int64_t out_pitch, int64_
         tg.kappa = 0.f;
         tg.l2_policy = ctx->l2_policy;
         tg.vec_store = aligned16(out) && (out_pitch & 3) == 0 && (batch == 1 || (out_image_stride & 3) == 0);
-        tg.pad_ = 0;
+        tg.sync_waves = ctx->sync_waves;
         e = launch_tma_sep(ctx->sep_cfg, exact, tmap, tg, grid, wv, wh, stream);
     } else {
         e = launch_generic_sep(exact, in, in_pitch, img_stride, out, out_pitch,

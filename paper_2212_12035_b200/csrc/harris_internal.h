@@ -25,7 +25,7 @@ struct TileGeom {
     int32_t batch;
     int32_t l2_policy;  // 0 evict_first, 1 evict_normal (default), 2 evict_last
     int32_t vec_store;  // 1: output rows 16-byte aligned -> float4 streaming stores
-    int32_t pad_;
+    int32_t sync_waves; // 1: CTA barrier at every tile boundary (keeps neighbour strips in step)
     int64_t tiles;
     int64_t out_pitch, out_image_stride;
     float* out;

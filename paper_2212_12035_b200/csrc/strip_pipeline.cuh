@@ -109,7 +109,11 @@ __global__ void __launch_bounds__(NW * 32, MINB)
 
     const int64_t GW = int64_t(gridDim.x) * NW;
     const int64_t gw = int64_t(blockIdx.x) * NW + warp;
-    if (gw >= g.tiles) return;  // warps are independent: no CTA-wide barrier below
+    const int64_t cta0 = int64_t(blockIdx.x) * NW;  // first warp-tile index of this CTA
+    if (cta0 >= g.tiles) return;                    // whole CTA idle
+    // waves in which at least one warp of this CTA has a tile: every warp of the CTA runs
+    // this many wave iterations so the per-wave CTA barrier below is uniform
+    const int64_t waves = (g.tiles - cta0 + GW - 1) / GW;
 
     if (lane == 0) {
         prefetch_tmap(&tmap);
@@ -151,7 +155,15 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     Op op(p);
     int stage = 0;
     uint32_t phase = 0;
-    for (int64_t t = gw; t < g.tiles; t += GW) {
+    for (int64_t k = 0; k < waves; ++k) {
+        const int64_t t = gw + k * GW;
+        // Re-align the CTA's warps at every tile boundary.  They work on adjacent strips
+        // of the same band, whose 4-column halo sectors hit in L2 only while the warps
+        // stay within a few microseconds of each other; without this the highest-wid-first
+        // warp arbiter lets them drift apart over the waves and the halo re-reads miss
+        // (DRAM read over-fetch 2-6.5 % -> measured in profiles/ncu_configs_r01.json).
+        if (k > 0 && g.sync_waves) asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+        if (t >= g.tiles) continue;
         const TileCoord<G> tc = decode_tile<G>(t, g);
         const int rows_out = band_rows_out(tc.band, g);
         const int nch = (rows_out + HALO + CH - 1) / CH;
