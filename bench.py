@@ -293,8 +293,37 @@ def run_gpu(a, world, rank, local) -> dict | None:
     x, out = make_inputs(sh, dev)
     stream = torch.cuda.current_stream(dev)
 
-    def step():
-        hb.harris(x if wl["B"] > 1 else x[0], out=out if wl["B"] > 1 else out[0])
+    gather = a.gather if world > 1 else "none"
+    pg = None
+    if gather == "peer":
+        # fused compute + gather: the kernel stores straight into root's result (peer.py)
+        from paper_2212_12035_b200.peer import PeerGather
+        full = (world * sh.nb if scaling == "weak" else wl["B"], sh.n, sh.m) if wl["B"] > 1 else (sh.n, sh.m)
+        pg = PeerGather(full, root=0, device=local, buffers=1)
+        img0 = rank * sh.nb if scaling == "weak" else sh.b0
+
+        def step():
+            if wl["B"] > 1:
+                pg.run_images(x, img0)
+            else:
+                pg.run_rows(x[0], sh.r0)
+    elif gather == "nccl":
+        from paper_2212_12035_b200 import shard as _shard
+        if wl["B"] > 1:
+            shards = [_shard.ImageShard(r, r * sh.nb, sh.nb) for r in range(world)] if scaling == "weak" \
+                else _shard.image_shards(wl["B"], world)
+        else:
+            bands = _shard.row_bands(sh.n, world)
+
+        def step():
+            hb.harris(x if wl["B"] > 1 else x[0], out=out if wl["B"] > 1 else out[0])
+            if wl["B"] > 1:
+                _shard.gather_images(out, shards, root=0)
+            else:
+                _shard.gather_rows(out[0], bands, root=0)
+    else:
+        def step():
+            hb.harris(x if wl["B"] > 1 else x[0], out=out if wl["B"] > 1 else out[0])
 
     for _ in range(a.warmup):
         step()
@@ -317,6 +346,10 @@ def run_gpu(a, world, rank, local) -> dict | None:
     sampler.stop()
     local_ms = ev0.elapsed_time(ev1)
     ms = max_over_ranks(local_ms, world, dev)
+    if pg is not None:
+        pg.check()
+        pg.close()
+        pg = None
     clocks = sampler.summary(w0, w1)
     value = sh.total_px * a.steps / (ms * 1e-3) / 1e6
 
@@ -364,6 +397,9 @@ def run_gpu(a, world, rank, local) -> dict | None:
                                       else "one 1024-image batch split over the GPUs") + "), no data-path collective")
                                   if wl["sharding"] == "image" else
                                   f"row-band-sharded x{world} (4-row halo re-read), no data-path collective",
+                   "gather": {"none": "none (outputs stay sharded)",
+                              "peer": "fused: kernel stores into root's buffer over peer memory + device flags",
+                              "nccl": "kernel, then send/recv of the outputs to root"}[gather],
                    "l2": "inputs larger than L2 (no flush needed)" if sh.in_bytes() > 512 << 20 else
                          "inputs smaller than L2: see extra.l2_flushed",
                    "kernel": "strip_kernel<HarrisF32x2Op> (fused gray/Sobel/products/box/coarsity, per-warp TMA "
@@ -373,7 +409,9 @@ def run_gpu(a, world, rank, local) -> dict | None:
         "cpu_baseline": cpu,
         "e2e": e2e,
         "clocks": clocks,
-        "gpu_launches": a.steps,
+        # our kernels per step on rank 0: the fused kernel (+ release-signal and flag-wait
+        # kernels with the fused peer gather)
+        "gpu_launches": a.steps * (3 if gather == "peer" else 1),
         "impl": "b200",
         "extra": extra,
     }
@@ -552,6 +590,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-images", type=int, default=32)
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl")
+    ap.add_argument("--gather", choices=["none", "peer", "nccl"], default="none",
+                    help="N>1: also move every step's output to rank 0 inside the timed region (peer = fused "
+                         "kernel stores over NVLink peer memory; nccl = send/recv after the kernel)")
     a = ap.parse_args()
     a.warmup = max(3, a.warmup)
     world, rank, local = dist_setup(init=a.impl == "b200", backend=a.dist_backend)

@@ -154,6 +154,45 @@ HARRIS_API int harris_run_grouping(harris_ctx* ctx, int grouping, float* out, in
                                    const float* rgb, void* scratch, int64_t scratch_bytes, float kappa,
                                    uint32_t flags, void* cuda_stream);
 
+/* ---- fused gather over peer memory ("results gathered over NVLink only
+ * for the final output").  The root exports its result buffer and a flag array
+ * (one uint32 slot per rank); every rank maps both (CUDA IPC; NVLink 5 / NVSwitch P2P on
+ * a multi-GPU node) and calls harris_run_notify with `out` pointing at its rows / images
+ * inside the root's buffer: the fused kernel's output stores travel over the link as
+ * each row is produced, and its last CTA releases `epoch` into the rank's flag slot.
+ * The root enqueues harris_peer_wait on its stream; work queued after it sees the whole
+ * result.  No host barrier and no collective call in the data path. */
+typedef struct harris_peer_handle {
+    unsigned char ipc[64];  /* cudaIpcMemHandle_t of the allocation holding the pointer */
+    int64_t offset;         /* byte offset of the exported pointer inside the allocation */
+    int64_t bytes;          /* bytes from the exported pointer to the end of the allocation */
+    int32_t device;         /* exporting device ordinal */
+    int32_t reserved;
+} harris_peer_handle;
+
+/* export a device pointer (any address inside a cudaMalloc allocation) for other processes */
+HARRIS_API int harris_peer_export(const void* dev_ptr, harris_peer_handle* out);
+/* map an exported pointer on `cuda_device` (another process; peer access enabled lazily).
+ * *ptr = the exported address in this process; *mapping is what harris_peer_close takes. */
+HARRIS_API int harris_peer_open(int cuda_device, const harris_peer_handle* h, void** mapping, void** ptr);
+HARRIS_API int harris_peer_close(int cuda_device, void* mapping);
+
+/* harris_run_strided + completion notification: after every CTA's output stores are
+ * performed at system scope, the kernel's last CTA stores `epoch` to *notify_flag with
+ * release semantics (system scope).  notify_flag may be a peer mapping.  Calls with a
+ * notify flag must not run concurrently on one ctx (they share its CTA counter). */
+HARRIS_API int harris_run_notify(harris_ctx* ctx, float* out, int64_t out_pitch, int64_t out_image_stride,
+                                 int64_t n, int64_t m, const float* rgb, int64_t in_pitch,
+                                 int64_t in_chan_stride, int64_t in_image_stride, int64_t batch, float kappa,
+                                 uint32_t flags, uint32_t* notify_flag, uint32_t epoch, void* cuda_stream);
+/* store `epoch` to *flag (release, system scope) once earlier work on the stream is done
+ * (for a rank that owns no rows) */
+HARRIS_API int harris_peer_signal(uint32_t* flag, uint32_t epoch, void* cuda_stream);
+/* stream-ordered wait until every flags[i] >= epoch (modular); gives up after timeout_ns
+ * (<= 0: never) and then ORs 1 into *status (device memory, may be NULL) */
+HARRIS_API int harris_peer_wait(const uint32_t* flags, int32_t count, uint32_t epoch, uint32_t* status,
+                                int64_t timeout_ns, void* cuda_stream);
+
 /* Launch geometry the TMA kernel would use (for tests / bench reporting). */
 typedef struct harris_plan_info {
     int32_t path;           /* HARRIS_PATH_* that harris_run_strided would take */

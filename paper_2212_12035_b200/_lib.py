@@ -38,6 +38,8 @@ EXPORTED_SYMBOLS = (
     "harris_num_sms", "harris_strerror", "harris_last_cuda_error", "harris_abi_version",
     "harris_grouping_scratch_bytes", "harris_grouping_launches", "harris_run_grouping",
     "harris_run_u8", "harris_run_host_u8", "harris_stencil3x3_sep",
+    "harris_peer_export", "harris_peer_open", "harris_peer_close", "harris_run_notify",
+    "harris_peer_signal", "harris_peer_wait",
 )
 
 GROUPING_UNFUSED, GROUPING_SOBEL_PROD, GROUPING_SOBEL, GROUPING_FUSED = 1, 2, 3, 4
@@ -62,6 +64,23 @@ class PlanInfo(ctypes.Structure):
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class PeerHandle(ctypes.Structure):
+    """harris_peer_handle: a CUDA IPC handle plus the pointer's offset in its allocation."""
+    _fields_ = [("ipc", ctypes.c_ubyte * 64), ("offset", ctypes.c_int64), ("bytes", ctypes.c_int64),
+                ("device", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+    def to_bytes(self) -> bytes:
+        return bytes(ctypes.string_at(ctypes.addressof(self), ctypes.sizeof(self)))
+
+    @classmethod
+    def from_bytes(cls, b: bytes) -> "PeerHandle":
+        if len(b) != ctypes.sizeof(cls):
+            raise ValueError("bad harris_peer_handle size")
+        h = cls()
+        ctypes.memmove(ctypes.addressof(h), b, len(b))
+        return h
 
 
 _lib = None
@@ -106,6 +125,12 @@ def lib() -> ctypes.CDLL:
         "harris_run_host_u8": ([vp, vp, i64, i64, i64, vp, i64, f32, u32], i32),
         "harris_stencil3x3_sep": ([vp, vp, i64, i64, i64, i64, vp, i64, i64, i64, ctypes.POINTER(f32),
                                    ctypes.POINTER(f32), u32, vp], i32),
+        "harris_peer_export": ([vp, ctypes.POINTER(PeerHandle)], i32),
+        "harris_peer_open": ([i32, ctypes.POINTER(PeerHandle), ctypes.POINTER(vp), ctypes.POINTER(vp)], i32),
+        "harris_peer_close": ([i32, vp], i32),
+        "harris_run_notify": ([vp, vp, i64, i64, i64, i64, vp, i64, i64, i64, i64, f32, u32, vp, u32, vp], i32),
+        "harris_peer_signal": ([vp, u32, vp], i32),
+        "harris_peer_wait": ([vp, i32, u32, vp, i64, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

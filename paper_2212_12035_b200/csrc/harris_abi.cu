@@ -47,6 +47,9 @@ struct harris_ctx {
     float* d_in[kSlots] = {nullptr, nullptr, nullptr};
     float* d_out[kSlots] = {nullptr, nullptr, nullptr};
     size_t cap_in = 0, cap_out = 0;
+    // finished-CTA counter of harris_run_notify (allocated on first use, zeroed; the
+    // kernel's last CTA resets it)
+    uint32_t* d_notify_counter = nullptr;
 };
 
 namespace {
@@ -78,6 +81,8 @@ struct Call {
     Geom g;
     uint32_t flags;
     int fmt = kF32Planar;  // u8: g.rgb is the byte base, in_pitch / in_image_stride are bytes
+    uint32_t* notify_flag = nullptr;  // harris_run_notify
+    uint32_t notify_epoch = 0;
 };
 
 int validate(const Call& c) {
@@ -241,10 +246,16 @@ int run(harris_ctx* ctx, const Call& c, cudaStream_t stream) {
         TileGeom tg;
         int64_t grid = 0;
         plan_launch(ctx, c, tg, grid);
+        if (c.notify_flag) {
+            tg.notify_counter = ctx->d_notify_counter;
+            tg.notify_flag = c.notify_flag;
+            tg.notify_epoch = c.notify_epoch;
+        }
         e = c.fmt == kU8Interleaved ? launch_tma_u8(ctx->u8_cfg, exact, tmap, tg, grid, stream)
                                     : launch_tma(ctx->tma_cfg, exact, tmap, tg, grid, stream);
     } else {
         e = c.fmt == kU8Interleaved ? launch_generic_u8(exact, c.g, stream) : launch_generic(exact, c.g, stream);
+        if (e == cudaSuccess && c.notify_flag) e = launch_peer_signal(c.notify_flag, c.notify_epoch, stream);
     }
     if (e != cudaSuccess) return cuda_fail(ctx, e, path == HARRIS_PATH_TMA ? "launch tma" : "launch generic");
     ctx->last_path = path;
@@ -400,6 +411,7 @@ void harris_destroy(harris_ctx* ctx) {
             cudaFree(ctx->d_in[k]);
             cudaFree(ctx->d_out[k]);
         }
+        cudaFree(ctx->d_notify_counter);
     }
     delete ctx;
 }
@@ -425,6 +437,29 @@ int harris_run_strided(harris_ctx* ctx, float* out, int64_t out_pitch, int64_t o
                make_call(out, out_pitch, out_image_stride, n, m, rgb, in_pitch, in_chan_stride, in_image_stride,
                          batch, kappa, flags),
                static_cast<cudaStream_t>(stream));
+}
+
+int harris_run_notify(harris_ctx* ctx, float* out, int64_t out_pitch, int64_t out_image_stride, int64_t n,
+                      int64_t m, const float* rgb, int64_t in_pitch, int64_t in_chan_stride, int64_t in_image_stride,
+                      int64_t batch, float kappa, uint32_t flags, uint32_t* notify_flag, uint32_t epoch,
+                      void* stream) {
+    if (!ctx || !notify_flag) return HARRIS_ERR_INVALID_ARGUMENT;
+    if (!ctx->d_notify_counter) {
+        DeviceGuard guard(ctx->device);
+        if (!guard.ok) return cuda_fail(ctx, cudaGetLastError(), "cudaSetDevice");
+        cudaError_t e = cudaMalloc(&ctx->d_notify_counter, sizeof(uint32_t));
+        if (e == cudaSuccess) e = cudaMemset(ctx->d_notify_counter, 0, sizeof(uint32_t));
+        if (e != cudaSuccess) {
+            cudaFree(ctx->d_notify_counter);
+            ctx->d_notify_counter = nullptr;
+            return cuda_fail(ctx, e, "notify counter");
+        }
+    }
+    Call c = make_call(out, out_pitch, out_image_stride, n, m, rgb, in_pitch, in_chan_stride, in_image_stride, batch,
+                       kappa, flags);
+    c.notify_flag = notify_flag;
+    c.notify_epoch = epoch;
+    return run(ctx, c, static_cast<cudaStream_t>(stream));
 }
 
 int harris_run_u8(harris_ctx* ctx, float* out, int64_t out_pitch, int64_t out_image_stride, int64_t n, int64_t m,

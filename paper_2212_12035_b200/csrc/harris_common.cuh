@@ -110,6 +110,16 @@ __device__ __forceinline__ void stg128_cs(float* p, float a, float b, float c, f
                  : "memory");
 }
 
+// system-scope release store / acquire load (cross-GPU flags of the fused gather)
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 // ------------------------------------------------------------ exact arithmetic
 __device__ __forceinline__ float gray_exact(float r, float g, float b) {
     float t = __fadd_rn(0.0f, __fmul_rn(kGrayR, r));

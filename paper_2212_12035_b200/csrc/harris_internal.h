@@ -30,6 +30,13 @@ struct TileGeom {
     int64_t out_pitch, out_image_stride;
     float* out;
     float kappa;
+    // completion notification (harris_run_notify): when notify_flag != nullptr, the last
+    // CTA to finish stores notify_epoch to *notify_flag (release, system scope) after every
+    // CTA's output stores are performed at system scope; notify_counter (device, zeroed)
+    // counts finished CTAs and is reset by that last CTA.
+    uint32_t* notify_counter = nullptr;
+    uint32_t* notify_flag = nullptr;
+    uint32_t notify_epoch = 0;
 };
 
 // TMA kernel configurations (warps per CTA, pipeline stages per warp, input rows
@@ -79,5 +86,10 @@ cudaError_t launch_grouping(int grouping, float* out, int64_t n, int64_t m, cons
 cudaError_t launch_synth(float* dst, int64_t planes, int64_t rows, int64_t W, int64_t dst_pitch,
                          int64_t dst_plane_stride, int64_t H_global, int64_t row0, int64_t plane0,
                          uint64_t seed, int dist, int num_sms, cudaStream_t stream);
+
+// fused-gather completion signalling (harris_peer.cu)
+cudaError_t launch_peer_signal(uint32_t* flag, uint32_t epoch, cudaStream_t stream);
+cudaError_t launch_peer_wait(const uint32_t* flags, int32_t count, uint32_t epoch, uint32_t* status,
+                             int64_t timeout_ns, cudaStream_t stream);
 
 }  // namespace harris

@@ -91,6 +91,25 @@ struct StripShape {
     static constexpr size_t kSmemBytes = size_t(NW) * NS * Op::kStageBytes + size_t(NW) * NS * 8 + 128;
 };
 
+// Completion notification for fused gathers (TileGeom::notify_flag): every thread
+// fences its output stores at system scope (they may be NVLink stores into a peer's
+// buffer), the CTA meets at a barrier, and the last CTA to count itself in resets the
+// counter and releases the epoch into the flag — the consumer on the other GPU acquires
+// it (harris_peer_wait) and then sees every output row of this launch.
+__device__ __forceinline__ void notify_epilogue(const TileGeom& g) {
+    if (g.notify_flag == nullptr) return;
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned done = atomicAdd(g.notify_counter, 1u);
+        if (done == gridDim.x - 1) {
+            __threadfence_system();  // acquire side of the other CTAs' fence + count
+            *reinterpret_cast<volatile uint32_t*>(g.notify_counter) = 0u;
+            st_release_sys(g.notify_flag, g.notify_epoch);
+        }
+    }
+}
+
 template <class Op, int NW, int NS, int MINB = 1>
 __global__ void __launch_bounds__(NW * 32, MINB)
     strip_kernel(const __grid_constant__ CUtensorMap tmap, const TileGeom g, const typename Op::Params p) {
@@ -110,7 +129,10 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     const int64_t GW = int64_t(gridDim.x) * NW;
     const int64_t gw = int64_t(blockIdx.x) * NW + warp;
     const int64_t cta0 = int64_t(blockIdx.x) * NW;  // first warp-tile index of this CTA
-    if (cta0 >= g.tiles) return;                    // whole CTA idle
+    if (cta0 >= g.tiles) {                          // whole CTA idle
+        notify_epilogue(g);
+        return;
+    }
     // waves in which at least one warp of this CTA has a tile: every warp of the CTA runs
     // this many wave iterations so the per-wave CTA barrier below is uniform
     const int64_t waves = (g.tiles - cta0 + GW - 1) / GW;
@@ -210,6 +232,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
             }
         }
     }
+    notify_epilogue(g);
 }
 
 }  // namespace harris

@@ -84,3 +84,34 @@ def test_algorithmic_bytes():
 def test_python_wrapper_validates_before_cuda():
     with pytest.raises((ValueError, TypeError)):
         hb.harris(torch.zeros((2, 10, 10)).cuda() if torch.cuda.is_available() else torch.zeros((4, 3, 2, 2, 2)))
+
+
+def test_peer_entry_points_validate_without_a_device():
+    """The fused-gather entry points reject bad arguments before touching CUDA."""
+    L = _lib.lib()
+    h = _lib.PeerHandle()
+    assert L.harris_peer_export(None, ctypes.byref(h)) == _lib.HARRIS_ERR_INVALID_ARGUMENT
+    mp, p = ctypes.c_void_p(), ctypes.c_void_p()
+    assert L.harris_peer_open(0, None, ctypes.byref(mp), ctypes.byref(p)) == _lib.HARRIS_ERR_INVALID_ARGUMENT
+    bad = _lib.PeerHandle()
+    bad.offset = -1
+    assert L.harris_peer_open(0, ctypes.byref(bad), ctypes.byref(mp), ctypes.byref(p)) == \
+        _lib.HARRIS_ERR_INVALID_ARGUMENT
+    assert L.harris_peer_close(0, None) == _lib.HARRIS_OK
+    assert L.harris_peer_signal(None, 1, None) == _lib.HARRIS_ERR_INVALID_ARGUMENT
+    assert L.harris_peer_wait(None, 0, 1, None, 0, None) == _lib.HARRIS_OK
+    assert L.harris_peer_wait(None, -1, 1, None, 0, None) == _lib.HARRIS_ERR_INVALID_ARGUMENT
+    assert L.harris_peer_wait(None, 2, 1, None, 0, None) == _lib.HARRIS_ERR_INVALID_ARGUMENT
+    assert L.harris_run_notify(None, None, 8, 64, 4, 4, None, 8, 64, 192, 1, 0.04, 0, None, 1, None) == \
+        _lib.HARRIS_ERR_INVALID_ARGUMENT
+
+
+def test_peer_handle_layout_and_roundtrip():
+    # harris_peer_handle: 64-byte IPC handle, int64 offset, int64 bytes, int32 device, int32 reserved
+    assert ctypes.sizeof(_lib.PeerHandle) == 64 + 8 + 8 + 4 + 4
+    h = _lib.PeerHandle()
+    for i in range(64):
+        h.ipc[i] = (7 * i) & 0xFF
+    h.offset, h.bytes, h.device = 4096, 1 << 30, 3
+    g = _lib.PeerHandle.from_bytes(h.to_bytes())
+    assert bytes(g.ipc) == bytes(h.ipc) and (g.offset, g.bytes, g.device) == (4096, 1 << 30, 3)

@@ -112,3 +112,24 @@ def test_gloo_shard_and_gather(world):
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
     ok_rows, ok_imgs = q.get(timeout=5)
     assert ok_rows and ok_imgs
+
+
+def test_peer_gather_offsets_tile_the_result():
+    """The fused gather's per-rank output offsets (peer.py) place every band / image
+    shard exactly once inside the root's result."""
+    from paper_2212_12035_b200 import peer
+    n, m = 1076, 1916
+    for G in (1, 2, 3, 8):
+        covered = np.zeros(n, dtype=np.int32)
+        for b in shard.row_bands(n, G):
+            off = peer.band_offset_elems(b.out_row0, m)
+            assert off % m == 0
+            covered[off // m: off // m + b.out_rows] += 1
+        assert (covered == 1).all()
+        B = 1024
+        seen = np.zeros(B, dtype=np.int32)
+        for s in shard.image_shards(B, G):
+            off = peer.image_offset_elems(s.image0, n, m)
+            assert off == s.image0 * n * m
+            seen[s.image0: s.image0 + s.images] += 1
+        assert (seen == 1).all()
