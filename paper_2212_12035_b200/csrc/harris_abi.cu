@@ -29,6 +29,7 @@ struct harris_ctx {
     int num_sms = 0;
     int cc_major = 0, cc_minor = 0;
     int tma_cfg = kDefaultTmaConfig;
+    bool tma_cfg_forced = false;  // HARRIS_TMA_CONFIG given: no per-call choice
     int u8_cfg = 0;
     int sep_cfg = 0;
     int occ_sep[kNumSepConfigs] = {0};
@@ -83,6 +84,7 @@ struct Call {
     int fmt = kF32Planar;  // u8: g.rgb is the byte base, in_pitch / in_image_stride are bytes
     uint32_t* notify_flag = nullptr;  // harris_run_notify
     uint32_t notify_epoch = 0;
+    int cfg = -1;  // f32 TMA configuration chosen for this call (resolve_cfg)
 };
 
 int validate(const Call& c) {
@@ -175,8 +177,9 @@ int choose_path(const Call& c) {
 
 void plan_launch(const harris_ctx* ctx, const Call& c, TileGeom& tg, int64_t& grid) {
     const bool u8 = c.fmt == kU8Interleaved;
-    const TmaConfig& cfg = u8 ? kU8Configs[ctx->u8_cfg] : kTmaConfigs[ctx->tma_cfg];
-    const int occ = std::max(1, u8 ? ctx->occ_u8[ctx->u8_cfg] : ctx->occ[ctx->tma_cfg]);
+    const int fcfg = c.cfg >= 0 ? c.cfg : ctx->tma_cfg;
+    const TmaConfig& cfg = u8 ? kU8Configs[ctx->u8_cfg] : kTmaConfigs[fcfg];
+    const int occ = std::max(1, u8 ? ctx->occ_u8[ctx->u8_cfg] : ctx->occ[fcfg]);
     const int64_t resident_ctas = int64_t(ctx->num_sms) * occ;
     plan_tiles(c.g.n, c.g.m, c.g.batch, resident_ctas * cfg.warps, cfg.rows, ctx->force_band_rows, tg, 4,
                cfg.groups);
@@ -188,6 +191,22 @@ void plan_launch(const harris_ctx* ctx, const Call& c, TileGeom& tg, int64_t& gr
     tg.l2_policy = ctx->l2_policy;
     tg.vec_store = aligned16(c.g.out) && (c.g.out_pitch & 3) == 0 && (c.g.batch == 1 || (c.g.out_image_stride & 3) == 0);
     tg.sync_waves = ctx->sync_waves;
+}
+
+// Short tiles (a small image fills the GPU with a few rows per warp): the pipeline ramp
+// dominates and the scalar single-strip core over all SMs beats the packed dual-strip
+// core (configs[1] 1536x2560: 18.5 vs 20.5 us, profiles/small_image_probe_r01.txt).
+constexpr int kShortTileRows = 32;
+constexpr int kShortTileTmaConfig = 0;
+
+int resolve_cfg(const harris_ctx* ctx, const Call& c) {
+    if (c.fmt == kU8Interleaved || ctx->tma_cfg_forced) return ctx->tma_cfg;
+    Call probe = c;
+    probe.cfg = ctx->tma_cfg;
+    TileGeom tg;
+    int64_t grid = 0;
+    plan_launch(ctx, probe, tg, grid);
+    return tg.band_rows < kShortTileRows ? kShortTileTmaConfig : ctx->tma_cfg;
 }
 
 int encode_tmap_u8(harris_ctx* ctx, const Call& c, CUtensorMap* tmap) {
@@ -212,7 +231,7 @@ int encode_tmap_u8(harris_ctx* ctx, const Call& c, CUtensorMap* tmap) {
 int encode_tmap(harris_ctx* ctx, const Call& c, CUtensorMap* tmap) {
     if (c.fmt == kU8Interleaved) return encode_tmap_u8(ctx, c, tmap);
     const Geom& g = c.g;
-    const TmaConfig& cfg = kTmaConfigs[ctx->tma_cfg];
+    const TmaConfig& cfg = kTmaConfigs[c.cfg >= 0 ? c.cfg : ctx->tma_cfg];
     cuuint64_t dims[4] = {cuuint64_t(g.m + 4), cuuint64_t(g.n + 4), 3, cuuint64_t(g.batch)};
     const int64_t img_stride = g.batch > 1 ? g.in_image_stride : 3 * g.in_chan_stride;
     cuuint64_t strides[3] = {cuuint64_t(g.in_pitch) * 4, cuuint64_t(g.in_chan_stride) * 4,
@@ -240,6 +259,9 @@ int run(harris_ctx* ctx, const Call& c, cudaStream_t stream) {
     if (!guard.ok) return cuda_fail(ctx, cudaGetLastError(), "cudaSetDevice");
     cudaError_t e;
     if (path == HARRIS_PATH_TMA) {
+        Call cc = c;
+        cc.cfg = resolve_cfg(ctx, c);
+        const Call& c = cc;
         CUtensorMap tmap;
         rc = encode_tmap(ctx, c, &tmap);
         if (rc) return rc;
@@ -252,7 +274,7 @@ int run(harris_ctx* ctx, const Call& c, cudaStream_t stream) {
             tg.notify_epoch = c.notify_epoch;
         }
         e = c.fmt == kU8Interleaved ? launch_tma_u8(ctx->u8_cfg, exact, tmap, tg, grid, stream)
-                                    : launch_tma(ctx->tma_cfg, exact, tmap, tg, grid, stream);
+                                    : launch_tma(c.cfg, exact, tmap, tg, grid, stream);
     } else {
         e = c.fmt == kU8Interleaved ? launch_generic_u8(exact, c.g, stream) : launch_generic(exact, c.g, stream);
         if (e == cudaSuccess && c.notify_flag) e = launch_peer_signal(c.notify_flag, c.notify_epoch, stream);
@@ -332,7 +354,10 @@ int harris_init(harris_ctx** out_ctx, int cuda_device) {
     const char* env = std::getenv("HARRIS_TMA_CONFIG");
     if (env) {
         int v = std::atoi(env);
-        if (v >= 0 && v < kNumTmaConfigs) ctx->tma_cfg = v;
+        if (v >= 0 && v < kNumTmaConfigs) {
+            ctx->tma_cfg = v;
+            ctx->tma_cfg_forced = true;
+        }
     }
     env = std::getenv("HARRIS_U8_CONFIG");
     if (env) {
@@ -536,7 +561,8 @@ int harris_plan(harris_ctx* ctx, int64_t n, int64_t m, int64_t batch, const floa
     if (rc) return rc;
     std::memset(info, 0, sizeof(*info));
     info->path = choose_path(c);
-    const TmaConfig& cfg = kTmaConfigs[ctx->tma_cfg];
+    c.cfg = resolve_cfg(ctx, c);
+    const TmaConfig& cfg = kTmaConfigs[c.cfg];
     info->warps_per_cta = cfg.warps;
     info->stages = cfg.stages;
     info->rows_per_stage = cfg.rows;
@@ -548,9 +574,9 @@ int harris_plan(harris_ctx* ctx, int64_t n, int64_t m, int64_t batch, const floa
     info->col_segments = tg.colsegs;
     info->tiles = tg.tiles;
     info->grid_ctas = grid;
-    info->smem_bytes = int64_t(tma_smem_bytes(ctx->tma_cfg));
+    info->smem_bytes = int64_t(tma_smem_bytes(c.cfg));
     info->groups = cfg.groups;
-    info->tma_config = ctx->tma_cfg;
+    info->tma_config = c.cfg;
     return HARRIS_OK;
 }
 

@@ -228,6 +228,11 @@ def test_plan_geometry(cuda_ctx):
     assert info["col_segments"] == 64
     assert info["bands"] * info["band_rows"] >= 8188
     assert info["grid_ctas"] % cuda_ctx.num_sms == 0 or info["grid_ctas"] * info["warps_per_cta"] >= info["tiles"]
+    # long tiles run the packed dual-strip core; short tiles (small images) the scalar core
+    if "HARRIS_TMA_CONFIG" not in __import__("os").environ:
+        assert info["tma_config"] == 6 and info["groups"] == 2
+        small = cuda_ctx.plan(1532, 2556)
+        assert small["tma_config"] == 0 and small["groups"] == 1
 
 
 @pytest.mark.parametrize("grouping", [1, 2, 3, 4])
