@@ -3,8 +3,9 @@
 //
 // Work decomposition: a *tile* is one 128-output-column warp strip x
 // `band_rows` output rows of one image (TileGeom).  A persistent grid of
-// NW-warp CTAs strides its warps over tiles; each warp is independent (no
-// CTA-wide barrier anywhere): it owns an NS-stage shared-memory ring, and its
+// NW-warp CTAs strides its warps over tiles; each warp runs its own pipeline (the
+// only CTA-wide barrier is one named barrier per tile wave that keeps neighbouring
+// strips in step for L2 halo reuse): it owns an NS-stage shared-memory ring, and its
 // lane 0 issues one TMA box per stage (Op::load) completing on the stage's
 // mbarrier.  The producer cursor runs NS stages ahead of the consumer and keeps
 // going across tile boundaries, so the pipeline never drains between tiles.
