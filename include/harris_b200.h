@@ -201,12 +201,14 @@ typedef struct harris_plan_info {
     int32_t rows_per_stage;
     int64_t band_rows;      /* output rows per tile */
     int64_t bands;          /* tiles per image column */
-    int64_t col_segments;   /* 128-column warp strips per image */
+    int64_t col_segments;   /* warp strips per image row (strip_cols columns each) */
     int64_t tiles;          /* batch * bands * col_segments */
     int64_t grid_ctas;
     int64_t smem_bytes;     /* dynamic shared memory per CTA */
     int32_t groups;         /* 128-column strips per tile (2: packed FP32x2 dual-strip core) */
     int32_t tma_config;     /* kernel configuration index (HARRIS_TMA_CONFIG) */
+    int32_t strip_cols;     /* output columns per strip (128, or 124 with the lane-halo layout) */
+    int32_t reserved;
 } harris_plan_info;
 
 HARRIS_API int harris_plan(harris_ctx* ctx, int64_t n, int64_t m, int64_t batch, const float* rgb,

@@ -60,10 +60,11 @@ class PlanInfo(ctypes.Structure):
         ("rows_per_stage", ctypes.c_int32), ("band_rows", ctypes.c_int64), ("bands", ctypes.c_int64),
         ("col_segments", ctypes.c_int64), ("tiles", ctypes.c_int64), ("grid_ctas", ctypes.c_int64),
         ("smem_bytes", ctypes.c_int64), ("groups", ctypes.c_int32), ("tma_config", ctypes.c_int32),
+        ("strip_cols", ctypes.c_int32), ("reserved", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
 
 
 class PeerHandle(ctypes.Structure):

@@ -30,7 +30,7 @@ struct harris_ctx {
     int cc_major = 0, cc_minor = 0;
     int tma_cfg = kDefaultTmaConfig;
     bool tma_cfg_forced = false;  // HARRIS_TMA_CONFIG given: no per-call choice
-    int u8_cfg = 0;
+    int u8_cfg = kDefaultU8Config;
     int sep_cfg = 0;
     int occ_sep[kNumSepConfigs] = {0};
     int occ_u8[kNumU8Configs] = {0};
@@ -134,8 +134,8 @@ bool tma_eligible(const Call& c) {
 // of `gw` warps.  A tile is `groups` 128-column strips: with groups == 2 the strips
 // of one band row of all images are paired consecutively (strip_pipeline.cuh).
 void plan_tiles(int64_t n, int64_t m, int64_t batch, int64_t gw, int rows_per_stage, int64_t force_rows,
-                TileGeom& tg, int halo = 4, int groups = 1) {
-    const int64_t colsegs = (m + kWarpCols - 1) / kWarpCols;
+                TileGeom& tg, int halo = 4, int groups = 1, int strip_cols = kWarpCols) {
+    const int64_t colsegs = (m + strip_cols - 1) / strip_cols;
     const int64_t units_per_band = groups == 2 ? (batch * colsegs + 1) / 2 : batch * colsegs;
     tg.n = int32_t(n);
     tg.m = int32_t(m);
@@ -182,7 +182,7 @@ void plan_launch(const harris_ctx* ctx, const Call& c, TileGeom& tg, int64_t& gr
     const int occ = std::max(1, u8 ? ctx->occ_u8[ctx->u8_cfg] : ctx->occ[fcfg]);
     const int64_t resident_ctas = int64_t(ctx->num_sms) * occ;
     plan_tiles(c.g.n, c.g.m, c.g.batch, resident_ctas * cfg.warps, cfg.rows, ctx->force_band_rows, tg, 4,
-               cfg.groups);
+               cfg.groups, cfg.strip_cols);
     grid = std::min<int64_t>((tg.tiles + cfg.warps - 1) / cfg.warps, resident_ctas);
     tg.out = c.g.out;
     tg.out_pitch = c.g.out_pitch;
@@ -236,7 +236,7 @@ int encode_tmap(harris_ctx* ctx, const Call& c, CUtensorMap* tmap) {
     const int64_t img_stride = g.batch > 1 ? g.in_image_stride : 3 * g.in_chan_stride;
     cuuint64_t strides[3] = {cuuint64_t(g.in_pitch) * 4, cuuint64_t(g.in_chan_stride) * 4,
                              cuuint64_t(img_stride) * 4};
-    cuuint32_t box[4] = {cuuint32_t(kBoxCols), cuuint32_t(cfg.rows), 3, 1};
+    cuuint32_t box[4] = {cuuint32_t(cfg.strip_cols + 4), cuuint32_t(cfg.rows), 3, 1};
     cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = ctx->encode(tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(g.rgb), dims, strides,
                              box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -577,6 +577,7 @@ int harris_plan(harris_ctx* ctx, int64_t n, int64_t m, int64_t batch, const floa
     info->smem_bytes = int64_t(tma_smem_bytes(c.cfg));
     info->groups = cfg.groups;
     info->tma_config = c.cfg;
+    info->strip_cols = cfg.strip_cols;
     return HARRIS_OK;
 }
 

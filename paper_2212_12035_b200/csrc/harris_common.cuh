@@ -30,6 +30,34 @@ constexpr int kWarpCols = kLanes * kColsPerLane;    // 128 output columns per wa
 constexpr int kBoxCols = kWarpCols + 4;             // + 4-column halo = 132 input columns
 constexpr int kU8BoxWords = 100;  // u8 HWC box: 400 bytes >= 132 px * 3 B (TMA inner box: 16-B multiple)
 
+// Strip layouts of the Harris ops (template parameter SC = output columns per strip):
+//   SC = 128: every lane owns 4 output columns; lane 31 loads and converts the box's
+//             4-column right halo itself (a divergent branch every row).
+//   SC = 124: lane 31 owns the halo columns: it converts them like any other lane and
+//             hands them to lane 30 through the same shuffle every lane uses, and stores
+//             nothing.  No branch, no extra loads / gray math, 1/32 of the lanes idle.
+// Box width = SC + 4 columns (f32: 132 / 128; u8: 100 / 96 words).
+template <int SC>
+struct Strip {
+    static_assert(SC == 128 || SC == 124, "strip layouts: 128 or 124 columns");
+    static constexpr int kCols = SC;
+    static constexpr int kBoxCols = SC + 4;
+    static constexpr bool kLaneHalo = SC == 124;  // lane 31 is the halo lane
+    // u8 tensor map over 32-bit words: a strip starts at word cs * kU8Words; TMA box starts
+    // must be 16-byte aligned, so with SC = 124 (93 words per strip) the box starts at the
+    // word rounded down to a multiple of 4 and the row reads skip the remainder (<= 3)
+    static constexpr int kU8Words = SC * 3 / 4;
+    static constexpr int kU8BoxWords = 100;       // >= 3 + 96 words; 400 B (16-B multiple)
+    __host__ __device__ static constexpr int u8_box_word(int cs) { return (cs * kU8Words) & ~3; }
+    __host__ __device__ static constexpr int u8_skip(int cs) { return (cs * kU8Words) & 3; }
+};
+
+// HaloFn placeholder of the lane-halo layout: the core skips the lane-31 branch
+struct NoHalo {
+    template <class... A>
+    __device__ __forceinline__ void operator()(A&...) const {}
+};
+
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -43,9 +43,10 @@ struct TileGeom {
 // per stage).  Index 0 is the default; HARRIS_TMA_CONFIG selects another one.
 struct TmaConfig {
     int warps, stages, rows;
-    int groups = 1;  // 128-column strips per tile (2: packed FP32x2 dual-strip op)
+    int groups = 1;        // strips per tile (2: packed FP32x2 dual-strip op)
+    int strip_cols = 128;  // output columns per strip (124: lane 31 is the halo lane)
 };
-constexpr int kNumTmaConfigs = 9;
+constexpr int kNumTmaConfigs = 11;
 constexpr int kDefaultTmaConfig = 6;  // packed FP32x2 dual-strip core, 8 warps x 2 stages (bench r01)
 extern const TmaConfig kTmaConfigs[kNumTmaConfigs];
 
@@ -59,7 +60,10 @@ cudaError_t launch_generic(bool exact, const Geom& g, cudaStream_t stream);
 
 // interleaved RGB u8 (HWC) input: TMA configs + generic fallback (Geom.rgb is then the
 // byte base pointer; in_pitch / in_image_stride are in BYTES, in_chan_stride unused)
-constexpr int kNumU8Configs = 5;
+constexpr int kNumU8Configs = 7;
+// 124-column lane-halo strips, scalar core, 16 warps/SM: the u8 op is issue-bound and the
+// halo branch was ~17 % of its instructions (510 k -> 585 k MP/s on configs[4] as u8)
+constexpr int kDefaultU8Config = 5;
 extern const TmaConfig kU8Configs[kNumU8Configs];
 size_t u8_smem_bytes(int cfg);
 cudaError_t u8_configure(int cfg);

@@ -20,6 +20,7 @@
 #include <cuda.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "harris_common.cuh"
 
@@ -76,7 +77,8 @@ struct HarrisCore {
             for (int k = 0; k < 4; ++k) gr[k] = gown[k];
 #pragma unroll
             for (int k = 0; k < 4; ++k) gr[4 + k] = __shfl_down_sync(0xffffffffu, gr[k], 1);
-            if (lane == 31) halo(gr[4], gr[5], gr[6], gr[7]);
+            if constexpr (!std::is_same_v<std::decay_t<HaloFn>, NoHalo>)
+                if (lane == 31) halo(gr[4], gr[5], gr[6], gr[7]);
 #pragma unroll
             for (int k = 0; k < 6; ++k) {
                 D[s2][k] = gr[k + 2] - gr[k];
@@ -106,7 +108,8 @@ struct HarrisCore {
             for (int k = 0; k < 4; ++k) G3[s2][k] = gown[k];
 #pragma unroll
             for (int k = 0; k < 4; ++k) G3[s2][4 + k] = __shfl_down_sync(0xffffffffu, G3[s2][k], 1);
-            if (lane == 31) halo(G3[s2][4], G3[s2][5], G3[s2][6], G3[s2][7]);
+            if constexpr (!std::is_same_v<std::decay_t<HaloFn>, NoHalo>)
+                if (lane == 31) halo(G3[s2][4], G3[s2][5], G3[s2][6], G3[s2][7]);
 #pragma unroll
             for (int k = 0; k < 6; ++k) {
                 const float ix = conv9_exact(WX, G3[s0][k], G3[s0][k + 1], G3[s0][k + 2], G3[s1][k], G3[s1][k + 1],
@@ -142,13 +145,16 @@ __device__ __forceinline__ float gray_of(float r, float g, float b) {
 }
 
 // ------------------------------------------------------------ planar RGB f32
-template <bool EXACT, int CH>
+template <bool EXACT, int CH, int SC = 128>
 struct HarrisF32Op {
     static_assert(CH % 3 == 0, "row rotation needs CH % 3 == 0");
+    using L = Strip<SC>;
     static constexpr int kGroups = 1;
+    static constexpr int kStripCols = SC;
     static constexpr int kRowsPerStage = CH;
     static constexpr int kHaloRows = 4;
-    static constexpr uint32_t kTxBytes = 3u * CH * kBoxCols * 4u;
+    static constexpr int kBox = L::kBoxCols;
+    static constexpr uint32_t kTxBytes = 3u * CH * kBox * 4u;
     static constexpr uint32_t kStageBytes = (kTxBytes + 127u) / 128u * 128u;
     struct Params {
         float kappa;
@@ -166,19 +172,23 @@ struct HarrisF32Op {
     template <int R>
     __device__ __forceinline__ void row(const unsigned char* stage, int lane, float (&out)[1][4]) {
         const float* sm = reinterpret_cast<const float*>(stage);
-        const float* pr = sm + (0 * CH + R) * kBoxCols;
-        const float* pg = sm + (1 * CH + R) * kBoxCols;
-        const float* pb = sm + (2 * CH + R) * kBoxCols;
+        const float* pr = sm + (0 * CH + R) * kBox;
+        const float* pg = sm + (1 * CH + R) * kBox;
+        const float* pb = sm + (2 * CH + R) * kBox;
         const float4 r = lds128(pr + lane * 4), g = lds128(pg + lane * 4), b = lds128(pb + lane * 4);
         const float gown[4] = {gray_of<EXACT>(r.x, g.x, b.x), gray_of<EXACT>(r.y, g.y, b.y),
                                gray_of<EXACT>(r.z, g.z, b.z), gray_of<EXACT>(r.w, g.w, b.w)};
-        core.template step<R>(gown, lane, [&](float& h0, float& h1, float& h2, float& h3) {
-            const float4 r2 = lds128(pr + kWarpCols), g2 = lds128(pg + kWarpCols), b2 = lds128(pb + kWarpCols);
-            h0 = gray_of<EXACT>(r2.x, g2.x, b2.x);
-            h1 = gray_of<EXACT>(r2.y, g2.y, b2.y);
-            h2 = gray_of<EXACT>(r2.z, g2.z, b2.z);
-            h3 = gray_of<EXACT>(r2.w, g2.w, b2.w);
-        }, out[0]);
+        if constexpr (L::kLaneHalo) {
+            core.template step<R>(gown, lane, NoHalo{}, out[0]);
+        } else {
+            core.template step<R>(gown, lane, [&](float& h0, float& h1, float& h2, float& h3) {
+                const float4 r2 = lds128(pr + kWarpCols), g2 = lds128(pg + kWarpCols), b2 = lds128(pb + kWarpCols);
+                h0 = gray_of<EXACT>(r2.x, g2.x, b2.x);
+                h1 = gray_of<EXACT>(r2.y, g2.y, b2.y);
+                h2 = gray_of<EXACT>(r2.z, g2.z, b2.z);
+                h3 = gray_of<EXACT>(r2.w, g2.w, b2.w);
+            }, out[0]);
+        }
     }
 };
 
@@ -211,13 +221,16 @@ __device__ __forceinline__ void gray4_u8(uint32_t w0, uint32_t w1, uint32_t w2, 
     g3 = gray_u8<EXACT>(u8f(w2, 1), u8f(w2, 2), u8f(w2, 3));
 }
 
-template <bool EXACT, int CH>
+template <bool EXACT, int CH, int SC = 128>
 struct HarrisU8Op {
     static_assert(CH % 3 == 0, "row rotation needs CH % 3 == 0");
+    using L = Strip<SC>;
     static constexpr int kGroups = 1;
+    static constexpr int kStripCols = SC;
     static constexpr int kRowsPerStage = CH;
     static constexpr int kHaloRows = 4;
-    static constexpr uint32_t kTxBytes = uint32_t(CH) * kU8BoxWords * 4u;
+    static constexpr int kWords = L::kU8BoxWords;
+    static constexpr uint32_t kTxBytes = uint32_t(CH) * kWords * 4u;
     static constexpr uint32_t kStageBytes = (kTxBytes + 127u) / 128u * 128u;
     struct Params {
         float kappa;
@@ -230,17 +243,26 @@ struct HarrisU8Op {
     __device__ __forceinline__ static void load(void* smem, const CUtensorMap* tmap, uint64_t* bar,
                                                 const int (&col0)[1], int row0, const int (&image)[1],
                                                 uint64_t policy) {
-        tma_load_3d(smem, tmap, bar, (col0[0] / kWarpCols) * (kWarpCols * 3 / 4), row0, image[0], policy);
+        tma_load_3d(smem, tmap, bar, L::u8_box_word(col0[0] / SC), row0, image[0], policy);
+    }
+
+    int skip = 0;  // words before the strip's first pixel in the box (SC = 124 only)
+    __device__ __forceinline__ void begin_tile(const int (&col0)[1]) {
+        if constexpr (SC != 128) skip = L::u8_skip(col0[0] / SC);
     }
 
     template <int R>
     __device__ __forceinline__ void row(const unsigned char* stage, int lane, float (&out)[1][4]) {
-        const uint32_t* w = reinterpret_cast<const uint32_t*>(stage) + R * kU8BoxWords;
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(stage) + R * kWords + skip;
         float gown[4];
         gray4_u8<EXACT>(w[3 * lane], w[3 * lane + 1], w[3 * lane + 2], gown[0], gown[1], gown[2], gown[3]);
-        core.template step<R>(gown, lane, [&](float& h0, float& h1, float& h2, float& h3) {
-            gray4_u8<EXACT>(w[96], w[97], w[98], h0, h1, h2, h3);
-        }, out[0]);
+        if constexpr (L::kLaneHalo) {
+            core.template step<R>(gown, lane, NoHalo{}, out[0]);
+        } else {
+            core.template step<R>(gown, lane, [&](float& h0, float& h1, float& h2, float& h3) {
+                gray4_u8<EXACT>(w[96], w[97], w[98], h0, h1, h2, h3);
+            }, out[0]);
+        }
     }
 };
 

@@ -19,6 +19,7 @@
 #include <cuda.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "harris_common.cuh"
 #include "harris_ops.cuh"
@@ -134,7 +135,8 @@ struct HarrisCore2 {
         for (int k = 0; k < 4; ++k) g[k] = gown[k];
 #pragma unroll
         for (int k = 0; k < 4; ++k) g[4 + k] = shfl_down2(g[k]);
-        if (lane == 31) halo(g[4], g[5], g[6], g[7]);
+        if constexpr (!std::is_same_v<std::decay_t<HaloFn>, NoHalo>)
+            if (lane == 31) halo(g[4], g[5], g[6], g[7]);
         if constexpr (!EXACT) {
 #pragma unroll
             for (int k = 0; k < 6; ++k) {
@@ -204,13 +206,16 @@ __device__ __forceinline__ float2 gray2_of(float2 r, float2 g, float2 b) {
 
 // ------------------------------------------------------------ planar RGB f32
 // Two TMA boxes per stage ({132 cols, CH rows, 3 channels, 1 image} at x and x+128).
-template <bool EXACT, int CH>
+template <bool EXACT, int CH, int SC = 128>
 struct HarrisF32x2Op {
     static_assert(CH % 3 == 0, "row rotation needs CH % 3 == 0");
+    using L = Strip<SC>;
     static constexpr int kGroups = 2;
+    static constexpr int kStripCols = SC;
     static constexpr int kRowsPerStage = CH;
     static constexpr int kHaloRows = 4;
-    static constexpr uint32_t kBoxBytes = 3u * CH * kBoxCols * 4u;
+    static constexpr int kBox = L::kBoxCols;
+    static constexpr uint32_t kBoxBytes = 3u * CH * kBox * 4u;
     static constexpr uint32_t kBoxStride = (kBoxBytes + 127u) / 128u * 128u;
     static constexpr uint32_t kTxBytes = 2u * kBoxBytes;
     static constexpr uint32_t kStageBytes = 2u * kBoxStride;
@@ -233,7 +238,7 @@ struct HarrisF32x2Op {
     __device__ __forceinline__ void row(const unsigned char* stage, int lane, float (&out)[2][4]) {
         const float* a = reinterpret_cast<const float*>(stage);
         const float* b = reinterpret_cast<const float*>(stage + kBoxStride);
-        const int o_r = (0 * CH + R) * kBoxCols, o_g = (1 * CH + R) * kBoxCols, o_b = (2 * CH + R) * kBoxCols;
+        const int o_r = (0 * CH + R) * kBox, o_g = (1 * CH + R) * kBox, o_b = (2 * CH + R) * kBox;
         const float4 ra = lds128(a + o_r + lane * 4), ga = lds128(a + o_g + lane * 4), ba = lds128(a + o_b + lane * 4);
         const float4 rb = lds128(b + o_r + lane * 4), gb = lds128(b + o_g + lane * 4), bb = lds128(b + o_b + lane * 4);
         // gray in scalar form: the results can be allocated straight into the (A, B)
@@ -243,16 +248,20 @@ struct HarrisF32x2Op {
             make_float2(gray_of<EXACT>(ra.y, ga.y, ba.y), gray_of<EXACT>(rb.y, gb.y, bb.y)),
             make_float2(gray_of<EXACT>(ra.z, ga.z, ba.z), gray_of<EXACT>(rb.z, gb.z, bb.z)),
             make_float2(gray_of<EXACT>(ra.w, ga.w, ba.w), gray_of<EXACT>(rb.w, gb.w, bb.w))};
-        core.template step<R>(gown, lane, [&](float2& h0, float2& h1, float2& h2, float2& h3) {
-            const float4 r2a = lds128(a + o_r + kWarpCols), g2a = lds128(a + o_g + kWarpCols),
-                         b2a = lds128(a + o_b + kWarpCols);
-            const float4 r2b = lds128(b + o_r + kWarpCols), g2b = lds128(b + o_g + kWarpCols),
-                         b2b = lds128(b + o_b + kWarpCols);
-            h0 = make_float2(gray_of<EXACT>(r2a.x, g2a.x, b2a.x), gray_of<EXACT>(r2b.x, g2b.x, b2b.x));
-            h1 = make_float2(gray_of<EXACT>(r2a.y, g2a.y, b2a.y), gray_of<EXACT>(r2b.y, g2b.y, b2b.y));
-            h2 = make_float2(gray_of<EXACT>(r2a.z, g2a.z, b2a.z), gray_of<EXACT>(r2b.z, g2b.z, b2b.z));
-            h3 = make_float2(gray_of<EXACT>(r2a.w, g2a.w, b2a.w), gray_of<EXACT>(r2b.w, g2b.w, b2b.w));
-        }, out);
+        if constexpr (L::kLaneHalo) {
+            core.template step<R>(gown, lane, NoHalo{}, out);
+        } else {
+            core.template step<R>(gown, lane, [&](float2& h0, float2& h1, float2& h2, float2& h3) {
+                const float4 r2a = lds128(a + o_r + kWarpCols), g2a = lds128(a + o_g + kWarpCols),
+                             b2a = lds128(a + o_b + kWarpCols);
+                const float4 r2b = lds128(b + o_r + kWarpCols), g2b = lds128(b + o_g + kWarpCols),
+                             b2b = lds128(b + o_b + kWarpCols);
+                h0 = make_float2(gray_of<EXACT>(r2a.x, g2a.x, b2a.x), gray_of<EXACT>(r2b.x, g2b.x, b2b.x));
+                h1 = make_float2(gray_of<EXACT>(r2a.y, g2a.y, b2a.y), gray_of<EXACT>(r2b.y, g2b.y, b2b.y));
+                h2 = make_float2(gray_of<EXACT>(r2a.z, g2a.z, b2a.z), gray_of<EXACT>(r2b.z, g2b.z, b2b.z));
+                h3 = make_float2(gray_of<EXACT>(r2a.w, g2a.w, b2a.w), gray_of<EXACT>(r2b.w, g2b.w, b2b.w));
+            }, out);
+        }
     }
 };
 
@@ -288,13 +297,16 @@ __device__ __forceinline__ void gray4_u8x2(const uint32_t (&a)[3], const uint32_
     g3 = gray2_u8<EXACT>(u8f2(a[2], b[2], 1), u8f2(a[2], b[2], 2), u8f2(a[2], b[2], 3));
 }
 
-template <bool EXACT, int CH>
+template <bool EXACT, int CH, int SC = 128>
 struct HarrisU8x2Op {
     static_assert(CH % 3 == 0, "row rotation needs CH % 3 == 0");
+    using L = Strip<SC>;
     static constexpr int kGroups = 2;
+    static constexpr int kStripCols = SC;
     static constexpr int kRowsPerStage = CH;
     static constexpr int kHaloRows = 4;
-    static constexpr uint32_t kBoxBytes = uint32_t(CH) * kU8BoxWords * 4u;
+    static constexpr int kWords = L::kU8BoxWords;
+    static constexpr uint32_t kBoxBytes = uint32_t(CH) * kWords * 4u;
     static constexpr uint32_t kBoxStride = (kBoxBytes + 127u) / 128u * 128u;
     static constexpr uint32_t kTxBytes = 2u * kBoxBytes;
     static constexpr uint32_t kStageBytes = 2u * kBoxStride;
@@ -309,24 +321,36 @@ struct HarrisU8x2Op {
     __device__ __forceinline__ static void load(void* smem, const CUtensorMap* tmap, uint64_t* bar,
                                                 const int (&col0)[2], int row0, const int (&image)[2],
                                                 uint64_t policy) {
-        tma_load_3d(smem, tmap, bar, (col0[0] / kWarpCols) * (kWarpCols * 3 / 4), row0, image[0], policy);
-        tma_load_3d(static_cast<unsigned char*>(smem) + kBoxStride, tmap, bar,
-                    (col0[1] / kWarpCols) * (kWarpCols * 3 / 4), row0, image[1], policy);
+        tma_load_3d(smem, tmap, bar, L::u8_box_word(col0[0] / SC), row0, image[0], policy);
+        tma_load_3d(static_cast<unsigned char*>(smem) + kBoxStride, tmap, bar, L::u8_box_word(col0[1] / SC), row0,
+                    image[1], policy);
+    }
+
+    int skip_a = 0, skip_b = 0;  // words before each strip's first pixel (SC = 124 only)
+    __device__ __forceinline__ void begin_tile(const int (&col0)[2]) {
+        if constexpr (SC != 128) {
+            skip_a = L::u8_skip(col0[0] / SC);
+            skip_b = L::u8_skip(col0[1] / SC);
+        }
     }
 
     template <int R>
     __device__ __forceinline__ void row(const unsigned char* stage, int lane, float (&out)[2][4]) {
-        const uint32_t* wa = reinterpret_cast<const uint32_t*>(stage) + R * kU8BoxWords;
-        const uint32_t* wb = reinterpret_cast<const uint32_t*>(stage + kBoxStride) + R * kU8BoxWords;
+        const uint32_t* wa = reinterpret_cast<const uint32_t*>(stage) + R * kWords + skip_a;
+        const uint32_t* wb = reinterpret_cast<const uint32_t*>(stage + kBoxStride) + R * kWords + skip_b;
         const uint32_t a[3] = {wa[3 * lane], wa[3 * lane + 1], wa[3 * lane + 2]};
         const uint32_t b[3] = {wb[3 * lane], wb[3 * lane + 1], wb[3 * lane + 2]};
         float2 gown[4];
         gray4_u8x2<EXACT>(a, b, gown[0], gown[1], gown[2], gown[3]);
-        core.template step<R>(gown, lane, [&](float2& h0, float2& h1, float2& h2, float2& h3) {
-            const uint32_t ha[3] = {wa[96], wa[97], wa[98]};
-            const uint32_t hb[3] = {wb[96], wb[97], wb[98]};
-            gray4_u8x2<EXACT>(ha, hb, h0, h1, h2, h3);
-        }, out);
+        if constexpr (L::kLaneHalo) {
+            core.template step<R>(gown, lane, NoHalo{}, out);
+        } else {
+            core.template step<R>(gown, lane, [&](float2& h0, float2& h1, float2& h2, float2& h3) {
+                const uint32_t ha[3] = {wa[96], wa[97], wa[98]};
+                const uint32_t hb[3] = {wb[96], wb[97], wb[98]};
+                gray4_u8x2<EXACT>(ha, hb, h0, h1, h2, h3);
+            }, out);
+        }
     }
 };
 

@@ -68,15 +68,25 @@ template <> struct F32Cfg<6> { static constexpr int NW = 8, NS = 2, CH = 3, MINB
 template <> struct F32Cfg<7> { static constexpr int NW = 4, NS = 4, CH = 3, MINB = 1, G = 2; };
 // scalar core, deep ring (small images: more of each short tile in flight)
 template <> struct F32Cfg<8> { static constexpr int NW = 8, NS = 4, CH = 3, MINB = 1, G = 1; };
+// 124-column lane-halo strips (harris_common.cuh Strip<124>): no lane-31 halo branch
+template <> struct F32Cfg<9> { static constexpr int NW = 8, NS = 2, CH = 3, MINB = 1, G = 2, SC = 124; };
+template <> struct F32Cfg<10> { static constexpr int NW = 8, NS = 3, CH = 3, MINB = 1, G = 1, SC = 124; };
+
+template <class C, class = void>
+struct StripColsOf : std::integral_constant<int, 128> {};
+template <class C>
+struct StripColsOf<C, std::void_t<decltype(C::SC)>> : std::integral_constant<int, C::SC> {};
 
 template <int CFG, bool EXACT>
-using F32OpOf = std::conditional_t<F32Cfg<CFG>::G == 2, HarrisF32x2Op<EXACT, F32Cfg<CFG>::CH>,
-                                   HarrisF32Op<EXACT, F32Cfg<CFG>::CH>>;
+using F32OpOf = std::conditional_t<F32Cfg<CFG>::G == 2,
+                                   HarrisF32x2Op<EXACT, F32Cfg<CFG>::CH, StripColsOf<F32Cfg<CFG>>::value>,
+                                   HarrisF32Op<EXACT, F32Cfg<CFG>::CH, StripColsOf<F32Cfg<CFG>>::value>>;
 
-#define HARRIS_CFG_ROW(k) {F32Cfg<k>::NW, F32Cfg<k>::NS, F32Cfg<k>::CH, F32Cfg<k>::G}
+#define HARRIS_CFG_ROW(k) {F32Cfg<k>::NW, F32Cfg<k>::NS, F32Cfg<k>::CH, F32Cfg<k>::G, StripColsOf<F32Cfg<k>>::value}
 const TmaConfig kTmaConfigs[kNumTmaConfigs] = {
-    HARRIS_CFG_ROW(0), HARRIS_CFG_ROW(1), HARRIS_CFG_ROW(2), HARRIS_CFG_ROW(3),
-    HARRIS_CFG_ROW(4), HARRIS_CFG_ROW(5), HARRIS_CFG_ROW(6), HARRIS_CFG_ROW(7), HARRIS_CFG_ROW(8),
+    HARRIS_CFG_ROW(0), HARRIS_CFG_ROW(1), HARRIS_CFG_ROW(2), HARRIS_CFG_ROW(3), HARRIS_CFG_ROW(4),
+    HARRIS_CFG_ROW(5), HARRIS_CFG_ROW(6), HARRIS_CFG_ROW(7), HARRIS_CFG_ROW(8), HARRIS_CFG_ROW(9),
+    HARRIS_CFG_ROW(10),
 };
 #undef HARRIS_CFG_ROW
 
@@ -133,6 +143,8 @@ static cudaError_t occupancy_one(int* n) {
         case 6: return EXPR_T(6);       \
         case 7: return EXPR_T(7);       \
         case 8: return EXPR_T(8);       \
+        case 9: return EXPR_T(9);       \
+        case 10: return EXPR_T(10);     \
         default: break;                 \
     }
 

@@ -20,11 +20,13 @@
 namespace harris {
 
 const TmaConfig kU8Configs[kNumU8Configs] = {
-    {8, 4, 6, 1},  // 0: scalar core, 2 CTAs (16 warps) per SM (registers capped at 128)
-    {8, 4, 6, 1},  // 1: scalar core, 1 CTA per SM
-    {8, 3, 3, 1},  // 2: scalar core
-    {8, 4, 6, 2},  // 3: packed FP32x2 dual-strip core
-    {8, 3, 3, 2},  // 4: packed FP32x2 dual-strip core
+    {8, 4, 6, 1},       // 0: scalar core, 2 CTAs (16 warps) per SM (registers capped at 128)
+    {8, 4, 6, 1},       // 1: scalar core, 1 CTA per SM
+    {8, 3, 3, 1},       // 2: scalar core
+    {8, 4, 6, 2},       // 3: packed FP32x2 dual-strip core
+    {8, 3, 3, 2},       // 4: packed FP32x2 dual-strip core
+    {8, 4, 6, 1, 124},  // 5: as 0, 124-column lane-halo strips (no lane-31 halo branch)
+    {8, 4, 6, 2, 124},  // 6: as 3, 124-column lane-halo strips
 };
 
 template <int CFG>
@@ -49,15 +51,29 @@ template <>
 struct U8Cfg<4> {
     static constexpr int NW = 8, NS = 3, CH = 3, MINB = 1, G = 2;
 };
+template <>
+struct U8Cfg<5> {
+    static constexpr int NW = 8, NS = 4, CH = 6, MINB = 2, SC = 124;
+};
+template <>
+struct U8Cfg<6> {
+    static constexpr int NW = 8, NS = 4, CH = 6, MINB = 1, G = 2, SC = 124;
+};
 
 template <class C, class = void>
 struct GroupsOf : std::integral_constant<int, 1> {};
 template <class C>
 struct GroupsOf<C, std::void_t<decltype(C::G)>> : std::integral_constant<int, C::G> {};
 
+template <class C, class = void>
+struct U8StripColsOf : std::integral_constant<int, 128> {};
+template <class C>
+struct U8StripColsOf<C, std::void_t<decltype(C::SC)>> : std::integral_constant<int, C::SC> {};
+
 template <int CFG, bool EXACT>
-using U8OpOf = std::conditional_t<GroupsOf<U8Cfg<CFG>>::value == 2, HarrisU8x2Op<EXACT, U8Cfg<CFG>::CH>,
-                                  HarrisU8Op<EXACT, U8Cfg<CFG>::CH>>;
+using U8OpOf = std::conditional_t<GroupsOf<U8Cfg<CFG>>::value == 2,
+                                  HarrisU8x2Op<EXACT, U8Cfg<CFG>::CH, U8StripColsOf<U8Cfg<CFG>>::value>,
+                                  HarrisU8Op<EXACT, U8Cfg<CFG>::CH, U8StripColsOf<U8Cfg<CFG>>::value>>;
 
 template <int CFG, bool EXACT>
 static constexpr auto u8_kernel() {
@@ -108,6 +124,8 @@ size_t u8_smem_bytes(int cfg) {
         case 2: return u8_smem<2>();
         case 3: return u8_smem<3>();
         case 4: return u8_smem<4>();
+        case 5: return u8_smem<5>();
+        case 6: return u8_smem<6>();
         default: return 0;
     }
 }
@@ -119,6 +137,8 @@ cudaError_t u8_configure(int cfg) {
         case 2: return u8_configure_one<2>();
         case 3: return u8_configure_one<3>();
         case 4: return u8_configure_one<4>();
+        case 5: return u8_configure_one<5>();
+        case 6: return u8_configure_one<6>();
         default: return cudaErrorInvalidValue;
     }
 }
@@ -130,6 +150,8 @@ cudaError_t u8_occupancy(int cfg, int* ctas_per_sm) {
         case 2: return u8_occupancy_one<2>(ctas_per_sm);
         case 3: return u8_occupancy_one<3>(ctas_per_sm);
         case 4: return u8_occupancy_one<4>(ctas_per_sm);
+        case 5: return u8_occupancy_one<5>(ctas_per_sm);
+        case 6: return u8_occupancy_one<6>(ctas_per_sm);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -142,6 +164,8 @@ cudaError_t launch_tma_u8(int cfg, bool exact, const CUtensorMap& tmap, const Ti
         case 2: return u8_launch_one<2>(exact, tmap, tg, grid, stream);
         case 3: return u8_launch_one<3>(exact, tmap, tg, grid, stream);
         case 4: return u8_launch_one<4>(exact, tmap, tg, grid, stream);
+        case 5: return u8_launch_one<5>(exact, tmap, tg, grid, stream);
+        case 6: return u8_launch_one<6>(exact, tmap, tg, grid, stream);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -26,6 +26,7 @@ template <bool EXACT, int CH>
 struct Sep3x3Op {
     static_assert(CH % 3 == 0, "row rotation needs CH % 3 == 0");
     static constexpr int kGroups = 1;
+    static constexpr int kStripCols = kWarpCols;
     static constexpr int kRowsPerStage = CH;
     static constexpr int kHaloRows = 2;
     static constexpr uint32_t kTxBytes = uint32_t(CH) * kBoxCols * 4u;

@@ -18,8 +18,9 @@
 // full (input row i >= Op::kHaloRows).
 //
 // Op concept:
-//   kGroups (1 or 2: 128-column strips per tile; with 2 a lane owns the same 4
-//            columns of two adjacent strips, so the op can run packed f32x2 math),
+//   kGroups (1 or 2: strips per tile; with 2 a lane owns the same 4 columns of two
+//            adjacent strips, so the op can run packed f32x2 math),
+//   kStripCols (output columns per strip: 128, or 124 when lane 31 is the halo lane),
 //   kRowsPerStage, kHaloRows, kStageBytes (multiple of 128), kTxBytes
 //   struct Params;  explicit Op(const Params&)
 //   static void load(void* smem, const CUtensorMap*, uint64_t* bar, const int (&strip_col0)[kGroups],
@@ -29,6 +30,7 @@
 #include <cuda.h>
 
 #include <cstdint>
+#include <type_traits>
 #include <utility>
 
 #include "harris_common.cuh"
@@ -85,6 +87,12 @@ template <class F, int... Rs>
 __device__ __forceinline__ void static_for(F&& f, std::integer_sequence<int, Rs...>) {
     (f(std::integral_constant<int, Rs>{}), ...);
 }
+
+// Op::begin_tile(strip_col0) is optional: per-tile state of the op (e.g. the u8 box skew)
+template <class Op, class = void>
+struct HasBeginTile : std::false_type {};
+template <class Op>
+struct HasBeginTile<Op, std::void_t<decltype(&Op::begin_tile)>> : std::true_type {};
 
 template <int NW, int NS, class Op>
 struct StripShape {
@@ -158,7 +166,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                 int cols[G], imgs[G];
 #pragma unroll
                 for (int k = 0; k < G; ++k) {
-                    cols[k] = c.cs[k] * kWarpCols;
+                    cols[k] = c.cs[k] * Op::kStripCols;
                     imgs[k] = c.b[k];
                 }
                 mbar_arrive_expect_tx(&bars[s], Op::kTxBytes);
@@ -190,13 +198,21 @@ __global__ void __launch_bounds__(NW * 32, MINB)
         const TileCoord<G> tc = decode_tile<G>(t, g);
         const int rows_out = band_rows_out(tc.band, g);
         const int nch = (rows_out + HALO + CH - 1) / CH;
+        if constexpr (HasBeginTile<Op>::value) {
+            int c0[G];
+#pragma unroll
+            for (int k = 0; k < G; ++k) c0[k] = tc.cs[k] * Op::kStripCols;
+            op.begin_tile(c0);
+        }
         int colg[G];
         float* orow[G];
 #pragma unroll
         for (int k = 0; k < G; ++k) {
-            colg[k] = tc.valid[k] ? tc.cs[k] * kWarpCols + lane * kColsPerLane : g.m;  // invalid: never stored
+            // invalid strip, or the halo lane of a 124-column strip: never stored
+            const bool own = tc.valid[k] && lane * kColsPerLane < Op::kStripCols;
+            colg[k] = own ? tc.cs[k] * Op::kStripCols + lane * kColsPerLane : g.m;
             orow[k] = g.out + int64_t(tc.b[k]) * g.out_image_stride +
-                      int64_t(tc.band) * g.band_rows * g.out_pitch + (tc.valid[k] ? colg[k] : 0);
+                      int64_t(tc.band) * g.band_rows * g.out_pitch + (colg[k] < g.m ? colg[k] : 0);
         }
 
         for (int c = 0; c < nch; ++c) {

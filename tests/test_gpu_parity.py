@@ -384,7 +384,7 @@ def _ctx_with(env: dict):
                 os.environ[k] = v
 
 
-@pytest.mark.parametrize("cfg", range(9))
+@pytest.mark.parametrize("cfg", range(11))
 def test_every_f32_tma_config_bitexact(cuda_ctx, cfg):
     """Every TMA kernel configuration (scalar and packed dual-strip cores), including a
     batch whose strip pairs straddle images and a single image with ragged strips."""
@@ -404,7 +404,7 @@ def test_every_f32_tma_config_bitexact(cuda_ctx, cfg):
     ctx.close()
 
 
-@pytest.mark.parametrize("cfg", range(5))
+@pytest.mark.parametrize("cfg", range(7))
 def test_every_u8_tma_config_bitexact(cuda_ctx, cfg):
     ctx = _ctx_with({"HARRIS_U8_CONFIG": cfg})
     for B, H, W in [(1, 9, 128), (3, 40, 400), (1, 133, 528)]:
