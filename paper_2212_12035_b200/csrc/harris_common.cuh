@@ -133,6 +133,13 @@ __device__ __forceinline__ float4 lds128(const float* p) {
 }
 
 // streaming 16-byte store (output is written once, never re-read by the kernel)
+// predicated form: one SETP + one predicated STG, no branch / reconvergence point
+__device__ __forceinline__ void stg128_cs_if(bool pred, float* p, float a, float b, float c, float d) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %5, 0;\n@p st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};\n}" ::"l"(p),
+        "f"(a), "f"(b), "f"(c), "f"(d), "r"(int(pred))
+        : "memory");
+}
 __device__ __forceinline__ void stg128_cs(float* p, float a, float b, float c, float d) {
     asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
                  : "memory");

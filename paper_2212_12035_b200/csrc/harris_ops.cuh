@@ -71,7 +71,44 @@ struct HarrisCore {
     template <int R, class HaloFn>
     __device__ __forceinline__ void step(const float (&gown)[4], int lane, HaloFn&& halo, float (&out)[4]) {
         constexpr int s2 = R % 3, s0 = (R + 1) % 3, s1 = (R + 2) % 3;
-        if constexpr (!EXACT) {
+        constexpr bool kLaneHalo = std::is_same_v<std::decay_t<HaloFn>, NoHalo>;
+        if constexpr (!EXACT && kLaneHalo) {
+            // lane-halo layout: every lane (lane 31 included) has a right neighbour holding
+            // the next columns, so Sobel is evaluated on this lane's 4 columns only and the
+            // 2 extra columns the box sums need come from lane+1 — the same operands in the
+            // same order as computing them here, i.e. bit-identical, 12 FP ops fewer per row
+            float gr[6];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) gr[k] = gown[k];
+            gr[4] = __shfl_down_sync(0xffffffffu, gr[0], 1);
+            gr[5] = __shfl_down_sync(0xffffffffu, gr[1], 1);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                D[s2][k] = gr[k + 2] - gr[k];
+                Hs[s2][k] = fmaf(2.f, gr[k + 1], gr[k]) + gr[k + 2];
+            }
+            float ix[6], iy[6];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                ix[k] = fmaf(2.f, D[s1][k], D[s0][k] + D[s2][k]);
+                iy[k] = Hs[s2][k] - Hs[s0][k];
+            }
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                ix[4 + k] = __shfl_down_sync(0xffffffffu, ix[k], 1);
+                iy[4 + k] = __shfl_down_sync(0xffffffffu, iy[k], 1);
+            }
+            prodsum4(ix, ix, HB[s2][0], HB[s2][1], HB[s2][2], HB[s2][3]);
+            prodsum4(ix, iy, HB[s2][4], HB[s2][5], HB[s2][6], HB[s2][7]);
+            prodsum4(iy, iy, HB[s2][8], HB[s2][9], HB[s2][10], HB[s2][11]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float sxx = (HB[s0][0 + j] + HB[s1][0 + j]) + HB[s2][0 + j];
+                const float sxy = (HB[s0][4 + j] + HB[s1][4 + j]) + HB[s2][4 + j];
+                const float syy = (HB[s0][8 + j] + HB[s1][8 + j]) + HB[s2][8 + j];
+                out[j] = coarsity_fast(sxx, sxy, syy, kappa);
+            }
+        } else if constexpr (!EXACT) {
             float gr[8];
 #pragma unroll
             for (int k = 0; k < 4; ++k) gr[k] = gown[k];

@@ -214,6 +214,16 @@ __global__ void __launch_bounds__(NW * 32, MINB)
             orow[k] = g.out + int64_t(tc.b[k]) * g.out_image_stride +
                       int64_t(tc.band) * g.band_rows * g.out_pitch + (colg[k] < g.m ? colg[k] : 0);
         }
+        // store mode per lane and group, fixed for the tile: a predicated 16-byte store, plus a
+        // scalar path behind a warp-uniform branch for tiles with a ragged / unaligned lane
+        bool vec[G];
+        bool ragged = false;
+#pragma unroll
+        for (int k = 0; k < G; ++k) {
+            vec[k] = g.vec_store && colg[k] + kColsPerLane <= g.m;
+            ragged |= !vec[k] && colg[k] < g.m;
+        }
+        ragged = __any_sync(0xffffffffu, ragged);
 
         for (int c = 0; c < nch; ++c) {
             mbar_wait(&bars[stage], phase);
@@ -227,15 +237,15 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                     if (i >= HALO && i - HALO < rows_out) {
 #pragma unroll
                         for (int gi = 0; gi < G; ++gi) {
-                            const int cg = colg[gi];
-                            if (cg >= g.m) continue;
                             float* po = orow[gi] + int64_t(i - HALO) * g.out_pitch;
-                            if (g.vec_store && cg + kColsPerLane <= g.m) {
-                                stg128_cs(po, out4[gi][0], out4[gi][1], out4[gi][2], out4[gi][3]);
-                            } else {  // unaligned output rows, or the ragged right edge
+                            stg128_cs_if(vec[gi], po, out4[gi][0], out4[gi][1], out4[gi][2], out4[gi][3]);
+                            if (ragged) {  // unaligned output rows, or the ragged right edge
+                                const int cg = colg[gi];
+                                if (!vec[gi] && cg < g.m) {
 #pragma unroll
-                                for (int k = 0; k < kColsPerLane; ++k)
-                                    if (cg + k < g.m) po[k] = out4[gi][k];
+                                    for (int k = 0; k < kColsPerLane; ++k)
+                                        if (cg + k < g.m) po[k] = out4[gi][k];
+                                }
                             }
                         }
                     }
