@@ -65,10 +65,17 @@ struct HarrisCore {
 #pragma unroll
             for (int k2 = 0; k2 < 18; ++k2) P[a][k2] = 0.f;
         }
+#pragma unroll
+        for (int q = 0; q < 12; ++q) PV[q] = 0.f;
     }
 
+    // lane-halo FAST core with an even stage height: vertical box sums share a row pair —
+    // odd row r: PV = H[r-1] + H[r], V = H[r-2] + PV; even row r: V = PV + H[r]
+    // (3 adds per 2 rows instead of 4; row parity = R parity because CH is even)
+    float PV[12];
+
     // gown: this lane's 4 gray values; halo(h0..h3) fills the right halo (lane 31 only)
-    template <int R, class HaloFn>
+    template <int R, class HaloFn, bool kPairRows = false>
     __device__ __forceinline__ void step(const float (&gown)[4], int lane, HaloFn&& halo, float (&out)[4]) {
         constexpr int s2 = R % 3, s0 = (R + 1) % 3, s1 = (R + 2) % 3;
         constexpr bool kLaneHalo = std::is_same_v<std::decay_t<HaloFn>, NoHalo>;
@@ -101,12 +108,28 @@ struct HarrisCore {
             prodsum4(ix, ix, HB[s2][0], HB[s2][1], HB[s2][2], HB[s2][3]);
             prodsum4(ix, iy, HB[s2][4], HB[s2][5], HB[s2][6], HB[s2][7]);
             prodsum4(iy, iy, HB[s2][8], HB[s2][9], HB[s2][10], HB[s2][11]);
+            if constexpr (kPairRows) {
+                float v[12];
+                if constexpr (R % 2 == 1) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const float sxx = (HB[s0][0 + j] + HB[s1][0 + j]) + HB[s2][0 + j];
-                const float sxy = (HB[s0][4 + j] + HB[s1][4 + j]) + HB[s2][4 + j];
-                const float syy = (HB[s0][8 + j] + HB[s1][8 + j]) + HB[s2][8 + j];
-                out[j] = coarsity_fast(sxx, sxy, syy, kappa);
+                    for (int q = 0; q < 12; ++q) {
+                        PV[q] = HB[s1][q] + HB[s2][q];
+                        v[q] = HB[s0][q] + PV[q];
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 12; ++q) v[q] = PV[q] + HB[s2][q];
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) out[j] = coarsity_fast(v[j], v[4 + j], v[8 + j], kappa);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float sxx = (HB[s0][0 + j] + HB[s1][0 + j]) + HB[s2][0 + j];
+                    const float sxy = (HB[s0][4 + j] + HB[s1][4 + j]) + HB[s2][4 + j];
+                    const float syy = (HB[s0][8 + j] + HB[s1][8 + j]) + HB[s2][8 + j];
+                    out[j] = coarsity_fast(sxx, sxy, syy, kappa);
+                }
             }
         } else if constexpr (!EXACT) {
             float gr[8];
@@ -216,7 +239,7 @@ struct HarrisF32Op {
         const float gown[4] = {gray_of<EXACT>(r.x, g.x, b.x), gray_of<EXACT>(r.y, g.y, b.y),
                                gray_of<EXACT>(r.z, g.z, b.z), gray_of<EXACT>(r.w, g.w, b.w)};
         if constexpr (L::kLaneHalo) {
-            core.template step<R>(gown, lane, NoHalo{}, out[0]);
+            core.template step<R, NoHalo, (CH % 2 == 0)>(gown, lane, NoHalo{}, out[0]);
         } else {
             core.template step<R>(gown, lane, [&](float& h0, float& h1, float& h2, float& h3) {
                 const float4 r2 = lds128(pr + kWarpCols), g2 = lds128(pg + kWarpCols), b2 = lds128(pb + kWarpCols);
@@ -249,13 +272,32 @@ __device__ __forceinline__ float gray_u8(float r, float g, float b) {
 }
 
 // 4 pixels = 12 bytes = 3 words: w0 = R0 G0 B0 R1, w1 = G1 B1 R2 G2, w2 = B2 R3 G3 B3
+// FAST: the red channel's 2^23 offset is cancelled inside the first FFMA —
+// fma(kR, 2^23 + b, -kR * 2^23) is exactly kR * b rounded once, i.e. the same value as
+// kR * float(b) — so only green and blue need the FADD of u8f
+__device__ __forceinline__ float u8raw(uint32_t w, int k) {
+    return __int_as_float(__byte_perm(w, 0x4B000000u, 0x7440u | uint32_t(k)));
+}
+__device__ __forceinline__ float gray_u8_fast_raw(float r_raw, float g, float b) {
+    constexpr float kR = 0.299f / (12.0f * 255.0f), kG = 0.587f / (12.0f * 255.0f),
+                    kB = 0.114f / (12.0f * 255.0f);
+    return fmaf(kB, b, fmaf(kG, g, fmaf(kR, r_raw, -kR * 8388608.0f)));
+}
+
 template <bool EXACT>
 __device__ __forceinline__ void gray4_u8(uint32_t w0, uint32_t w1, uint32_t w2, float& g0, float& g1, float& g2,
                                          float& g3) {
-    g0 = gray_u8<EXACT>(u8f(w0, 0), u8f(w0, 1), u8f(w0, 2));
-    g1 = gray_u8<EXACT>(u8f(w0, 3), u8f(w1, 0), u8f(w1, 1));
-    g2 = gray_u8<EXACT>(u8f(w1, 2), u8f(w1, 3), u8f(w2, 0));
-    g3 = gray_u8<EXACT>(u8f(w2, 1), u8f(w2, 2), u8f(w2, 3));
+    if constexpr (EXACT) {
+        g0 = gray_u8<EXACT>(u8f(w0, 0), u8f(w0, 1), u8f(w0, 2));
+        g1 = gray_u8<EXACT>(u8f(w0, 3), u8f(w1, 0), u8f(w1, 1));
+        g2 = gray_u8<EXACT>(u8f(w1, 2), u8f(w1, 3), u8f(w2, 0));
+        g3 = gray_u8<EXACT>(u8f(w2, 1), u8f(w2, 2), u8f(w2, 3));
+    } else {
+        g0 = gray_u8_fast_raw(u8raw(w0, 0), u8f(w0, 1), u8f(w0, 2));
+        g1 = gray_u8_fast_raw(u8raw(w0, 3), u8f(w1, 0), u8f(w1, 1));
+        g2 = gray_u8_fast_raw(u8raw(w1, 2), u8f(w1, 3), u8f(w2, 0));
+        g3 = gray_u8_fast_raw(u8raw(w2, 1), u8f(w2, 2), u8f(w2, 3));
+    }
 }
 
 template <bool EXACT, int CH, int SC = 128>
@@ -294,7 +336,7 @@ struct HarrisU8Op {
         float gown[4];
         gray4_u8<EXACT>(w[3 * lane], w[3 * lane + 1], w[3 * lane + 2], gown[0], gown[1], gown[2], gown[3]);
         if constexpr (L::kLaneHalo) {
-            core.template step<R>(gown, lane, NoHalo{}, out[0]);
+            core.template step<R, NoHalo, (CH % 2 == 0)>(gown, lane, NoHalo{}, out[0]);
         } else {
             core.template step<R>(gown, lane, [&](float& h0, float& h1, float& h2, float& h3) {
                 gray4_u8<EXACT>(w[96], w[97], w[98], h0, h1, h2, h3);
