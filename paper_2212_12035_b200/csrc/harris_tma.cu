@@ -102,8 +102,11 @@ static constexpr size_t f32_smem() {
     return StripShape<C::NW, C::NS, F32OpOf<CFG, false>>::kSmemBytes;
 }
 
+constexpr size_t kMaxDynSmem = 227 * 1024;  // sm_100 opt-in maximum per block
+
 template <int CFG>
 static cudaError_t configure_one() {
+    static_assert(f32_smem<CFG>() <= kMaxDynSmem, "TMA config exceeds 227 KB of shared memory");
     cudaError_t e = cudaFuncSetAttribute(f32_kernel<CFG, false>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(f32_smem<CFG>()));
     if (e != cudaSuccess) return e;

@@ -89,6 +89,7 @@ static constexpr size_t u8_smem() {
 
 template <int CFG>
 static cudaError_t u8_configure_one() {
+    static_assert(u8_smem<CFG>() <= 227 * 1024, "u8 config exceeds 227 KB of shared memory");
     cudaError_t e = cudaFuncSetAttribute(u8_kernel<CFG, false>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(u8_smem<CFG>()));
     if (e != cudaSuccess) return e;
