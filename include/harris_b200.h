@@ -22,8 +22,10 @@
  *   - Return 0 on success, a negative HARRIS_ERR_* code otherwise; nothing throws
  *     across this boundary.  harris_strerror() names the code.
  *   - A ctx is immutable after harris_init except for the host-staging buffers of
- *     harris_run_host, so harris_run* may be called concurrently on different
- *     streams; harris_run_host must not be called concurrently on one ctx.
+ *     harris_run_host and an internally locked launch cache (tensor maps + tile plans
+ *     of the last 8 call geometries, so repeated calls skip descriptor encoding and
+ *     planning), so harris_run* may be called concurrently on different streams;
+ *     harris_run_host must not be called concurrently on one ctx.
  *   - Element type is f32 throughout; kappa is the coarsity constant (0.04 in the
  *     thesis).
  */

@@ -109,12 +109,28 @@ _contexts: dict[int, HarrisContext] = {}
 def context(device: Optional[int] = None) -> HarrisContext:
     """The process-wide context of a CUDA device (created on first use)."""
     dev = torch.cuda.current_device() if device is None else int(device)
+    c = _contexts.get(dev)
+    if c is not None:
+        return c
     with _ctx_lock:
         c = _contexts.get(dev)
         if c is None:
             c = HarrisContext(dev)
             _contexts[dev] = c
         return c
+
+
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
+def _stream_handle(dev: int, stream: Optional[torch.cuda.Stream]) -> int:
+    """cudaStream_t of `stream` or of the device's current stream (the raw query avoids
+    building a Stream object per call: this is on the per-launch host path)."""
+    if stream is not None:
+        return stream.cuda_stream
+    if _raw_stream is not None:
+        return _raw_stream(dev)
+    return torch.cuda.current_stream(dev).cuda_stream
 
 
 def _flags(exact: bool, force_generic: bool, force_tma: bool) -> int:
@@ -183,9 +199,8 @@ def harris(rgb, kappa: float = KAPPA, *, out: Optional[torch.Tensor] = None, exa
         out_pitch = s_out[0]
         out_image = n * out_pitch
     dev = rgb.device.index if rgb.device.index is not None else torch.cuda.current_device()
-    st = stream if stream is not None else torch.cuda.current_stream(dev)
     (ctx or context(dev)).run_strided(out.data_ptr(), out_pitch, out_image, n, m, rgb.data_ptr(), in_pitch,
-                                      in_chan, in_image, B, kappa, flags, st.cuda_stream)
+                                      in_chan, in_image, B, kappa, flags, _stream_handle(dev, stream))
     return out
 
 

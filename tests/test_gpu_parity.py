@@ -444,3 +444,32 @@ def test_cuda_graph_capture_replay(cuda_ctx):
     g.replay()
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy(), cref.harris_f32(b))
+
+
+def test_launch_cache_keys(cuda_ctx):
+    """Repeated calls hit the ctx's launch cache: the key must cover geometry, pointers,
+    kappa and flags, and eviction (more than 8 geometries) must stay correct."""
+    rgb = synth.synth_numpy(3, 70, 264, seed=5)
+    x = _dev(rgb)
+    out = torch.empty((66, 260), device="cuda")
+    ref32 = cref.harris_f32(rgb)
+    for _ in range(3):
+        hb.harris(x, out=out, exact=True)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), ref32)
+        hb.harris(x, out=out, exact=True, kappa=0.05)  # same pointers, other kappa
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), cref.harris_f32(rgb, kappa=0.05))
+        hb.harris(x, out=out)                          # same pointers, FAST flags
+        torch.cuda.synchronize()
+        ok, m = synth.within_tolerance(out.cpu().numpy(), cref.harris_f64(rgb))
+        assert ok, m
+    # more distinct geometries than cache slots, then back to the first
+    for k in range(12):
+        sub = x[:, : 20 + k, : 136 + 4 * k]
+        got = hb.harris(sub, exact=True)
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy(), cref.harris_f32(np.ascontiguousarray(rgb[:, : 20 + k, : 136 + 4 * k])))
+    hb.harris(x, out=out, exact=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), ref32)
