@@ -42,7 +42,9 @@ def _check_exact(got: torch.Tensor, rgb_host: np.ndarray, what: str):
         raise AssertionError(f"{what}: {len(bad)} pixels differ, first at {bad[0].tolist()}")
 
 
-@pytest.mark.parametrize("H,W", [(1536, 2560), (2560, 1536), (8192, 8192)])
+# thesis evaluation sizes (1536x2560 and 4256x2832, both
+# orientations) and the bandwidth-roofline config
+@pytest.mark.parametrize("H,W", [(1536, 2560), (2560, 1536), (4256, 2832), (2832, 4256), (8192, 8192)])
 def test_fullsize_single_image(cuda_ctx, H, W):
     x = _image(H, W)
     ex = hb.harris(x, exact=True)

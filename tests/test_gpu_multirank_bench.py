@@ -1,0 +1,48 @@
+"""GPU: the bench's N>1 code path on a one-GPU box.
+
+Two torchrun ranks share cuda:0 (HARRIS_BENCH_SHARE_GPU=1, gloo for the host-side
+collectives — NCCL refuses two ranks on one device): the row-band workload with the fused
+peer gather and the image-sharded batch workload (weak scaling) must each print exactly
+one JSON line with n_gpus = 2.  The numbers themselves are meaningless here (two
+processes time-slice one GPU); this checks the plumbing the 8-GPU scaling run uses.
+"""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _torchrun(args, timeout=600):
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"), "--gpus", "2",
+           "--dist-backend", "gloo"] + args
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout,
+                       env=dict(os.environ, HARRIS_BENCH_SHARE_GPU="1"))
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    return lines[0]
+
+
+def test_two_rank_row_bands_with_fused_gather():
+    d = _torchrun(["--workload", "image8192", "--steps", "3", "--warmup", "3", "--no-e2e", "--gather", "peer"])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
+    assert d["config"]["gather"].startswith("fused")
+    assert d["gpu_launches"] == 3 * 3
+
+
+def test_two_rank_weak_scaling_batch():
+    d = _torchrun(["--steps", "3", "--warmup", "3", "--e2e-images", "8", "--e2e-steps", "1"])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak"
+    assert d["config"]["images"] == 2048 and d["config"]["images_per_gpu"] == 1024
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
