@@ -442,27 +442,45 @@ def run_e2e(a, sh: Shard, x_dev, dev, world, ctx) -> dict:
            "steps": steps, "images_per_rank_per_step": nb,
            "api": "HarrisContext.run_host -> harris_run_host (pipelined H2D/kernel/D2H, 3 streams)",
            "note": "bytes are per rank; host wall clock, max over ranks"}
-    # the e2e roofline: input bytes over PCIe at this box's raw pinned H2D bandwidth
+    # the e2e roofline: input bytes over PCIe at this box's raw pinned H2D bandwidth, alone
+    # and with the step's D2H running concurrently in the other direction (the two share
+    # the link's host side: 55.6 -> 51.8 GB/s H2D with 1/3 the bytes going back)
     raw = pinned_h2d_gbs(host_in, x_dev[:nb])
+    mixed = pinned_h2d_gbs(host_in, x_dev[:nb], host_out, d2h_ratio=sh.out_bytes() / sh.in_bytes())
     if raw:
         achieved = h2d_bytes * steps / dt / 1e9
         res["h2d_roofline"] = {"bound": "pcie_h2d", "achieved_gbs": achieved, "raw_pinned_h2d_gbs": raw,
-                               "frac": achieved / raw,
-                               "note": "raw = plain cudaMemcpyAsync of the same pinned input, same box"}
+                               "raw_h2d_gbs_with_concurrent_d2h": mixed,
+                               "frac": achieved / (mixed or raw),
+                               "note": "raw = plain cudaMemcpyAsync of the same pinned input on the same box; frac "
+                                       "is against the H2D rate with the step's D2H share running concurrently"}
     del host_in, host_out
     return res
 
 
-def pinned_h2d_gbs(host: torch.Tensor, dev_buf: torch.Tensor, reps: int = 3) -> float | None:
+def pinned_h2d_gbs(host: torch.Tensor, dev_buf: torch.Tensor, host_back: torch.Tensor | None = None,
+                   d2h_ratio: float = 0.0, reps: int = 3) -> float | None:
+    """H2D GB/s of plain pinned copies; with `host_back`, a D2H of d2h_ratio x the bytes runs
+    concurrently on a second stream."""
     try:
         n = min(host.numel(), dev_buf.numel(), 1 << 28)  # <= 1 GiB
         h, d = host.view(-1)[:n], dev_buf.reshape(-1)[:n]
+        nb = 0
+        if host_back is not None and d2h_ratio > 0:
+            nb = min(int(n * d2h_ratio), host_back.numel())
+            hb_, db_ = host_back.view(-1)[:nb], dev_buf.reshape(-1)[:nb]
+        s2 = torch.cuda.Stream()
         d.copy_(h, non_blocking=True)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(reps):
+            if nb:
+                s2.wait_event(e0)
+                with torch.cuda.stream(s2):
+                    hb_.copy_(db_, non_blocking=True)
             d.copy_(h, non_blocking=True)
+        torch.cuda.current_stream().wait_stream(s2)
         e1.record()
         torch.cuda.synchronize()
         return reps * n * 4 / (e0.elapsed_time(e1) * 1e-3) / 1e9
