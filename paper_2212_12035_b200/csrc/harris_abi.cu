@@ -136,6 +136,9 @@ int validate(const Call& c) {
 bool tma_eligible(const Call& c) {
     const Geom& g = c.g;
     if (!aligned16(g.rgb)) return false;
+    // the strip engine decodes tiles with 32-bit math: strips per band row < 2^31
+    // (tiles = bands x strips/groups stays below that too for any image the TMA box covers)
+    if (g.batch * ((g.m + 123) / 124) >= (int64_t(1) << 30)) return false;
     if (c.fmt == kU8Interleaved) {  // byte strides, tensor map over 32-bit words
         if ((g.in_pitch & 15) || (g.batch > 1 && (g.in_image_stride & 15))) return false;
         if (g.batch > INT32_MAX) return false;
@@ -329,6 +332,7 @@ int run(harris_ctx* ctx, const Call& c, cudaStream_t stream) {
             if (rc) return rc;
             plan_launch(ctx, cc, ent.tg, ent.grid);
             ent.cfg = cc.cfg;
+            if (ent.tg.tiles > INT32_MAX) return HARRIS_ERR_SIZE;  // beyond the engine's 32-bit tile index
             cache_insert(ctx, c, ent);
         }
         TileGeom tg = ent.tg;

@@ -210,6 +210,7 @@ template <bool EXACT, int CH, int SC = 128>
 struct HarrisF32x2Op {
     static_assert(CH % 3 == 0, "row rotation needs CH % 3 == 0");
     using L = Strip<SC>;
+    static constexpr bool kCacheProducer = false;  // measured: per-stage decode is faster here
     static constexpr int kGroups = 2;
     static constexpr int kStripCols = SC;
     static constexpr int kRowsPerStage = CH;
