@@ -35,6 +35,7 @@ struct harris_ctx {
     int sep_cfg = 0;
     int occ_sep[kNumSepConfigs] = {0};
     int occ_u8[kNumU8Configs] = {0};
+    int occ_ldg = 0;
     int sync_waves = 1;  // dev knob HARRIS_SYNC_WAVES=0 disables the per-tile CTA barrier
     int l2_policy = 1;  // evict_normal: the 4-column halo sectors are re-read by the neighbouring strip
     int64_t force_band_rows = 0;  // dev knob (HARRIS_BAND_ROWS): override the planner
@@ -107,6 +108,7 @@ struct Call {
     uint32_t* notify_flag = nullptr;  // harris_run_notify
     uint32_t notify_epoch = 0;
     int cfg = -1;  // f32 TMA configuration chosen for this call (resolve_cfg)
+    bool ldg = false;  // plan for the cp.async (LDG) kernel
 };
 
 int validate(const Call& c) {
@@ -195,16 +197,26 @@ void plan_tiles(int64_t n, int64_t m, int64_t batch, int64_t gw, int rows_per_st
     tg.tiles = units_per_band * best_bands;
 }
 
+// f32 inputs TMA cannot describe (pitch / strides / base not 16-byte aligned) keep the
+// strip engine with cp.async stage fills; only 4-byte alignment of the floats is needed
+bool ldg_eligible(const Call& c) {
+    const Geom& g = c.g;
+    if (c.fmt != kF32Planar || (reinterpret_cast<uintptr_t>(g.rgb) & 3)) return false;
+    if (g.batch * ((g.m + 123) / 124) >= (int64_t(1) << 30)) return false;
+    return g.n + 4 <= INT32_MAX && g.m + 4 <= INT32_MAX;
+}
+
 int choose_path(const Call& c) {
     if (c.flags & HARRIS_FLAG_FORCE_GENERIC) return HARRIS_PATH_GENERIC;
-    return tma_eligible(c) ? HARRIS_PATH_TMA : HARRIS_PATH_GENERIC;
+    if (tma_eligible(c)) return HARRIS_PATH_TMA;
+    return ldg_eligible(c) ? HARRIS_PATH_LDG : HARRIS_PATH_GENERIC;
 }
 
 void plan_launch(const harris_ctx* ctx, const Call& c, TileGeom& tg, int64_t& grid) {
     const bool u8 = c.fmt == kU8Interleaved;
     const int fcfg = c.cfg >= 0 ? c.cfg : ctx->tma_cfg;
-    const TmaConfig& cfg = u8 ? kU8Configs[ctx->u8_cfg] : kTmaConfigs[fcfg];
-    const int occ = std::max(1, u8 ? ctx->occ_u8[ctx->u8_cfg] : ctx->occ[fcfg]);
+    const TmaConfig& cfg = c.ldg ? kLdgConfig : u8 ? kU8Configs[ctx->u8_cfg] : kTmaConfigs[fcfg];
+    const int occ = std::max(1, c.ldg ? ctx->occ_ldg : u8 ? ctx->occ_u8[ctx->u8_cfg] : ctx->occ[fcfg]);
     const int64_t resident_ctas = int64_t(ctx->num_sms) * occ;
     plan_tiles(c.g.n, c.g.m, c.g.batch, resident_ctas * cfg.warps, cfg.rows, ctx->force_band_rows, tg, 4,
                cfg.groups, cfg.strip_cols);
@@ -323,13 +335,17 @@ int run(harris_ctx* ctx, const Call& c, cudaStream_t stream) {
     DeviceGuard guard(ctx->device);
     if (!guard.ok) return cuda_fail(ctx, cudaGetLastError(), "cudaSetDevice");
     cudaError_t e;
-    if (path == HARRIS_PATH_TMA) {
+    if (path == HARRIS_PATH_TMA || path == HARRIS_PATH_LDG) {
+        const bool ldg = path == HARRIS_PATH_LDG;
         harris_ctx::LaunchEntry ent;
         if (!cache_lookup(ctx, c, ent)) {
             Call cc = c;
-            cc.cfg = resolve_cfg(ctx, c);
-            rc = encode_tmap(ctx, cc, &ent.tmap);
-            if (rc) return rc;
+            cc.ldg = ldg;
+            if (!ldg) {
+                cc.cfg = resolve_cfg(ctx, c);
+                rc = encode_tmap(ctx, cc, &ent.tmap);
+                if (rc) return rc;
+            }
             plan_launch(ctx, cc, ent.tg, ent.grid);
             ent.cfg = cc.cfg;
             if (ent.tg.tiles > INT32_MAX) return HARRIS_ERR_SIZE;  // beyond the engine's 32-bit tile index
@@ -341,13 +357,16 @@ int run(harris_ctx* ctx, const Call& c, cudaStream_t stream) {
             tg.notify_flag = c.notify_flag;
             tg.notify_epoch = c.notify_epoch;
         }
-        e = c.fmt == kU8Interleaved ? launch_tma_u8(ctx->u8_cfg, exact, ent.tmap, tg, ent.grid, stream)
-                                    : launch_tma(ent.cfg, exact, ent.tmap, tg, ent.grid, stream);
+        e = ldg                         ? launch_ldg(exact, c.g, tg, ent.grid, stream)
+            : c.fmt == kU8Interleaved ? launch_tma_u8(ctx->u8_cfg, exact, ent.tmap, tg, ent.grid, stream)
+                                      : launch_tma(ent.cfg, exact, ent.tmap, tg, ent.grid, stream);
     } else {
         e = c.fmt == kU8Interleaved ? launch_generic_u8(exact, c.g, stream) : launch_generic(exact, c.g, stream);
         if (e == cudaSuccess && c.notify_flag) e = launch_peer_signal(c.notify_flag, c.notify_epoch, stream);
     }
-    if (e != cudaSuccess) return cuda_fail(ctx, e, path == HARRIS_PATH_TMA ? "launch tma" : "launch generic");
+    if (e != cudaSuccess)
+        return cuda_fail(ctx, e, path == HARRIS_PATH_TMA ? "launch tma" : path == HARRIS_PATH_LDG ? "launch ldg"
+                                                                                              : "launch generic");
     ctx->last_path = path;
     return HARRIS_OK;
 }
@@ -470,6 +489,12 @@ int harris_init(harris_ctx** out_ctx, int cuda_device) {
             delete ctx;
             return rc;
         }
+    }
+    e = ldg_configure(&ctx->occ_ldg);
+    if (e != cudaSuccess) {
+        int rc = cuda_fail(ctx, e, "configure ldg kernel");
+        delete ctx;
+        return rc;
     }
     for (int k = 0; k < kNumSepConfigs; ++k) {
         e = sep_configure(k, &ctx->occ_sep[k]);
@@ -629,8 +654,9 @@ int harris_plan(harris_ctx* ctx, int64_t n, int64_t m, int64_t batch, const floa
     if (rc) return rc;
     std::memset(info, 0, sizeof(*info));
     info->path = choose_path(c);
-    c.cfg = resolve_cfg(ctx, c);
-    const TmaConfig& cfg = kTmaConfigs[c.cfg];
+    c.ldg = info->path == HARRIS_PATH_LDG;
+    c.cfg = c.ldg ? -1 : resolve_cfg(ctx, c);
+    const TmaConfig& cfg = c.ldg ? kLdgConfig : kTmaConfigs[c.cfg];
     info->warps_per_cta = cfg.warps;
     info->stages = cfg.stages;
     info->rows_per_stage = cfg.rows;
@@ -642,9 +668,9 @@ int harris_plan(harris_ctx* ctx, int64_t n, int64_t m, int64_t batch, const floa
     info->col_segments = tg.colsegs;
     info->tiles = tg.tiles;
     info->grid_ctas = grid;
-    info->smem_bytes = int64_t(tma_smem_bytes(c.cfg));
+    info->smem_bytes = c.ldg ? 0 : int64_t(tma_smem_bytes(c.cfg));
     info->groups = cfg.groups;
-    info->tma_config = c.cfg;
+    info->tma_config = c.cfg;  // -1: the LDG kernel
     info->strip_cols = cfg.strip_cols;
     return HARRIS_OK;
 }

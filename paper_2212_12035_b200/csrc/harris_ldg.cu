@@ -1,0 +1,153 @@
+// harris_ldg.cu — the fused Harris strip engine for inputs TMA cannot describe.
+//
+// TMA needs 16-byte aligned row starts and strides; a planar image whose width is not a
+// multiple of 4 floats (1918, 8190, 4255 ...) or whose base is only 4-byte aligned has
+// neither.  Such inputs used to fall back to the generic shared-memory tile kernel K0
+// (118 k MP/s, 29 % of HBM).  This op keeps everything of the TMA path — the warp-strip
+// pipeline, the packed FP32x2 dual-strip core, the stage ring and its mbarriers — and
+// only replaces the stage fill: all 32 lanes copy the stage's 2 boxes x 3 channels x CH
+// rows x 132 columns with 4-byte cp.async (LDGSTS) into exactly the shared-memory layout
+// the TMA box has, and each lane's `cp.async.mbarrier.arrive.noinc` completes the stage
+// barrier once its copies have landed.  Rows beyond the image are skipped and columns
+// beyond the row end are zero-filled; neither reaches a stored output.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+
+#include "harris_common.cuh"
+#include "harris_internal.h"
+#include "harris_ops.cuh"
+#include "harris_ops2.cuh"
+#include "strip_pipeline.cuh"
+
+namespace harris {
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, uint32_t src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(smem)), "l"(gmem), "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, uint32_t src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(smem)), "l"(gmem), "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem), "r"(src_bytes)
+                 : "memory");
+}
+
+// one box row of kBoxCols floats, chunked by the row's own alignment (warp-uniform: the
+// strip starts at a multiple of 128 columns): 16-byte copies for 16-byte aligned rows,
+// 8-byte for 8-byte aligned ones, 4-byte otherwise; columns at or beyond `avail` are
+// zero-filled (src-size 0 reads nothing)
+template <int BYTES>
+__device__ __forceinline__ void copy_row(float* dst, const float* src, int avail, int lane) {
+    constexpr int E = BYTES / 4;                          // floats per chunk
+    constexpr int NCH = (kBoxCols + E - 1) / E;           // chunks per row
+#pragma unroll
+    for (int j = lane; j < NCH; j += 32) {
+        const int c0 = j * E;
+        const int valid = avail - c0;                     // floats of this chunk inside the row
+        const uint32_t nb = valid >= E ? uint32_t(BYTES) : valid > 0 ? uint32_t(valid) * 4u : 0u;
+        const float* sp = src + (nb ? c0 : 0);
+        if constexpr (BYTES == 16)
+            cp_async16(dst + c0, sp, nb);
+        else if constexpr (BYTES == 8)
+            cp_async8(dst + c0, sp, nb);
+        else
+            cp_async4(dst + c0, sp, nb);
+    }
+}
+
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// BYTES: copy granularity (4; wider copies measured slower: per-row 16/8/4 selection
+// -27 %, 8-byte on 8-byte aligned rows -7 %, profiles/ab_ldg_r01.txt)
+template <bool EXACT, int CH, int BYTES>
+struct HarrisF32x2LdgOp : HarrisF32x2Op<EXACT, CH, 128> {
+    using Base = HarrisF32x2Op<EXACT, CH, 128>;
+    static constexpr bool kWarpLoad = true;
+    static constexpr bool kCacheProducer = true;
+    struct Params {
+        float kappa;
+        const float* rgb;
+        int64_t in_pitch, in_chan_stride, in_image_stride;  // elements
+        int32_t W, H;                                       // input columns / rows per image
+    };
+
+    __device__ __forceinline__ explicit HarrisF32x2LdgOp(const Params& p) : Base(typename Base::Params{p.kappa}) {}
+
+    __device__ __forceinline__ static void load_warp(void* smem, const Params& p, uint64_t* bar,
+                                                     const int (&col0)[2], int row0, const int (&image)[2],
+                                                     int lane) {
+        unsigned char* s = static_cast<unsigned char*>(smem);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const float* img = p.rgb + int64_t(image[k]) * p.in_image_stride + col0[k];
+            const int avail = p.W - col0[k];  // columns of this row from col0 to the row end
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+#pragma unroll
+                for (int r = 0; r < CH; ++r) {
+                    const int y = row0 + r;
+                    if (y >= p.H) continue;  // below the image: never reaches a stored output
+                    const float* src = img + int64_t(ch) * p.in_chan_stride + int64_t(y) * p.in_pitch;
+                    float* dst = reinterpret_cast<float*>(s + k * Base::kBoxStride) + (ch * CH + r) * kBoxCols;
+                    copy_row<BYTES>(dst, src, avail, lane);
+                }
+            }
+        }
+        cp_async_mbar_arrive_noinc(bar);
+    }
+};
+
+constexpr int kLdgNW = 8, kLdgNS = 2, kLdgCH = 3;
+
+template <bool EXACT, int BYTES>
+static constexpr auto ldg_kernel() {
+    return strip_kernel<HarrisF32x2LdgOp<EXACT, kLdgCH, BYTES>, kLdgNW, kLdgNS, 1>;
+}
+static constexpr size_t ldg_smem() {
+    return StripShape<kLdgNW, kLdgNS, HarrisF32x2LdgOp<false, kLdgCH, 4>>::kSmemBytes;
+}
+static_assert(ldg_smem() <= 227 * 1024, "ldg config exceeds 227 KB of shared memory");
+
+const TmaConfig kLdgConfig = {kLdgNW, kLdgNS, kLdgCH, 2, 128};
+
+cudaError_t ldg_configure(int* ctas_per_sm) {
+    cudaError_t e = cudaFuncSetAttribute(ldg_kernel<false, 4>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(ldg_smem()));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(ldg_kernel<true, 4>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(ldg_smem()));
+
+    if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, ldg_kernel<false, 4>(), kLdgNW * 32,
+                                                          ldg_smem());
+    return e;
+}
+
+template <bool EXACT, int BYTES>
+static void launch_ldg_one(const Geom& geom, const TileGeom& tg, int64_t grid, cudaStream_t stream) {
+    CUtensorMap unused;
+    std::memset(&unused, 0, sizeof(unused));
+    const typename HarrisF32x2LdgOp<EXACT, kLdgCH, BYTES>::Params p{
+        geom.kappa, geom.rgb, geom.in_pitch, geom.in_chan_stride, geom.in_image_stride, int32_t(geom.m + 4),
+        int32_t(geom.n + 4)};
+    ldg_kernel<EXACT, BYTES>()<<<unsigned(grid), unsigned(kLdgNW * 32), ldg_smem(), stream>>>(unused, tg, p);
+}
+
+cudaError_t launch_ldg(bool exact, const Geom& geom, const TileGeom& tg, int64_t grid, cudaStream_t stream) {
+    // 4-byte copies for every alignment: 8-byte copies on 8-byte aligned rows measured
+    // 7 % slower (profiles/ab_ldg_r01.txt)
+    if (exact)
+        launch_ldg_one<true, 4>(geom, tg, grid, stream);
+    else
+        launch_ldg_one<false, 4>(geom, tg, grid, stream);
+    return cudaGetLastError();
+}
+
+}  // namespace harris

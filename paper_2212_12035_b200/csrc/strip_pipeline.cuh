@@ -91,6 +91,15 @@ __device__ __forceinline__ void static_for(F&& f, std::integer_sequence<int, Rs.
     (f(std::integral_constant<int, Rs>{}), ...);
 }
 
+// Op::kWarpLoad is optional (default false): the stage is filled by all 32 lanes with
+// Op::load_warp(smem, params, bar, cols, row0, imgs, lane) (cp.async, for inputs TMA
+// cannot describe) instead of one TMA issue by lane 0; the stage barrier then counts
+// 32 arrivals instead of an expect_tx byte count
+template <class Op, class = void>
+struct WarpLoadOf : std::false_type {};
+template <class Op>
+struct WarpLoadOf<Op, std::void_t<decltype(Op::kWarpLoad)>> : std::integral_constant<bool, Op::kWarpLoad> {};
+
 // Op::kCacheProducer is optional (default true): decode the producer's tile once per tile
 template <class Op, class = void>
 struct CacheProducerOf : std::true_type {};
@@ -156,10 +165,11 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     // this many wave iterations so the per-wave CTA barrier below is uniform
     const int64_t waves = (g.tiles - cta0 + GW - 1) / GW;
 
+    constexpr bool kWarpLoad = WarpLoadOf<Op>::value;
     if (lane == 0) {
-        prefetch_tmap(&tmap);
+        if constexpr (!kWarpLoad) prefetch_tmap(&tmap);
 #pragma unroll
-        for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < NS; ++s) mbar_init(&bars[s], kWarpLoad ? 32 : 1);
         fence_barrier_init();
     }
     __syncwarp();
@@ -171,6 +181,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     // the per-stage form measured 2-3 % faster (profiles/ab_producer_decode_r01.txt), so
     // the op opts out. ----
     constexpr bool kCacheP = CacheProducerOf<Op>::value;
+    static_assert(!kWarpLoad || kCacheP, "warp loads use the cached producer tile");
     int64_t pt = gw;
     int pc = 0, pn = 0, prow0 = 0;
     int pcols[G], pimgs[G];
@@ -191,7 +202,9 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     }
     auto issue = [&](int s) {
         if (pt < g.tiles) {
-            if (lane == 0) {
+            if constexpr (kWarpLoad) {
+                Op::load_warp(ring + s * Op::kStageBytes, p, &bars[s], pcols, prow0 + pc * CH, pimgs, lane);
+            } else if (lane == 0) {
                 if constexpr (kCacheP) {
                     mbar_arrive_expect_tx(&bars[s], Op::kTxBytes);
                     Op::load(ring + s * Op::kStageBytes, &tmap, &bars[s], pcols, prow0 + pc * CH, pimgs, policy);

@@ -44,7 +44,9 @@ def _check_exact(got: torch.Tensor, rgb_host: np.ndarray, what: str):
 
 # thesis evaluation sizes (1536x2560 and 4256x2832, both
 # orientations) and the bandwidth-roofline config
-@pytest.mark.parametrize("H,W", [(1536, 2560), (2560, 1536), (4256, 2832), (2832, 4256), (8192, 8192)])
+# (8190, 8190): row starts not 16-byte aligned -> the cp.async strip engine (K2)
+@pytest.mark.parametrize("H,W", [(1536, 2560), (2560, 1536), (4256, 2832), (2832, 4256), (8192, 8192),
+                                 (8190, 8190)])
 def test_fullsize_single_image(cuda_ctx, H, W):
     x = _image(H, W)
     ex = hb.harris(x, exact=True)

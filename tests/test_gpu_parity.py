@@ -473,3 +473,50 @@ def test_launch_cache_keys(cuda_ctx):
     hb.harris(x, out=out, exact=True)
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy(), ref32)
+
+
+# ------------------------------------- K2: cp.async strip engine for unaligned inputs
+@pytest.mark.parametrize("H,W", ANY_SHAPES + [(300, 1918), (133, 2563), (64, 1029)])
+def test_ldg_exact_bitexact(cuda_ctx, H, W):
+    """W % 4 != 0 (row starts not 16-byte aligned): the strip engine with cp.async stage
+    fills runs, bit-identical to the C oracle in EXACT order, within tolerance in FAST."""
+    rgb = synth.synth_numpy(3, H, W, seed=H * 31 + W)
+    got = _run(rgb, exact=True)
+    assert cuda_ctx.last_path == _lib.PATH_LDG
+    assert np.array_equal(got, cref.harris_f32(rgb))
+    ok, m = synth.within_tolerance(_run(rgb), cref.harris_f64(rgb))
+    assert ok, m
+
+
+def test_ldg_unaligned_base_batch_and_bands(cuda_ctx):
+    B, H, W = 5, 70, 261
+    rgb = synth.synth_numpy(3 * B, H, W, seed=77).reshape(B, 3, H, W)
+    # base only 4-byte aligned: a 1-float offset into a larger buffer
+    buf = torch.zeros(rgb.size + 1, device="cuda")
+    x = buf[1:].view(B, 3, H, W)
+    x.copy_(torch.from_numpy(rgb))
+    ex = hb.harris(x, exact=True)
+    assert cuda_ctx.last_path == _lib.PATH_LDG
+    fast = hb.harris(x)
+    torch.cuda.synchronize()
+    for b in range(B):  # strip pairs straddle image boundaries (3 strips per image)
+        assert np.array_equal(ex[b].cpu().numpy(), cref.harris_f32(rgb[b])), b
+        assert torch.equal(fast[b], hb.harris(x[b]))
+    # row bands of an unaligned-pitch image (the multi-GPU split) are bit-identical
+    from paper_2212_12035_b200 import shard
+    img = x[2]
+    full = hb.harris(img)
+    parts = [hb.harris(shard.band_view(img, bnd)) for bnd in shard.row_bands(H - 4, 3)]
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(parts, 0), full)
+    # aligned input viewed with an unaligned base is not TMA either, but equals the TMA result
+    al = torch.from_numpy(synth.synth_numpy(3, 40, 136, seed=3)).cuda()
+    big = torch.zeros(al.numel() + 4, device="cuda")
+    big[1:1 + al.numel()].copy_(al.view(-1))
+    mis = big[1:1 + al.numel()].view(3, 40, 136)
+    r_ldg = hb.harris(mis, exact=True)
+    assert cuda_ctx.last_path == _lib.PATH_LDG
+    r_tma = hb.harris(al, exact=True)
+    assert cuda_ctx.last_path == _lib.PATH_TMA
+    torch.cuda.synchronize()
+    assert torch.equal(r_ldg, r_tma)
