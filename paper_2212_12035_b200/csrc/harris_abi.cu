@@ -35,7 +35,8 @@ struct harris_ctx {
     int sep_cfg = 0;
     int occ_sep[kNumSepConfigs] = {0};
     int occ_u8[kNumU8Configs] = {0};
-    int occ_ldg = 0;
+    int occ_ldg[kNumLdgConfigs] = {0};
+    int ldg_cfg = 2;  // HARRIS_LDG_CONFIG; 2 = scalar lane-halo core, 16 warps/SM (284 k MP/s on 8190^2)
     int sync_waves = 1;  // dev knob HARRIS_SYNC_WAVES=0 disables the per-tile CTA barrier
     int l2_policy = 1;  // evict_normal: the 4-column halo sectors are re-read by the neighbouring strip
     int64_t force_band_rows = 0;  // dev knob (HARRIS_BAND_ROWS): override the planner
@@ -215,8 +216,8 @@ int choose_path(const Call& c) {
 void plan_launch(const harris_ctx* ctx, const Call& c, TileGeom& tg, int64_t& grid) {
     const bool u8 = c.fmt == kU8Interleaved;
     const int fcfg = c.cfg >= 0 ? c.cfg : ctx->tma_cfg;
-    const TmaConfig& cfg = c.ldg ? kLdgConfig : u8 ? kU8Configs[ctx->u8_cfg] : kTmaConfigs[fcfg];
-    const int occ = std::max(1, c.ldg ? ctx->occ_ldg : u8 ? ctx->occ_u8[ctx->u8_cfg] : ctx->occ[fcfg]);
+    const TmaConfig& cfg = c.ldg ? kLdgConfigs[ctx->ldg_cfg] : u8 ? kU8Configs[ctx->u8_cfg] : kTmaConfigs[fcfg];
+    const int occ = std::max(1, c.ldg ? ctx->occ_ldg[ctx->ldg_cfg] : u8 ? ctx->occ_u8[ctx->u8_cfg] : ctx->occ[fcfg]);
     const int64_t resident_ctas = int64_t(ctx->num_sms) * occ;
     plan_tiles(c.g.n, c.g.m, c.g.batch, resident_ctas * cfg.warps, cfg.rows, ctx->force_band_rows, tg, 4,
                cfg.groups, cfg.strip_cols);
@@ -357,7 +358,7 @@ int run(harris_ctx* ctx, const Call& c, cudaStream_t stream) {
             tg.notify_flag = c.notify_flag;
             tg.notify_epoch = c.notify_epoch;
         }
-        e = ldg                         ? launch_ldg(exact, c.g, tg, ent.grid, stream)
+        e = ldg                         ? launch_ldg(ctx->ldg_cfg, exact, c.g, tg, ent.grid, stream)
             : c.fmt == kU8Interleaved ? launch_tma_u8(ctx->u8_cfg, exact, ent.tmap, tg, ent.grid, stream)
                                       : launch_tma(ent.cfg, exact, ent.tmap, tg, ent.grid, stream);
     } else {
@@ -456,6 +457,11 @@ int harris_init(harris_ctx** out_ctx, int cuda_device) {
         int v = std::atoi(env);
         if (v >= 0 && v < kNumSepConfigs) ctx->sep_cfg = v;
     }
+    env = std::getenv("HARRIS_LDG_CONFIG");
+    if (env) {
+        int v = std::atoi(env);
+        if (v >= 0 && v < kNumLdgConfigs) ctx->ldg_cfg = v;
+    }
     env = std::getenv("HARRIS_SYNC_WAVES");
     if (env) ctx->sync_waves = std::atoi(env) != 0;
     env = std::getenv("HARRIS_L2_PROMO");
@@ -490,11 +496,13 @@ int harris_init(harris_ctx** out_ctx, int cuda_device) {
             return rc;
         }
     }
-    e = ldg_configure(&ctx->occ_ldg);
-    if (e != cudaSuccess) {
-        int rc = cuda_fail(ctx, e, "configure ldg kernel");
-        delete ctx;
-        return rc;
+    for (int k = 0; k < kNumLdgConfigs; ++k) {
+        e = ldg_configure(k, &ctx->occ_ldg[k]);
+        if (e != cudaSuccess) {
+            int rc = cuda_fail(ctx, e, "configure ldg kernel");
+            delete ctx;
+            return rc;
+        }
     }
     for (int k = 0; k < kNumSepConfigs; ++k) {
         e = sep_configure(k, &ctx->occ_sep[k]);
@@ -656,7 +664,7 @@ int harris_plan(harris_ctx* ctx, int64_t n, int64_t m, int64_t batch, const floa
     info->path = choose_path(c);
     c.ldg = info->path == HARRIS_PATH_LDG;
     c.cfg = c.ldg ? -1 : resolve_cfg(ctx, c);
-    const TmaConfig& cfg = c.ldg ? kLdgConfig : kTmaConfigs[c.cfg];
+    const TmaConfig& cfg = c.ldg ? kLdgConfigs[ctx->ldg_cfg] : kTmaConfigs[c.cfg];
     info->warps_per_cta = cfg.warps;
     info->stages = cfg.stages;
     info->rows_per_stage = cfg.rows;

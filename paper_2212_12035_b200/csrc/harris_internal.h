@@ -60,9 +60,10 @@ cudaError_t launch_generic(bool exact, const Geom& g, cudaStream_t stream);
 
 // cp.async (LDGSTS) warp-strip kernel for f32 inputs TMA cannot describe (row pitch or
 // base not 16-byte aligned): same engine and dual-strip core as the TMA path
-extern const TmaConfig kLdgConfig;
-cudaError_t ldg_configure(int* ctas_per_sm);
-cudaError_t launch_ldg(bool exact, const Geom& g, const TileGeom& tg, int64_t grid, cudaStream_t stream);
+constexpr int kNumLdgConfigs = 3;
+extern const TmaConfig kLdgConfigs[kNumLdgConfigs];
+cudaError_t ldg_configure(int cfg, int* ctas_per_sm);
+cudaError_t launch_ldg(int cfg, bool exact, const Geom& g, const TileGeom& tg, int64_t grid, cudaStream_t stream);
 
 // interleaved RGB u8 (HWC) input: TMA configs + generic fallback (Geom.rgb is then the
 // byte base pointer; in_pitch / in_image_stride are in BYTES, in_chan_stride unused)

@@ -41,10 +41,10 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, uint32_
 // strip starts at a multiple of 128 columns): 16-byte copies for 16-byte aligned rows,
 // 8-byte for 8-byte aligned ones, 4-byte otherwise; columns at or beyond `avail` are
 // zero-filled (src-size 0 reads nothing)
-template <int BYTES>
+template <int BYTES, int ROW = kBoxCols>
 __device__ __forceinline__ void copy_row(float* dst, const float* src, int avail, int lane) {
     constexpr int E = BYTES / 4;                          // floats per chunk
-    constexpr int NCH = (kBoxCols + E - 1) / E;           // chunks per row
+    constexpr int NCH = (ROW + E - 1) / E;                // chunks per row
 #pragma unroll
     for (int j = lane; j < NCH; j += 32) {
         const int c0 = j * E;
@@ -65,10 +65,16 @@ __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
 }
 
 // BYTES: copy granularity (4; wider copies measured slower: per-row 16/8/4 selection
-// -27 %, 8-byte on 8-byte aligned rows -7 %, profiles/ab_ldg_r01.txt)
-template <bool EXACT, int CH, int BYTES>
-struct HarrisF32x2LdgOp : HarrisF32x2Op<EXACT, CH, 128> {
-    using Base = HarrisF32x2Op<EXACT, CH, 128>;
+// -27 %, 8-byte on 8-byte aligned rows -7 %, profiles/ab_ldg_r01.txt).  BaseOp: the TMA
+// path's op whose shared-memory box layout and row arithmetic are reused unchanged.
+template <class BaseOp, int BYTES>
+struct LdgOp : BaseOp {
+    static constexpr int G = BaseOp::kGroups;
+    static constexpr int CH = BaseOp::kRowsPerStage;
+    // byte distance between the G boxes of a stage (the TMA layout): one box holds
+    // 3 channels x CH rows x kBoxCols floats, padded to 128 bytes
+    static constexpr int kRowFloats = BaseOp::kBox;  // 132, or 128 in the 124-column lane-halo layout
+    static constexpr uint32_t kBoxBytes = (3u * CH * kRowFloats * 4u + 127u) / 128u * 128u;
     static constexpr bool kWarpLoad = true;
     static constexpr bool kCacheProducer = true;
     struct Params {
@@ -78,14 +84,14 @@ struct HarrisF32x2LdgOp : HarrisF32x2Op<EXACT, CH, 128> {
         int32_t W, H;                                       // input columns / rows per image
     };
 
-    __device__ __forceinline__ explicit HarrisF32x2LdgOp(const Params& p) : Base(typename Base::Params{p.kappa}) {}
+    __device__ __forceinline__ explicit LdgOp(const Params& p) : BaseOp(typename BaseOp::Params{p.kappa}) {}
 
     __device__ __forceinline__ static void load_warp(void* smem, const Params& p, uint64_t* bar,
-                                                     const int (&col0)[2], int row0, const int (&image)[2],
+                                                     const int (&col0)[G], int row0, const int (&image)[G],
                                                      int lane) {
         unsigned char* s = static_cast<unsigned char*>(smem);
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < G; ++k) {
             const float* img = p.rgb + int64_t(image[k]) * p.in_image_stride + col0[k];
             const int avail = p.W - col0[k];  // columns of this row from col0 to the row end
 #pragma unroll
@@ -95,8 +101,8 @@ struct HarrisF32x2LdgOp : HarrisF32x2Op<EXACT, CH, 128> {
                     const int y = row0 + r;
                     if (y >= p.H) continue;  // below the image: never reaches a stored output
                     const float* src = img + int64_t(ch) * p.in_chan_stride + int64_t(y) * p.in_pitch;
-                    float* dst = reinterpret_cast<float*>(s + k * Base::kBoxStride) + (ch * CH + r) * kBoxCols;
-                    copy_row<BYTES>(dst, src, avail, lane);
+                    float* dst = reinterpret_cast<float*>(s + k * kBoxBytes) + (ch * CH + r) * kRowFloats;
+                    copy_row<BYTES, kRowFloats>(dst, src, avail, lane);
                 }
             }
         }
@@ -104,49 +110,84 @@ struct HarrisF32x2LdgOp : HarrisF32x2Op<EXACT, CH, 128> {
     }
 };
 
-constexpr int kLdgNW = 8, kLdgNS = 2, kLdgCH = 3;
+// configs: 0 = packed dual-strip core (8 warps/SM), 1 = scalar core (2 x 8 warps/SM)
+template <int CFG>
+struct LdgCfg;
+template <>
+struct LdgCfg<0> {
+    static constexpr int NW = 8, NS = 2, CH = 3, MINB = 1, G = 2;
+    template <bool EXACT>
+    using Op = LdgOp<HarrisF32x2Op<EXACT, CH, 128>, 4>;
+};
+template <>
+struct LdgCfg<1> {
+    static constexpr int NW = 8, NS = 2, CH = 3, MINB = 2, G = 1;
+    template <bool EXACT>
+    using Op = LdgOp<HarrisF32Op<EXACT, CH, 128>, 4>;
+};
 
-template <bool EXACT, int BYTES>
+// 2 = scalar core in the 124-column lane-halo layout: 128-column rows are exactly 4
+// copies per lane (132 need a 5th), and the halo branch disappears
+template <>
+struct LdgCfg<2> {
+    static constexpr int NW = 8, NS = 2, CH = 3, MINB = 2, G = 1;
+    template <bool EXACT>
+    using Op = LdgOp<HarrisF32Op<EXACT, CH, 124>, 4>;
+};
+
+const TmaConfig kLdgConfigs[kNumLdgConfigs] = {{8, 2, 3, 2, 128}, {8, 2, 3, 1, 128}, {8, 2, 3, 1, 124}};
+
+template <int CFG, bool EXACT>
 static constexpr auto ldg_kernel() {
-    return strip_kernel<HarrisF32x2LdgOp<EXACT, kLdgCH, BYTES>, kLdgNW, kLdgNS, 1>;
+    using C = LdgCfg<CFG>;
+    return strip_kernel<typename C::template Op<EXACT>, C::NW, C::NS, C::MINB>;
 }
+template <int CFG>
 static constexpr size_t ldg_smem() {
-    return StripShape<kLdgNW, kLdgNS, HarrisF32x2LdgOp<false, kLdgCH, 4>>::kSmemBytes;
+    using C = LdgCfg<CFG>;
+    return StripShape<C::NW, C::NS, typename C::template Op<false>>::kSmemBytes;
 }
-static_assert(ldg_smem() <= 227 * 1024, "ldg config exceeds 227 KB of shared memory");
+static_assert(ldg_smem<0>() <= 227 * 1024 && ldg_smem<1>() <= 227 * 1024 && ldg_smem<2>() <= 227 * 1024,
+              "ldg smem");
 
-const TmaConfig kLdgConfig = {kLdgNW, kLdgNS, kLdgCH, 2, 128};
-
-cudaError_t ldg_configure(int* ctas_per_sm) {
-    cudaError_t e = cudaFuncSetAttribute(ldg_kernel<false, 4>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(ldg_smem()));
+template <int CFG>
+static cudaError_t ldg_configure_one(int* ctas_per_sm) {
+    cudaError_t e = cudaFuncSetAttribute(ldg_kernel<CFG, false>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(ldg_smem<CFG>()));
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(ldg_kernel<true, 4>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(ldg_smem()));
-
+        e = cudaFuncSetAttribute(ldg_kernel<CFG, true>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(ldg_smem<CFG>()));
     if (e == cudaSuccess)
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, ldg_kernel<false, 4>(), kLdgNW * 32,
-                                                          ldg_smem());
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, ldg_kernel<CFG, false>(), LdgCfg<CFG>::NW * 32,
+                                                          ldg_smem<CFG>());
     return e;
 }
 
-template <bool EXACT, int BYTES>
+cudaError_t ldg_configure(int cfg, int* ctas_per_sm) {
+    return cfg == 0 ? ldg_configure_one<0>(ctas_per_sm)
+           : cfg == 1 ? ldg_configure_one<1>(ctas_per_sm)
+                      : ldg_configure_one<2>(ctas_per_sm);
+}
+
+template <int CFG, bool EXACT>
 static void launch_ldg_one(const Geom& geom, const TileGeom& tg, int64_t grid, cudaStream_t stream) {
     CUtensorMap unused;
     std::memset(&unused, 0, sizeof(unused));
-    const typename HarrisF32x2LdgOp<EXACT, kLdgCH, BYTES>::Params p{
-        geom.kappa, geom.rgb, geom.in_pitch, geom.in_chan_stride, geom.in_image_stride, int32_t(geom.m + 4),
-        int32_t(geom.n + 4)};
-    ldg_kernel<EXACT, BYTES>()<<<unsigned(grid), unsigned(kLdgNW * 32), ldg_smem(), stream>>>(unused, tg, p);
+    const typename LdgCfg<CFG>::template Op<EXACT>::Params p{geom.kappa, geom.rgb, geom.in_pitch,
+                                                            geom.in_chan_stride, geom.in_image_stride,
+                                                            int32_t(geom.m + 4), int32_t(geom.n + 4)};
+    ldg_kernel<CFG, EXACT>()<<<unsigned(grid), unsigned(LdgCfg<CFG>::NW * 32), ldg_smem<CFG>(), stream>>>(unused, tg,
+                                                                                                       p);
 }
 
-cudaError_t launch_ldg(bool exact, const Geom& geom, const TileGeom& tg, int64_t grid, cudaStream_t stream) {
-    // 4-byte copies for every alignment: 8-byte copies on 8-byte aligned rows measured
-    // 7 % slower (profiles/ab_ldg_r01.txt)
-    if (exact)
-        launch_ldg_one<true, 4>(geom, tg, grid, stream);
+cudaError_t launch_ldg(int cfg, bool exact, const Geom& geom, const TileGeom& tg, int64_t grid,
+                       cudaStream_t stream) {
+    if (cfg == 0)
+        exact ? launch_ldg_one<0, true>(geom, tg, grid, stream) : launch_ldg_one<0, false>(geom, tg, grid, stream);
+    else if (cfg == 1)
+        exact ? launch_ldg_one<1, true>(geom, tg, grid, stream) : launch_ldg_one<1, false>(geom, tg, grid, stream);
     else
-        launch_ldg_one<false, 4>(geom, tg, grid, stream);
+        exact ? launch_ldg_one<2, true>(geom, tg, grid, stream) : launch_ldg_one<2, false>(geom, tg, grid, stream);
     return cudaGetLastError();
 }
 

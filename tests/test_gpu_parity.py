@@ -520,3 +520,21 @@ def test_ldg_unaligned_base_batch_and_bands(cuda_ctx):
     assert cuda_ctx.last_path == _lib.PATH_TMA
     torch.cuda.synchronize()
     assert torch.equal(r_ldg, r_tma)
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2])
+def test_every_ldg_config_bitexact(cuda_ctx, cfg):
+    ctx = _ctx_with({"HARRIS_LDG_CONFIG": cfg})
+    for B, H, W in [(1, 9, 131), (1, 70, 261), (3, 41, 387), (1, 300, 2563), (5, 21, 137)]:
+        rgb = synth.synth_numpy(3 * B, H, W, seed=cfg * 13 + H).reshape(B, 3, H, W)
+        x = _dev(rgb if B > 1 else rgb[0])
+        ex = hb.harris(x, exact=True, ctx=ctx)
+        assert ctx.last_path == _lib.PATH_LDG
+        fast = hb.harris(x, ctx=ctx)
+        torch.cuda.synchronize()
+        ex, fast = ex.cpu().numpy().reshape(B, H - 4, W - 4), fast.cpu().numpy().reshape(B, H - 4, W - 4)
+        for b in range(B):
+            assert np.array_equal(ex[b], cref.harris_f32(rgb[b])), (cfg, B, H, W, b)
+            ok, m = synth.within_tolerance(fast[b], cref.harris_f64(rgb[b]))
+            assert ok, (cfg, B, H, W, b, m)
+    ctx.close()
