@@ -67,8 +67,9 @@ extern "C" {
 #define HARRIS_PATH_NONE    0
 #define HARRIS_PATH_TMA     1  /* K1: TMA-staged warp-strip kernel (W%4==0, aligned) */
 #define HARRIS_PATH_GENERIC 2  /* K0: shared-memory tile kernel (any W, any pitch)   */
-#define HARRIS_PATH_LDG     3  /* K2: the TMA kernel's engine with cp.async stage fills, for f32
-                                      inputs whose pitch / base are not 16-byte aligned */
+#define HARRIS_PATH_LDG     3  /* K2: the TMA kernel's engine with cp.async stage fills, for
+                                      inputs whose strides / base TMA cannot describe (f32 with
+                                      W % 4 != 0 or a 4-byte aligned base; u8 with 3W % 16 != 0) */
 
 typedef struct harris_ctx harris_ctx;
 

@@ -36,6 +36,7 @@ struct harris_ctx {
     int occ_sep[kNumSepConfigs] = {0};
     int occ_u8[kNumU8Configs] = {0};
     int occ_ldg[kNumLdgConfigs] = {0};
+    int occ_u8ldg = 0;
     int ldg_cfg = 2;  // HARRIS_LDG_CONFIG; 2 = scalar lane-halo core, 16 warps/SM (284 k MP/s on 8190^2)
     int sync_waves = 1;  // dev knob HARRIS_SYNC_WAVES=0 disables the per-tile CTA barrier
     int l2_policy = 1;  // evict_normal: the 4-column halo sectors are re-read by the neighbouring strip
@@ -202,7 +203,7 @@ void plan_tiles(int64_t n, int64_t m, int64_t batch, int64_t gw, int rows_per_st
 // strip engine with cp.async stage fills; only 4-byte alignment of the floats is needed
 bool ldg_eligible(const Call& c) {
     const Geom& g = c.g;
-    if (c.fmt != kF32Planar || (reinterpret_cast<uintptr_t>(g.rgb) & 3)) return false;
+    if (c.fmt == kF32Planar && (reinterpret_cast<uintptr_t>(g.rgb) & 3)) return false;  // u8: any byte address
     if (g.batch * ((g.m + 123) / 124) >= (int64_t(1) << 30)) return false;
     return g.n + 4 <= INT32_MAX && g.m + 4 <= INT32_MAX;
 }
@@ -216,8 +217,10 @@ int choose_path(const Call& c) {
 void plan_launch(const harris_ctx* ctx, const Call& c, TileGeom& tg, int64_t& grid) {
     const bool u8 = c.fmt == kU8Interleaved;
     const int fcfg = c.cfg >= 0 ? c.cfg : ctx->tma_cfg;
-    const TmaConfig& cfg = c.ldg ? kLdgConfigs[ctx->ldg_cfg] : u8 ? kU8Configs[ctx->u8_cfg] : kTmaConfigs[fcfg];
-    const int occ = std::max(1, c.ldg ? ctx->occ_ldg[ctx->ldg_cfg] : u8 ? ctx->occ_u8[ctx->u8_cfg] : ctx->occ[fcfg]);
+    const TmaConfig& cfg = c.ldg ? (u8 ? kU8LdgConfig : kLdgConfigs[ctx->ldg_cfg])
+                                 : u8 ? kU8Configs[ctx->u8_cfg] : kTmaConfigs[fcfg];
+    const int occ = std::max(1, c.ldg ? (u8 ? ctx->occ_u8ldg : ctx->occ_ldg[ctx->ldg_cfg])
+                                      : u8 ? ctx->occ_u8[ctx->u8_cfg] : ctx->occ[fcfg]);
     const int64_t resident_ctas = int64_t(ctx->num_sms) * occ;
     plan_tiles(c.g.n, c.g.m, c.g.batch, resident_ctas * cfg.warps, cfg.rows, ctx->force_band_rows, tg, 4,
                cfg.groups, cfg.strip_cols);
@@ -358,7 +361,8 @@ int run(harris_ctx* ctx, const Call& c, cudaStream_t stream) {
             tg.notify_flag = c.notify_flag;
             tg.notify_epoch = c.notify_epoch;
         }
-        e = ldg                         ? launch_ldg(ctx->ldg_cfg, exact, c.g, tg, ent.grid, stream)
+        e = ldg ? (c.fmt == kU8Interleaved ? launch_u8_ldg(exact, c.g, tg, ent.grid, stream)
+                                           : launch_ldg(ctx->ldg_cfg, exact, c.g, tg, ent.grid, stream))
             : c.fmt == kU8Interleaved ? launch_tma_u8(ctx->u8_cfg, exact, ent.tmap, tg, ent.grid, stream)
                                       : launch_tma(ent.cfg, exact, ent.tmap, tg, ent.grid, stream);
     } else {
@@ -495,6 +499,12 @@ int harris_init(harris_ctx** out_ctx, int cuda_device) {
             delete ctx;
             return rc;
         }
+    }
+    e = u8_ldg_configure(&ctx->occ_u8ldg);
+    if (e != cudaSuccess) {
+        int rc = cuda_fail(ctx, e, "configure u8 ldg kernel");
+        delete ctx;
+        return rc;
     }
     for (int k = 0; k < kNumLdgConfigs; ++k) {
         e = ldg_configure(k, &ctx->occ_ldg[k]);

@@ -64,6 +64,10 @@ constexpr int kNumLdgConfigs = 3;
 extern const TmaConfig kLdgConfigs[kNumLdgConfigs];
 cudaError_t ldg_configure(int cfg, int* ctas_per_sm);
 cudaError_t launch_ldg(int cfg, bool exact, const Geom& g, const TileGeom& tg, int64_t grid, cudaStream_t stream);
+// interleaved u8 inputs whose byte strides TMA cannot describe (3W % 16 != 0)
+extern const TmaConfig kU8LdgConfig;
+cudaError_t u8_ldg_configure(int* ctas_per_sm);
+cudaError_t launch_u8_ldg(bool exact, const Geom& g, const TileGeom& tg, int64_t grid, cudaStream_t stream);
 
 // interleaved RGB u8 (HWC) input: TMA configs + generic fallback (Geom.rgb is then the
 // byte base pointer; in_pitch / in_image_stride are in BYTES, in_chan_stride unused)

@@ -326,7 +326,7 @@ struct HarrisU8Op {
     }
 
     int skip = 0;  // words before the strip's first pixel in the box (SC = 124 only)
-    __device__ __forceinline__ void begin_tile(const int (&col0)[1]) {
+    __device__ __forceinline__ void begin_tile(const int (&col0)[1], int, const int (&)[1]) {
         if constexpr (SC != 128) skip = L::u8_skip(col0[0] / SC);
     }
 

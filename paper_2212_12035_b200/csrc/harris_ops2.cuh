@@ -328,7 +328,7 @@ struct HarrisU8x2Op {
     }
 
     int skip_a = 0, skip_b = 0;  // words before each strip's first pixel (SC = 124 only)
-    __device__ __forceinline__ void begin_tile(const int (&col0)[2]) {
+    __device__ __forceinline__ void begin_tile(const int (&col0)[2], int, const int (&)[2]) {
         if constexpr (SC != 128) {
             skip_a = L::u8_skip(col0[0] / SC);
             skip_b = L::u8_skip(col0[1] / SC);

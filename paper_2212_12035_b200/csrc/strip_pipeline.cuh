@@ -107,7 +107,8 @@ template <class Op>
 struct CacheProducerOf<Op, std::void_t<decltype(Op::kCacheProducer)>>
     : std::integral_constant<bool, Op::kCacheProducer> {};
 
-// Op::begin_tile(strip_col0) is optional: per-tile state of the op (e.g. the u8 box skew)
+// Op::begin_tile(strip_col0, row0, image) is optional: per-tile state of the op (e.g. the
+// u8 box skew)
 template <class Op, class = void>
 struct HasBeginTile : std::false_type {};
 template <class Op>
@@ -252,10 +253,13 @@ __global__ void __launch_bounds__(NW * 32, MINB)
         const int rows_out = band_rows_out(tc.band, g);
         const int nch = (rows_out + HALO + CH - 1) / CH;
         if constexpr (HasBeginTile<Op>::value) {
-            int c0[G];
+            int c0[G], im[G];
 #pragma unroll
-            for (int k = 0; k < G; ++k) c0[k] = tc.cs[k] * Op::kStripCols;
-            op.begin_tile(c0);
+            for (int k = 0; k < G; ++k) {
+                c0[k] = tc.cs[k] * Op::kStripCols;
+                im[k] = tc.b[k];
+            }
+            op.begin_tile(c0, tc.band * g.band_rows, im);
         }
         int colg[G];
         float* orow[G];

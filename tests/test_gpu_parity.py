@@ -538,3 +538,44 @@ def test_every_ldg_config_bitexact(cuda_ctx, cfg):
             ok, m = synth.within_tolerance(fast[b], cref.harris_f64(rgb[b]))
             assert ok, (cfg, B, H, W, b, m)
     ctx.close()
+
+
+@pytest.mark.parametrize("H,W", [(5, 5), (13, 17), (40, 130), (64, 200), (300, 1918), (133, 2563)])
+def test_u8_ldg_exact_equals_f32_path(cuda_ctx, H, W):
+    """3W % 16 != 0 (rows not 16-byte aligned): the u8 cp.async path, bit-identical in
+    EXACT order to the planar f32 path / C oracle on byte/255."""
+    hwc, f32 = _u8_image(1, H, W, seed=5 * H + W)
+    x = torch.from_numpy(hwc[0]).cuda()
+    got = hb.harris_u8(x, exact=True)
+    assert cuda_ctx.last_path == _lib.PATH_LDG
+    torch.cuda.synchronize()
+    assert np.array_equal(got.cpu().numpy(), cref.harris_f32(f32[0]))
+    fast = hb.harris_u8(x)
+    torch.cuda.synchronize()
+    ok, m = synth.within_tolerance(fast.cpu().numpy(), cref.harris_f64(f32[0]))
+    assert ok, m
+
+
+def test_u8_ldg_unaligned_base_and_batch(cuda_ctx):
+    B, H, W = 4, 37, 263
+    hwc, f32 = _u8_image(B, H, W, seed=91)
+    for off in (1, 2, 3):  # byte offsets: every row start misaligned differently
+        buf = torch.zeros(hwc.size + off, dtype=torch.uint8, device="cuda")
+        x = buf[off:].view(B, H, W, 3)
+        x.copy_(torch.from_numpy(hwc))
+        got = hb.harris_u8(x, exact=True)
+        assert cuda_ctx.last_path == _lib.PATH_LDG
+        torch.cuda.synchronize()
+        for b in range(B):
+            assert np.array_equal(got[b].cpu().numpy(), cref.harris_f32(f32[b])), (off, b)
+    # an aligned-width image through a misaligned base equals the TMA result
+    hwc2, _ = _u8_image(2, 40, 128, seed=3)
+    ref = hb.harris_u8(torch.from_numpy(hwc2).cuda(), exact=True)
+    assert cuda_ctx.last_path == _lib.PATH_TMA
+    buf = torch.zeros(hwc2.size + 1, dtype=torch.uint8, device="cuda")
+    mis = buf[1:].view(2, 40, 128, 3)
+    mis.copy_(torch.from_numpy(hwc2))
+    got = hb.harris_u8(mis, exact=True)
+    assert cuda_ctx.last_path == _lib.PATH_LDG
+    torch.cuda.synchronize()
+    assert torch.equal(got, ref)
