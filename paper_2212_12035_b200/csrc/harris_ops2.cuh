@@ -130,24 +130,35 @@ struct HarrisCore2 {
     template <int R, class HaloFn>
     __device__ __forceinline__ void step(const float2 (&gown)[4], int lane, HaloFn&& halo, float (&out)[2][4]) {
         constexpr int s2 = R % 3, s0 = (R + 1) % 3, s1 = (R + 2) % 3;
+        constexpr bool kLaneHalo = std::is_same_v<std::decay_t<HaloFn>, NoHalo>;
+        // lane-halo layout, FAST: Sobel on this lane's 4 columns only, columns 4 and 5 from
+        // lane + 1 (same operands, same order: bit-identical; 24 fewer state registers)
+        constexpr int NC = (kLaneHalo && !EXACT) ? 4 : 6;
         float2 g[8];
 #pragma unroll
         for (int k = 0; k < 4; ++k) g[k] = gown[k];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) g[4 + k] = shfl_down2(g[k]);
-        if constexpr (!std::is_same_v<std::decay_t<HaloFn>, NoHalo>)
+        for (int k = 0; k < NC - 2; ++k) g[4 + k] = shfl_down2(g[k]);
+        if constexpr (!kLaneHalo)
             if (lane == 31) halo(g[4], g[5], g[6], g[7]);
         if constexpr (!EXACT) {
 #pragma unroll
-            for (int k = 0; k < 6; ++k) {
+            for (int k = 0; k < NC; ++k) {
                 D[s2][k] = sub2(g[k + 2], g[k]);
                 Hs[s2][k] = add2(fma2(f2(2.f), g[k + 1], g[k]), g[k + 2]);
             }
             float2 ix[6], iy[6];
 #pragma unroll
-            for (int k = 0; k < 6; ++k) {
+            for (int k = 0; k < NC; ++k) {
                 ix[k] = fma2(f2(2.f), D[s1][k], add2(D[s0][k], D[s2][k]));
                 iy[k] = sub2(Hs[s2][k], Hs[s0][k]);
+            }
+            if constexpr (NC == 4) {
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    ix[4 + k] = shfl_down2(ix[k]);
+                    iy[4 + k] = shfl_down2(iy[k]);
+                }
             }
             prodsum4(ix, ix, HB[s2][0], HB[s2][1], HB[s2][2], HB[s2][3]);
             prodsum4(ix, iy, HB[s2][4], HB[s2][5], HB[s2][6], HB[s2][7]);
