@@ -272,6 +272,30 @@ def cpu_baseline(wl_name: str, wl: dict, min_seconds: float = 10.0) -> dict:
             "cpu_model": cpu_model()}
 
 
+def opencv_baseline(wl: dict, images: int = 2) -> dict:
+    """The thesis's other CPU comparison point: an OpenCV-composed Harris (PAPER.md:2879,
+    2891) on the same synthetic images (informational; oracle/opencv_ref.py)."""
+    try:
+        from oracle import cref, opencv_ref
+        if not opencv_ref.available():
+            return {"unavailable": "cv2 not importable"}
+        import cv2
+        H, W = wl["H"], wl["W"]
+        x = cref.synth(3 * images, H, W, seed=SEED).reshape(images, 3, H, W)
+        opencv_ref.harris_opencv(x[0])
+        t0 = time.perf_counter()
+        k = 0
+        while time.perf_counter() - t0 < 1.0:
+            for b in range(images):
+                opencv_ref.harris_opencv(x[b])
+            k += 1
+        dt = time.perf_counter() - t0
+        return {"value": k * images * (H - 4) * (W - 4) / dt / 1e6, "unit": "MP/s", "threads": cv2.getNumThreads(),
+                "opencv": cv2.__version__, "sample": f"{images} image(s) of {W}x{H}, {k} pass(es)"}
+    except Exception as e:  # informational only
+        return {"error": repr(e)}
+
+
 def cpu_model() -> str:
     try:
         for line in open("/proc/cpuinfo"):
@@ -380,6 +404,8 @@ def run_gpu(a, world, rank, local) -> dict | None:
     cpu = None
     if world == 1 and rank == 0 and not a.no_cpu_baseline:
         cpu = cpu_baseline(a.workload, wl, a.cpu_seconds)
+        if not a.no_extra:
+            extra["cpu_opencv"] = opencv_baseline(wl)
     if rank != 0:
         return None
     return {

@@ -143,3 +143,16 @@ def test_sges_bridge_registration_types_and_evaluates(oracle_lib):
     sges_bridge.register(bad, amb_bad, impl=cref.harris_f64, reference_src=sges_oracle.REFERENCE_SRC)
     with pytest.raises(ValueError):
         sges_bridge.evaluate("harris rgb", bad, amb_bad, reference_src=sges_oracle.REFERENCE_SRC)
+
+
+def test_opencv_composition_meets_tolerance(oracle_lib):
+    """The thesis's OpenCV-composed comparison pipeline, restated with
+    the image's OpenCV, matches the f64 oracle within the SURVEY.md §8(d) tolerance (it is a
+    reported CPU baseline in bench.py)."""
+    from oracle import cref, opencv_ref, synth
+    if not opencv_ref.available():
+        pytest.skip("cv2 not importable")
+    for H, W, seed in [(64, 96, 1), (300, 517, 2)]:
+        x = cref.synth(3, H, W, seed=seed)
+        ok, m = synth.within_tolerance(opencv_ref.harris_opencv(x), cref.harris_f64(x))
+        assert ok, m
