@@ -33,6 +33,8 @@ def timed(fn, iters=40):
     return round(ts[len(ts) // 2], 2), round(ts[0], 2)
 
 
+tiny_t = torch.empty(1, device="cuda")
+print("minimal kernel (1-element fill_) after flush us", timed(lambda: tiny_t.fill_(1.0)))
 xt = torch.empty((3, 12, 136), device="cuda")
 hb.synth_(xt, seed=1)
 ot = torch.empty((8, 132), device="cuda")
