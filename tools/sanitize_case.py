@@ -1,0 +1,56 @@
+"""Dev: one small launch of every kernel path, for compute-sanitizer (memcheck / racecheck /
+synccheck / initcheck).  Prints the paths it exercised."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2212_12035_b200 as hb  # noqa: E402
+from paper_2212_12035_b200 import _lib  # noqa: E402
+
+ctx = hb.context(0)
+seen = []
+
+
+def f32(B, H, W, off=0, **kw):
+    buf = torch.rand(off + B * 3 * H * W, device="cuda")
+    x = buf[off:].view(B, 3, H, W)
+    for exact in (False, True):
+        hb.harris(x if B > 1 else x[0], exact=exact, **kw)
+        seen.append(("f32", B, H, W, off, exact, ctx.last_path, kw.get("force_generic", False)))
+
+
+def u8(B, H, W, off=0, **kw):
+    buf = torch.randint(0, 256, (off + B * H * W * 3,), dtype=torch.uint8, device="cuda")
+    x = buf[off:].view(B, H, W, 3)
+    for exact in (False, True):
+        hb.harris_u8(x if B > 1 else x[0], exact=exact, **kw)
+        seen.append(("u8", B, H, W, off, exact, ctx.last_path))
+
+
+f32(1, 70, 264)            # TMA, short tiles -> scalar core
+f32(1, 300, 1028)          # TMA dual-strip core
+f32(3, 41, 388)            # TMA dual, strip pairs straddling images
+f32(2, 37, 71)             # K2 cp.async (width % 4 != 0)
+f32(1, 40, 136, off=1)     # K2 (4-byte aligned base)
+f32(1, 37, 71, force_generic=True)  # K0
+u8(2, 40, 400)             # u8 TMA
+u8(2, 37, 263, off=1)      # u8 K2
+img = torch.rand(2, 50, 260, device="cuda")
+hb.stencil3x3_sep(img)
+hb.stencil3x3_sep(img, exact=True)
+for g in (1, 2, 3, 4):
+    hb.harris_grouping(torch.rand(3, 40, 132, device="cuda"), g)
+x = torch.rand(3, 40, 136, device="cuda")
+out = torch.empty(36, 132, device="cuda")
+flag = torch.zeros(2, dtype=torch.int32, device="cuda")
+st = torch.cuda.current_stream().cuda_stream
+L = _lib.lib()
+assert L.harris_run_notify(ctx.handle, out.data_ptr(), 132, 36 * 132, 36, 132, x.data_ptr(), 136, 40 * 136,
+                           3 * 40 * 136, 1, 0.04, 0, flag.data_ptr(), 1, st) == 0
+assert L.harris_peer_wait(flag.data_ptr(), 1, 1, flag.data_ptr() + 4, 1_000_000_000, st) == 0
+torch.cuda.synchronize()
+assert int(flag[0].item()) == 1 and int(flag[1].item()) == 0
+paths = sorted({s[-2] if s[0] == "f32" else s[-1] for s in seen})
+print("ok; paths exercised:", paths, "cases:", len(seen))
