@@ -37,6 +37,7 @@ struct harris_ctx {
     int occ_u8[kNumU8Configs] = {0};
     int occ_ldg[kNumLdgConfigs] = {0};
     int occ_u8ldg = 0;
+    int occ_sepldg = 0;
     int ldg_cfg = 2;  // HARRIS_LDG_CONFIG; 2 = scalar lane-halo core, 16 warps/SM (284 k MP/s on 8190^2)
     int sync_waves = 1;  // dev knob HARRIS_SYNC_WAVES=0 disables the per-tile CTA barrier
     int l2_policy = 1;  // evict_normal: the 4-column halo sectors are re-read by the neighbouring strip
@@ -500,7 +501,8 @@ int harris_init(harris_ctx** out_ctx, int cuda_device) {
             return rc;
         }
     }
-    e = u8_ldg_configure(&ctx->occ_u8ldg);
+    e = sep_ldg_configure(&ctx->occ_sepldg);
+    if (e == cudaSuccess) e = u8_ldg_configure(&ctx->occ_u8ldg);
     if (e != cudaSuccess) {
         int rc = cuda_fail(ctx, e, "configure u8 ldg kernel");
         delete ctx;
@@ -623,10 +625,27 @@ int harris_stencil3x3_sep(harris_ctx* ctx, float* out, int64_t out_pitch, int64_
     const bool tma = !(flags & HARRIS_FLAG_FORCE_GENERIC) && aligned16(in) && (in_pitch & 3) == 0 &&
                      (batch == 1 || (in_image_stride & 3) == 0) && batch <= INT32_MAX;
     if (!tma && (flags & HARRIS_FLAG_FORCE_TMA)) return HARRIS_ERR_ALIGNMENT;
+    // other 4-byte aligned planes: the same strip engine with cp.async stage fills
+    const bool ldg = !tma && !(flags & HARRIS_FLAG_FORCE_GENERIC) && (reinterpret_cast<uintptr_t>(in) & 3) == 0 &&
+                     batch * ((m + 127) / 128) < (int64_t(1) << 30);
     DeviceGuard guard(ctx->device);
     if (!guard.ok) return cuda_fail(ctx, cudaGetLastError(), "cudaSetDevice");
     cudaError_t e;
-    if (tma) {
+    if (ldg) {
+        TileGeom tg;
+        const int64_t resident = int64_t(ctx->num_sms) * std::max(1, ctx->occ_sepldg);
+        plan_tiles(n, m, batch, resident * kSepLdgConfig.warps, kSepLdgConfig.rows, ctx->force_band_rows, tg, 2);
+        const int64_t grid = std::min<int64_t>((tg.tiles + kSepLdgConfig.warps - 1) / kSepLdgConfig.warps, resident);
+        tg.out = out;
+        tg.out_pitch = out_pitch;
+        tg.out_image_stride = batch > 1 ? out_image_stride : n * out_pitch;
+        tg.kappa = 0.f;
+        tg.l2_policy = ctx->l2_policy;
+        tg.vec_store = aligned16(out) && (out_pitch & 3) == 0 && (batch == 1 || (out_image_stride & 3) == 0);
+        tg.sync_waves = ctx->sync_waves;
+        if (tg.tiles > INT32_MAX) return HARRIS_ERR_SIZE;
+        e = launch_sep_ldg(exact, in, in_pitch, img_stride, m + 2, n + 2, tg, grid, wv, wh, stream);
+    } else if (tma) {
         CUtensorMap tmap;
         cuuint64_t dims[3] = {cuuint64_t(m + 2), cuuint64_t(n + 2), cuuint64_t(batch)};
         cuuint64_t strides[2] = {cuuint64_t(in_pitch) * 4, cuuint64_t((img_stride + 3) / 4 * 4) * 4};
@@ -658,7 +677,7 @@ int harris_stencil3x3_sep(harris_ctx* ctx, float* out, int64_t out_pitch, int64_
                                stream);
     }
     if (e != cudaSuccess) return cuda_fail(ctx, e, "launch stencil");
-    ctx->last_path = tma ? HARRIS_PATH_TMA : HARRIS_PATH_GENERIC;
+    ctx->last_path = tma ? HARRIS_PATH_TMA : ldg ? HARRIS_PATH_LDG : HARRIS_PATH_GENERIC;
     return HARRIS_OK;
 }
 

@@ -68,6 +68,12 @@ cudaError_t launch_ldg(int cfg, bool exact, const Geom& g, const TileGeom& tg, i
 extern const TmaConfig kU8LdgConfig;
 cudaError_t u8_ldg_configure(int* ctas_per_sm);
 cudaError_t launch_u8_ldg(bool exact, const Geom& g, const TileGeom& tg, int64_t grid, cudaStream_t stream);
+// separable stencil planes TMA cannot describe
+extern const TmaConfig kSepLdgConfig;
+cudaError_t sep_ldg_configure(int* ctas_per_sm);
+cudaError_t launch_sep_ldg(bool exact, const float* in, int64_t in_pitch, int64_t in_image_stride, int64_t W,
+                           int64_t H, const TileGeom& tg, int64_t grid, const float* wv, const float* wh,
+                           cudaStream_t stream);
 
 // interleaved RGB u8 (HWC) input: TMA configs + generic fallback (Geom.rgb is then the
 // byte base pointer; in_pitch / in_image_stride are in BYTES, in_chan_stride unused)

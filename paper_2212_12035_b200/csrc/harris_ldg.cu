@@ -20,6 +20,7 @@
 #include "harris_internal.h"
 #include "harris_ops.cuh"
 #include "harris_ops2.cuh"
+#include "stencil_sep.cuh"
 #include "strip_pipeline.cuh"
 
 namespace harris {
@@ -67,24 +68,36 @@ __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
 // BYTES: copy granularity (4; wider copies measured slower: per-row 16/8/4 selection
 // -27 %, 8-byte on 8-byte aligned rows -7 %, profiles/ab_ldg_r01.txt).  BaseOp: the TMA
 // path's op whose shared-memory box layout and row arithmetic are reused unchanged.
+// planes per input image (3 for the Harris ops, 1 for the separable stencil) and the
+// shared-memory row width of the base op's box
+template <class Op, class = void>
+struct PlanesOf : std::integral_constant<int, 3> {};
+template <class Op>
+struct PlanesOf<Op, std::void_t<decltype(Op::kPlanes)>> : std::integral_constant<int, Op::kPlanes> {};
+template <class Op, class = void>
+struct BoxFloatsOf : std::integral_constant<int, kBoxCols> {};
+template <class Op>
+struct BoxFloatsOf<Op, std::void_t<decltype(Op::kBox)>> : std::integral_constant<int, Op::kBox> {};
+
 template <class BaseOp, int BYTES>
 struct LdgOp : BaseOp {
     static constexpr int G = BaseOp::kGroups;
     static constexpr int CH = BaseOp::kRowsPerStage;
-    // byte distance between the G boxes of a stage (the TMA layout): one box holds
-    // 3 channels x CH rows x kBoxCols floats, padded to 128 bytes
-    static constexpr int kRowFloats = BaseOp::kBox;  // 132, or 128 in the 124-column lane-halo layout
-    static constexpr uint32_t kBoxBytes = (3u * CH * kRowFloats * 4u + 127u) / 128u * 128u;
+    static constexpr int P = PlanesOf<BaseOp>::value;
+    static constexpr int kRowFloats = BoxFloatsOf<BaseOp>::value;  // 132, or 128 in the lane-halo layout
+    // byte distance between the G boxes of a stage (the TMA layout): P planes x CH rows,
+    // padded to 128 bytes
+    static constexpr uint32_t kBoxBytes = (uint32_t(P) * CH * kRowFloats * 4u + 127u) / 128u * 128u;
     static constexpr bool kWarpLoad = true;
     static constexpr bool kCacheProducer = true;
     struct Params {
-        float kappa;
-        const float* rgb;
-        int64_t in_pitch, in_chan_stride, in_image_stride;  // elements
-        int32_t W, H;                                       // input columns / rows per image
+        typename BaseOp::Params base;
+        const float* src;
+        int64_t in_pitch, in_plane_stride, in_image_stride;  // elements
+        int32_t W, H;                                        // input columns / rows per image
     };
 
-    __device__ __forceinline__ explicit LdgOp(const Params& p) : BaseOp(typename BaseOp::Params{p.kappa}) {}
+    __device__ __forceinline__ explicit LdgOp(const Params& p) : BaseOp(p.base) {}
 
     __device__ __forceinline__ static void load_warp(void* smem, const Params& p, uint64_t* bar,
                                                      const int (&col0)[G], int row0, const int (&image)[G],
@@ -92,15 +105,15 @@ struct LdgOp : BaseOp {
         unsigned char* s = static_cast<unsigned char*>(smem);
 #pragma unroll
         for (int k = 0; k < G; ++k) {
-            const float* img = p.rgb + int64_t(image[k]) * p.in_image_stride + col0[k];
+            const float* img = p.src + int64_t(image[k]) * p.in_image_stride + col0[k];
             const int avail = p.W - col0[k];  // columns of this row from col0 to the row end
 #pragma unroll
-            for (int ch = 0; ch < 3; ++ch) {
+            for (int ch = 0; ch < P; ++ch) {
 #pragma unroll
                 for (int r = 0; r < CH; ++r) {
                     const int y = row0 + r;
                     if (y >= p.H) continue;  // below the image: never reaches a stored output
-                    const float* src = img + int64_t(ch) * p.in_chan_stride + int64_t(y) * p.in_pitch;
+                    const float* src = img + int64_t(ch) * p.in_plane_stride + int64_t(y) * p.in_pitch;
                     float* dst = reinterpret_cast<float*>(s + k * kBoxBytes) + (ch * CH + r) * kRowFloats;
                     copy_row<BYTES, kRowFloats>(dst, src, avail, lane);
                 }
@@ -281,9 +294,9 @@ template <int CFG, bool EXACT>
 static void launch_ldg_one(const Geom& geom, const TileGeom& tg, int64_t grid, cudaStream_t stream) {
     CUtensorMap unused;
     std::memset(&unused, 0, sizeof(unused));
-    const typename LdgCfg<CFG>::template Op<EXACT>::Params p{geom.kappa, geom.rgb, geom.in_pitch,
-                                                            geom.in_chan_stride, geom.in_image_stride,
-                                                            int32_t(geom.m + 4), int32_t(geom.n + 4)};
+    using Op = typename LdgCfg<CFG>::template Op<EXACT>;
+    const typename Op::Params p{{geom.kappa}, geom.rgb, geom.in_pitch, geom.in_chan_stride, geom.in_image_stride,
+                                int32_t(geom.m + 4), int32_t(geom.n + 4)};
     ldg_kernel<CFG, EXACT>()<<<unsigned(grid), unsigned(LdgCfg<CFG>::NW * 32), ldg_smem<CFG>(), stream>>>(unused, tg,
                                                                                                        p);
 }
@@ -296,6 +309,53 @@ cudaError_t launch_ldg(int cfg, bool exact, const Geom& geom, const TileGeom& tg
         exact ? launch_ldg_one<1, true>(geom, tg, grid, stream) : launch_ldg_one<1, false>(geom, tg, grid, stream);
     else
         exact ? launch_ldg_one<2, true>(geom, tg, grid, stream) : launch_ldg_one<2, false>(geom, tg, grid, stream);
+    return cudaGetLastError();
+}
+
+// ---- separable 3x3 stencil on planes TMA cannot describe (pitch % 4 != 0 / base) ----
+constexpr int kSepLdgNW = 8, kSepLdgNS = 8, kSepLdgCH = 6;
+const TmaConfig kSepLdgConfig = {kSepLdgNW, kSepLdgNS, kSepLdgCH, 1, 128};
+
+template <bool EXACT>
+static constexpr auto sep_ldg_kernel() {
+    return strip_kernel<LdgOp<Sep3x3Op<EXACT, kSepLdgCH>, 4>, kSepLdgNW, kSepLdgNS, 1>;
+}
+static constexpr size_t sep_ldg_smem() {
+    return StripShape<kSepLdgNW, kSepLdgNS, LdgOp<Sep3x3Op<false, kSepLdgCH>, 4>>::kSmemBytes;
+}
+static_assert(sep_ldg_smem() <= 227 * 1024, "stencil ldg smem");
+
+cudaError_t sep_ldg_configure(int* ctas_per_sm) {
+    cudaError_t e = cudaFuncSetAttribute(sep_ldg_kernel<false>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(sep_ldg_smem()));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(sep_ldg_kernel<true>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(sep_ldg_smem()));
+    if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, sep_ldg_kernel<false>(), kSepLdgNW * 32,
+                                                          sep_ldg_smem());
+    return e;
+}
+
+template <bool EXACT>
+static void launch_sep_ldg_one(const float* in, int64_t in_pitch, int64_t in_image_stride, int32_t W, int32_t H,
+                               const TileGeom& tg, int64_t grid, const float* wv, const float* wh,
+                               cudaStream_t stream) {
+    CUtensorMap unused;
+    std::memset(&unused, 0, sizeof(unused));
+    using Op = LdgOp<Sep3x3Op<EXACT, kSepLdgCH>, 4>;
+    const typename Op::Params p{{{wv[0], wv[1], wv[2]}, {wh[0], wh[1], wh[2]}}, in, in_pitch, 0, in_image_stride, W,
+                                H};
+    sep_ldg_kernel<EXACT>()<<<unsigned(grid), unsigned(kSepLdgNW * 32), sep_ldg_smem(), stream>>>(unused, tg, p);
+}
+
+cudaError_t launch_sep_ldg(bool exact, const float* in, int64_t in_pitch, int64_t in_image_stride, int64_t W,
+                           int64_t H, const TileGeom& tg, int64_t grid, const float* wv, const float* wh,
+                           cudaStream_t stream) {
+    if (exact)
+        launch_sep_ldg_one<true>(in, in_pitch, in_image_stride, int32_t(W), int32_t(H), tg, grid, wv, wh, stream);
+    else
+        launch_sep_ldg_one<false>(in, in_pitch, in_image_stride, int32_t(W), int32_t(H), tg, grid, wv, wh, stream);
     return cudaGetLastError();
 }
 

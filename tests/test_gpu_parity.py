@@ -318,7 +318,7 @@ def test_u8_batched_and_host(cuda_ctx):
 def test_stencil_exact_bitexact(cuda_ctx, H, W, generic):
     img = synth.synth_numpy(1, H, W, seed=H * 7 + W)[0]
     got = hb.stencil3x3_sep(_dev(img), exact=True, force_generic=generic)
-    assert cuda_ctx.last_path == (_lib.PATH_GENERIC if generic or (W % 4) else _lib.PATH_TMA)
+    assert cuda_ctx.last_path == (_lib.PATH_GENERIC if generic else _lib.PATH_LDG if W % 4 else _lib.PATH_TMA)
     torch.cuda.synchronize()
     assert np.array_equal(got.cpu().numpy(), cref.sep3x3_f32(img))
 
