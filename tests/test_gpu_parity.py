@@ -579,3 +579,35 @@ def test_u8_ldg_unaligned_base_and_batch(cuda_ctx):
     assert cuda_ctx.last_path == _lib.PATH_LDG
     torch.cuda.synchronize()
     assert torch.equal(got, ref)
+
+
+def test_concurrent_streams_and_threads(cuda_ctx):
+    """One ctx driven from 4 host threads on 4 streams (ctypes drops the GIL, so the C
+    launch path and its launch cache really run concurrently); every result bit-exact."""
+    import threading
+    shapes = [(40, 136), (70, 264), (37, 71), (100, 388)]
+    imgs = [synth.synth_numpy(3, H, W, seed=17 + k) for k, (H, W) in enumerate(shapes)]
+    refs = [cref.harris_f32(x) for x in imgs]
+    devs = [_dev(x) for x in imgs]
+    streams = [torch.cuda.Stream() for _ in shapes]
+    outs = [[None] * 20 for _ in shapes]
+    errors = []
+
+    def work(k):
+        try:
+            with torch.cuda.stream(streams[k]):
+                for it in range(20):
+                    outs[k][it] = hb.harris(devs[k], exact=True, stream=streams[k])
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(len(shapes))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    torch.cuda.synchronize()
+    assert not errors, errors
+    for k in range(len(shapes)):
+        for it in range(20):
+            assert np.array_equal(outs[k][it].cpu().numpy(), refs[k]), (k, it)
