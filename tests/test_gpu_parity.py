@@ -611,3 +611,17 @@ def test_concurrent_streams_and_threads(cuda_ctx):
     for k in range(len(shapes)):
         for it in range(20):
             assert np.array_equal(outs[k][it].cpu().numpy(), refs[k]), (k, it)
+
+
+def test_host_paths_unaligned_widths(cuda_ctx):
+    """harris_run_host / harris_run_host_u8 with widths the staging buffers cannot make
+    16-byte aligned (the K2 kernels run on them), batched and banded."""
+    for shape in [(3, 37, 71), (2, 3, 60, 203)]:
+        rgb = synth.synth_numpy(int(np.prod(shape[:-2])), shape[-2], shape[-1], seed=23).reshape(shape)
+        host = hb.harris(rgb, exact=True)
+        ref = np.stack([cref.harris_f32(r) for r in rgb.reshape(-1, 3, *shape[-2:])])
+        assert np.array_equal(host.reshape(ref.shape), ref)
+    hwc, f32 = _u8_image(3, 45, 131, seed=29)
+    got = hb.harris_u8(hwc, exact=True)
+    for b in range(3):
+        assert np.array_equal(got[b], cref.harris_f32(f32[b]))
