@@ -38,6 +38,7 @@ struct harris_ctx {
     int occ_ldg[kNumLdgConfigs] = {0};
     int occ_u8ldg = 0;
     int occ_sepldg = 0;
+    int u8ldg_chunk = 16;  // HARRIS_U8LDG_CHUNK: 4 or 16-byte copies in the u8 K2 kernel
     int ldg_cfg = 2;  // HARRIS_LDG_CONFIG; 2 = scalar lane-halo core, 16 warps/SM (284 k MP/s on 8190^2)
     int sync_waves = 1;  // dev knob HARRIS_SYNC_WAVES=0 disables the per-tile CTA barrier
     int l2_policy = 1;  // evict_normal: the 4-column halo sectors are re-read by the neighbouring strip
@@ -362,7 +363,7 @@ int run(harris_ctx* ctx, const Call& c, cudaStream_t stream) {
             tg.notify_flag = c.notify_flag;
             tg.notify_epoch = c.notify_epoch;
         }
-        e = ldg ? (c.fmt == kU8Interleaved ? launch_u8_ldg(exact, c.g, tg, ent.grid, stream)
+        e = ldg ? (c.fmt == kU8Interleaved ? launch_u8_ldg(exact, ctx->u8ldg_chunk, c.g, tg, ent.grid, stream)
                                            : launch_ldg(ctx->ldg_cfg, exact, c.g, tg, ent.grid, stream))
             : c.fmt == kU8Interleaved ? launch_tma_u8(ctx->u8_cfg, exact, ent.tmap, tg, ent.grid, stream)
                                       : launch_tma(ent.cfg, exact, ent.tmap, tg, ent.grid, stream);
@@ -462,6 +463,8 @@ int harris_init(harris_ctx** out_ctx, int cuda_device) {
         int v = std::atoi(env);
         if (v >= 0 && v < kNumSepConfigs) ctx->sep_cfg = v;
     }
+    env = std::getenv("HARRIS_U8LDG_CHUNK");
+    if (env) ctx->u8ldg_chunk = std::atoi(env) == 4 ? 4 : 16;
     env = std::getenv("HARRIS_LDG_CONFIG");
     if (env) {
         int v = std::atoi(env);

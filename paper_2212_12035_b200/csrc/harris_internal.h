@@ -67,7 +67,8 @@ cudaError_t launch_ldg(int cfg, bool exact, const Geom& g, const TileGeom& tg, i
 // interleaved u8 inputs whose byte strides TMA cannot describe (3W % 16 != 0)
 extern const TmaConfig kU8LdgConfig;
 cudaError_t u8_ldg_configure(int* ctas_per_sm);
-cudaError_t launch_u8_ldg(bool exact, const Geom& g, const TileGeom& tg, int64_t grid, cudaStream_t stream);
+cudaError_t launch_u8_ldg(bool exact, int chunk, const Geom& g, const TileGeom& tg, int64_t grid,
+                          cudaStream_t stream);
 // separable stencil planes TMA cannot describe
 extern const TmaConfig kSepLdgConfig;
 cudaError_t sep_ldg_configure(int* ctas_per_sm);

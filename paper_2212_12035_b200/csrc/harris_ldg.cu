@@ -127,30 +127,35 @@ struct LdgOp : BaseOp {
 // (3W % 16 == 0); other widths get 4-byte cp.async of the row's words from its 4-byte
 // aligned-down start, and the consumer realigns each lane's 3 words with funnel shifts by
 // the row's byte skew (a running value: the op sees the tile's rows in order).
-template <bool EXACT, int CH>
+// A: copy granularity in bytes (4: 4-byte copies from the 4-byte aligned-down start; 16:
+// one 16-byte copy per lane per row from the 16-byte aligned-down start, the consumer
+// then also skips skew / 4 whole words)
+template <bool EXACT, int CH, int A>
 struct U8LdgOp : HarrisU8Op<EXACT, CH, 124> {
     using Base = HarrisU8Op<EXACT, CH, 124>;
+    static_assert(A == 4 || A == 16, "u8 K2 copy granularity");
     static constexpr bool kWarpLoad = true;
     static constexpr bool kCacheProducer = true;
-    static constexpr int kRowWords = Base::kWords;  // 100 >= 97: 96 words of 128 px + 1 for the skew
-    static constexpr int kCopyWords = 97;
+    static constexpr int kRowWords = Base::kWords;  // 100 words: 96 of 128 px + up to 15 skew bytes
+    static constexpr int kChunks = A == 4 ? 97 : 25;  // copies per row
+    static constexpr uint32_t kMask = A - 1;
     struct Params {
         float kappa;
         const uint8_t* rgb;
         int64_t in_pitch, in_image_stride;  // bytes
         int32_t W, H;                       // input pixels per row / rows per image
     };
-    uint32_t base4, pitch4, image4;  // byte address residues mod 4
-    uint32_t skew = 0;               // byte misalignment of the current row's start
+    uint32_t base_r, pitch_r, image_r;  // byte address residues mod A
+    uint32_t skew = 0;                  // misalignment (bytes, mod A) of the current row's start
 
     __device__ __forceinline__ explicit U8LdgOp(const Params& p)
         : Base(typename Base::Params{p.kappa}),
-          base4(uint32_t(reinterpret_cast<uintptr_t>(p.rgb)) & 3u),
-          pitch4(uint32_t(p.in_pitch) & 3u),
-          image4(uint32_t(p.in_image_stride) & 3u) {}
+          base_r(uint32_t(reinterpret_cast<uintptr_t>(p.rgb)) & kMask),
+          pitch_r(uint32_t(p.in_pitch) & kMask),
+          image_r(uint32_t(p.in_image_stride) & kMask) {}
 
     __device__ __forceinline__ void begin_tile(const int (&col0)[1], int row0, const int (&image)[1]) {
-        skew = (base4 + uint32_t(image[0]) * image4 + uint32_t(row0) * pitch4 + uint32_t(col0[0]) * 3u) & 3u;
+        skew = (base_r + uint32_t(image[0]) * image_r + uint32_t(row0) * pitch_r + uint32_t(col0[0]) * 3u) & kMask;
     }
 
     __device__ __forceinline__ static void load_warp(void* smem, const Params& p, uint64_t* bar,
@@ -165,14 +170,17 @@ struct U8LdgOp : HarrisU8Op<EXACT, CH, 124> {
             if (y >= p.H) continue;  // below the image: never reaches a stored output
             const uint8_t* src = img + int64_t(y) * p.in_pitch;
             const uintptr_t a = reinterpret_cast<uintptr_t>(src);
-            const uint8_t* al = reinterpret_cast<const uint8_t*>(a & ~uintptr_t(3));
-            const int avail = int(a & 3) + avail_px * 3;  // bytes from `al` to the row end
+            const uint8_t* al = reinterpret_cast<const uint8_t*>(a & ~uintptr_t(kMask));
+            const int avail = int(a & kMask) + avail_px * 3;  // bytes from `al` to the row end
             uint32_t* dst = s + r * kRowWords;
 #pragma unroll
-            for (int j = lane; j < kCopyWords; j += 32) {
-                const int v = avail - 4 * j;
-                const uint32_t nb = v >= 4 ? 4u : v > 0 ? uint32_t(v) : 0u;
-                cp_async4(dst + j, al + (nb ? 4 * j : 0), nb);
+            for (int j = lane; j < kChunks; j += 32) {
+                const int v = avail - A * j;
+                const uint32_t nb = v >= A ? uint32_t(A) : v > 0 ? uint32_t(v) : 0u;
+                if constexpr (A == 16)
+                    cp_async16(dst + 4 * j, al + (nb ? 16 * j : 0), nb);
+                else
+                    cp_async4(dst + j, al + (nb ? 4 * j : 0), nb);
             }
         }
         cp_async_mbar_arrive_noinc(bar);
@@ -180,54 +188,67 @@ struct U8LdgOp : HarrisU8Op<EXACT, CH, 124> {
 
     template <int R, int RP = R>
     __device__ __forceinline__ void row(const unsigned char* stage, int lane, float (&out)[1][4]) {
-        const uint32_t* w = reinterpret_cast<const uint32_t*>(stage) + R * kRowWords + 3 * lane;
-        const uint32_t sh = skew * 8u;
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(stage) + R * kRowWords + (skew >> 2) + 3 * lane;
+        const uint32_t sh = (skew & 3u) * 8u;
         const uint32_t w3 = w[3];
         const uint32_t a0 = __funnelshift_r(w[0], w[1], sh), a1 = __funnelshift_r(w[1], w[2], sh),
                        a2 = __funnelshift_r(w[2], w3, sh);
         float gown[4];
         gray4_u8<EXACT>(a0, a1, a2, gown[0], gown[1], gown[2], gown[3]);
         this->core.template step<R, NoHalo, (CH % 2 == 0)>(gown, lane, NoHalo{}, out[0]);
-        skew = (skew + pitch4) & 3u;
+        skew = (skew + pitch_r) & kMask;
     }
 };
 
 constexpr int kU8LdgNW = 8, kU8LdgNS = 4, kU8LdgCH = 6;
 const TmaConfig kU8LdgConfig = {kU8LdgNW, kU8LdgNS, kU8LdgCH, 1, 124};
 
-template <bool EXACT>
+template <bool EXACT, int A>
 static constexpr auto u8_ldg_kernel() {
-    return strip_kernel<U8LdgOp<EXACT, kU8LdgCH>, kU8LdgNW, kU8LdgNS, 2>;
+    return strip_kernel<U8LdgOp<EXACT, kU8LdgCH, A>, kU8LdgNW, kU8LdgNS, 2>;
 }
-static constexpr size_t u8_ldg_smem() { return StripShape<kU8LdgNW, kU8LdgNS, U8LdgOp<false, kU8LdgCH>>::kSmemBytes; }
+static constexpr size_t u8_ldg_smem() {
+    return StripShape<kU8LdgNW, kU8LdgNS, U8LdgOp<false, kU8LdgCH, 4>>::kSmemBytes;
+}
 static_assert(u8_ldg_smem() <= 227 * 1024, "u8 ldg smem");
 
-cudaError_t u8_ldg_configure(int* ctas_per_sm) {
-    cudaError_t e = cudaFuncSetAttribute(u8_ldg_kernel<false>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+template <int A>
+static cudaError_t u8_ldg_configure_one() {
+    cudaError_t e = cudaFuncSetAttribute(u8_ldg_kernel<false, A>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(u8_ldg_smem()));
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(u8_ldg_kernel<true>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+        e = cudaFuncSetAttribute(u8_ldg_kernel<true, A>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(u8_ldg_smem()));
+    return e;
+}
+
+cudaError_t u8_ldg_configure(int* ctas_per_sm) {
+    cudaError_t e = u8_ldg_configure_one<4>();
+    if (e == cudaSuccess) e = u8_ldg_configure_one<16>();
     if (e == cudaSuccess)
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, u8_ldg_kernel<false>(), kU8LdgNW * 32,
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, u8_ldg_kernel<false, 16>(), kU8LdgNW * 32,
                                                           u8_ldg_smem());
     return e;
 }
 
-cudaError_t launch_u8_ldg(bool exact, const Geom& geom, const TileGeom& tg, int64_t grid, cudaStream_t stream) {
+template <bool EXACT, int A>
+static void launch_u8_ldg_one(const Geom& geom, const TileGeom& tg, int64_t grid, cudaStream_t stream) {
     CUtensorMap unused;
     std::memset(&unused, 0, sizeof(unused));
-    const uint8_t* rgb8 = reinterpret_cast<const uint8_t*>(geom.rgb);
     const int64_t img_stride = geom.batch > 1 ? geom.in_image_stride : 0;
-    if (exact) {
-        const typename U8LdgOp<true, kU8LdgCH>::Params p{geom.kappa, rgb8, geom.in_pitch, img_stride,
-                                                         int32_t(geom.m + 4), int32_t(geom.n + 4)};
-        u8_ldg_kernel<true>()<<<unsigned(grid), unsigned(kU8LdgNW * 32), u8_ldg_smem(), stream>>>(unused, tg, p);
-    } else {
-        const typename U8LdgOp<false, kU8LdgCH>::Params p{geom.kappa, rgb8, geom.in_pitch, img_stride,
-                                                          int32_t(geom.m + 4), int32_t(geom.n + 4)};
-        u8_ldg_kernel<false>()<<<unsigned(grid), unsigned(kU8LdgNW * 32), u8_ldg_smem(), stream>>>(unused, tg, p);
-    }
+    const typename U8LdgOp<EXACT, kU8LdgCH, A>::Params p{geom.kappa, reinterpret_cast<const uint8_t*>(geom.rgb),
+                                                         geom.in_pitch, img_stride, int32_t(geom.m + 4),
+                                                         int32_t(geom.n + 4)};
+    u8_ldg_kernel<EXACT, A>()<<<unsigned(grid), unsigned(kU8LdgNW * 32), u8_ldg_smem(), stream>>>(unused, tg, p);
+}
+
+cudaError_t launch_u8_ldg(bool exact, int chunk, const Geom& geom, const TileGeom& tg, int64_t grid,
+                          cudaStream_t stream) {
+    if (chunk == 4)
+        exact ? launch_u8_ldg_one<true, 4>(geom, tg, grid, stream) : launch_u8_ldg_one<false, 4>(geom, tg, grid, stream);
+    else
+        exact ? launch_u8_ldg_one<true, 16>(geom, tg, grid, stream)
+              : launch_u8_ldg_one<false, 16>(geom, tg, grid, stream);
     return cudaGetLastError();
 }
 
