@@ -19,13 +19,13 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _torchrun(args, timeout=600):
+def _torchrun(args, timeout=600, nproc=2):
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
-           "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"), "--gpus", "2",
-           "--dist-backend", "gloo"] + args
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(nproc),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"), "--gpus",
+           str(nproc), "--dist-backend", "gloo"] + args
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout,
                        env=dict(os.environ, HARRIS_BENCH_SHARE_GPU="1"))
     assert r.returncode == 0, r.stderr[-3000:]
@@ -46,3 +46,10 @@ def test_two_rank_weak_scaling_batch():
     assert d["n_gpus"] == 2 and d["scaling"] == "weak"
     assert d["config"]["images"] == 2048 and d["config"]["images_per_gpu"] == 1024
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
+
+
+def test_four_rank_row_bands_fused_gather():
+    """4 ranks, 4 row bands of 8192^2, every band's kernel storing into rank 0's buffer."""
+    d = _torchrun(["--workload", "image8192", "--steps", "2", "--warmup", "3", "--no-e2e", "--gather", "peer"],
+                  nproc=4)
+    assert d["n_gpus"] == 4 and d["value"] > 0 and d["config"]["gather"].startswith("fused")
