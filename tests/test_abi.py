@@ -115,3 +115,15 @@ def test_peer_handle_layout_and_roundtrip():
     h.offset, h.bytes, h.device = 4096, 1 << 30, 3
     g = _lib.PeerHandle.from_bytes(h.to_bytes())
     assert bytes(g.ipc) == bytes(h.ipc) and (g.offset, g.bytes, g.device) == (4096, 1 << 30, 3)
+
+
+def test_plain_c_host_example_without_a_device():
+    """examples/harris_host.c links only the C-ABI (no CUDA headers / runtime in the app);
+    without a GPU it must fail cleanly through harris_init's error code."""
+    exe = os.path.join(ROOT, "examples", "harris_host")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-C", os.path.join(ROOT, "examples")], check=True, capture_output=True)
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present (tests/test_gpu_parity.py runs the example)")
+    r = subprocess.run([exe, "64", "136"], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 4 and "harris_init" in r.stderr

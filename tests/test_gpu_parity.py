@@ -625,3 +625,18 @@ def test_host_paths_unaligned_widths(cuda_ctx):
     got = hb.harris_u8(hwc, exact=True)
     for b in range(3):
         assert np.array_equal(got[b], cref.harris_f32(f32[b]))
+
+
+@pytest.mark.parametrize("H,W", [(1536, 2560), (37, 71)])
+def test_plain_c_host_example(cuda_ctx, H, W):
+    """The plain-C host program (examples/harris_host.c): exact order bit-identical to the
+    oracle and the default order within tolerance, through harris_run_host only."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "examples", "harris_host")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-C", os.path.join(root, "examples")], check=True, capture_output=True)
+    r = subprocess.run([exe, str(H), str(W)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "exact bit-identical" in r.stdout
