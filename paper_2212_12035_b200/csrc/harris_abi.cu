@@ -673,6 +673,7 @@ int harris_stencil3x3_sep(harris_ctx* ctx, float* out, int64_t out_pitch, int64_
         tg.l2_policy = ctx->l2_policy;
         tg.vec_store = aligned16(out) && (out_pitch & 3) == 0 && (batch == 1 || (out_image_stride & 3) == 0);
         tg.sync_waves = ctx->sync_waves;
+        if (tg.tiles > INT32_MAX) return HARRIS_ERR_SIZE;  // beyond the engine's 32-bit tile index
         e = launch_tma_sep(ctx->sep_cfg, exact, tmap, tg, grid, wv, wh, stream);
     } else {
         e = launch_generic_sep(exact, in, in_pitch, img_stride, out, out_pitch,
