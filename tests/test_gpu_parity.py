@@ -640,3 +640,15 @@ def test_plain_c_host_example(cuda_ctx, H, W):
     r = subprocess.run([exe, str(H), str(W)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "exact bit-identical" in r.stdout
+
+
+def test_host_pipeline_many_chunks(cuda_ctx):
+    """harris_run_host over more chunks than staging slots (48 MB chunks, 3 slots): a
+    large image in row bands and a batch that is not a multiple of the chunk size."""
+    rgb = synth.synth_numpy(3, 3000, 2052, seed=41)               # 74 MB -> 2 bands
+    assert np.array_equal(hb.harris(rgb), _run(rgb))
+    B = 37
+    imgs = synth.synth_numpy(3 * B, 480, 644, seed=43).reshape(B, 3, 480, 644)  # 3.7 MB each
+    host = hb.harris(imgs, exact=True)
+    for b in (0, 12, 13, 36):
+        assert np.array_equal(host[b], cref.harris_f32(imgs[b])), b
