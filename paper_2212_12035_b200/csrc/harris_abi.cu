@@ -180,12 +180,18 @@ void plan_tiles(int64_t n, int64_t m, int64_t batch, int64_t gw, int rows_per_st
         return;
     }
     const int64_t kTileOverheadRows = 6;  // pipeline/tile switch cost in row-equivalents
+    // Tiles taller than this lose more than the cost model sees: the per-tile CTA barrier
+    // re-aligns neighbouring strips less often (L2 halo reuse) and the last wave is
+    // coarser.  Measured on configs[4]: 538-row tiles 5.12-5.21 ms, 269-row 5.05-5.07 ms;
+    // 32768^2: 886-row 2.526 ms, 254-row 2.517 ms (profiles/band_rows_r01.txt).
+    const int64_t kMaxBandRows = 288;
     const int64_t max_bands = std::max<int64_t>(1, std::min<int64_t>(n, 1 + n / 8));
     int64_t best_cost = INT64_MAX, best_rows = n, best_bands = 1;
     for (int64_t nb = 1; nb <= max_bands; ++nb) {
         const int64_t rows = (n + nb - 1) / nb;
         const int64_t bands = (n + rows - 1) / rows;
         if (bands != nb) continue;  // same split as a smaller nb
+        if (rows > kMaxBandRows && nb < max_bands) continue;
         const int64_t tiles = units_per_band * bands;
         const int64_t waves = (tiles + gw - 1) / gw;
         const int64_t rows_in = ((rows + halo + rows_per_stage - 1) / rows_per_stage) * rows_per_stage;
