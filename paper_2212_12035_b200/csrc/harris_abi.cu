@@ -165,7 +165,7 @@ bool tma_eligible(const Call& c) {
 // of `gw` warps.  A tile is `groups` 128-column strips: with groups == 2 the strips
 // of one band row of all images are paired consecutively (strip_pipeline.cuh).
 void plan_tiles(int64_t n, int64_t m, int64_t batch, int64_t gw, int rows_per_stage, int64_t force_rows,
-                TileGeom& tg, int halo = 4, int groups = 1, int strip_cols = kWarpCols) {
+                TileGeom& tg, int halo = 4, int groups = 1, int strip_cols = kWarpCols, bool cap_rows = true) {
     const int64_t colsegs = (m + strip_cols - 1) / strip_cols;
     const int64_t units_per_band = groups == 2 ? (batch * colsegs + 1) / 2 : batch * colsegs;
     tg.n = int32_t(n);
@@ -180,11 +180,13 @@ void plan_tiles(int64_t n, int64_t m, int64_t batch, int64_t gw, int rows_per_st
         return;
     }
     const int64_t kTileOverheadRows = 6;  // pipeline/tile switch cost in row-equivalents
-    // Tiles taller than this lose more than the cost model sees: the per-tile CTA barrier
-    // re-aligns neighbouring strips less often (L2 halo reuse) and the last wave is
-    // coarser.  Measured on configs[4]: 538-row tiles 5.12-5.21 ms, 269-row 5.05-5.07 ms;
-    // 32768^2: 886-row 2.526 ms, 254-row 2.517 ms (profiles/band_rows_r01.txt).
-    const int64_t kMaxBandRows = 288;
+    // Tiles taller than this lose more than the cost model sees for the memory-bound ops:
+    // the per-tile CTA barrier re-aligns neighbouring strips less often (L2 halo reuse) and
+    // the last wave is coarser.  Measured on configs[4]: 538-row tiles 5.12-5.21 ms,
+    // 269-row 5.05-5.07 ms; binomial 1076-row 3.48 ms, 269-row 2.97 ms; 32768^2: 886-row
+    // 2.526 ms, 254-row 2.517 ms.  The issue-bound u8 op prefers long tiles (1076 rows
+    // 2.93-2.95 ms vs 3.03 ms capped) and plans without the cap (profiles/band_rows_r01.txt).
+    const int64_t kMaxBandRows = cap_rows ? 288 : INT64_MAX;
     const int64_t max_bands = std::max<int64_t>(1, std::min<int64_t>(n, 1 + n / 8));
     int64_t best_cost = INT64_MAX, best_rows = n, best_bands = 1;
     for (int64_t nb = 1; nb <= max_bands; ++nb) {
@@ -231,7 +233,7 @@ void plan_launch(const harris_ctx* ctx, const Call& c, TileGeom& tg, int64_t& gr
                                       : u8 ? ctx->occ_u8[ctx->u8_cfg] : ctx->occ[fcfg]);
     const int64_t resident_ctas = int64_t(ctx->num_sms) * occ;
     plan_tiles(c.g.n, c.g.m, c.g.batch, resident_ctas * cfg.warps, cfg.rows, ctx->force_band_rows, tg, 4,
-               cfg.groups, cfg.strip_cols);
+               cfg.groups, cfg.strip_cols, /*cap_rows=*/!u8);
     grid = std::min<int64_t>((tg.tiles + cfg.warps - 1) / cfg.warps, resident_ctas);
     tg.out = c.g.out;
     tg.out_pitch = c.g.out_pitch;
