@@ -174,7 +174,12 @@ def harris(rgb, kappa: float = KAPPA, *, out: Optional[torch.Tensor] = None, exa
         arr = rgb if isinstance(rgb, np.ndarray) else rgb.numpy()
         arr = np.ascontiguousarray(arr)
         dev = torch.cuda.current_device()
-        res = context(dev).run_host(arr, kappa=kappa, flags=flags)
+        host_out = None
+        if out is not None:  # a host array / CPU tensor of the output shape (pinned for full speed)
+            host_out = out if isinstance(out, np.ndarray) else out.numpy()
+        res = context(dev).run_host(arr, out=host_out, kappa=kappa, flags=flags)
+        if out is not None:
+            return out
         return res if isinstance(rgb, np.ndarray) else torch.from_numpy(res)
     B, H, W = _check_rgb(rgb)
     if rgb.stride(-1) != 1:

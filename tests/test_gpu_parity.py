@@ -652,3 +652,13 @@ def test_host_pipeline_many_chunks(cuda_ctx):
     host = hb.harris(imgs, exact=True)
     for b in (0, 12, 13, 36):
         assert np.array_equal(host[b], cref.harris_f32(imgs[b])), b
+
+
+def test_host_path_honours_out(cuda_ctx):
+    rgb = synth.synth_numpy(3, 40, 68, seed=5)
+    out = np.full((36, 64), -1.0, dtype=np.float32)
+    r = hb.harris(rgb, out=out, exact=True)
+    assert r is out and np.array_equal(out, cref.harris_f32(rgb))
+    pinned = torch.empty((36, 64), dtype=torch.float32).pin_memory()
+    r = hb.harris(torch.from_numpy(rgb), out=pinned, exact=True)
+    assert r is pinned and np.array_equal(pinned.numpy(), cref.harris_f32(rgb))
