@@ -262,6 +262,18 @@ struct HarrisF32x2Op {
             make_float2(gray_of<EXACT>(ra.w, ga.w, ba.w), gray_of<EXACT>(rb.w, gb.w, bb.w))};
         if constexpr (L::kLaneHalo) {
             core.template step<R>(gown, lane, NoHalo{}, out);
+        } else if (adjacent) {
+            float hA[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) hA[k] = __shfl_sync(0xffffffffu, gown[k].y, 0);
+            core.template step<R>(gown, lane, [&](float2& h0, float2& h1, float2& h2, float2& h3) {
+                const float4 r2b = lds128(b + o_r + kWarpCols), g2b = lds128(b + o_g + kWarpCols),
+                             b2b = lds128(b + o_b + kWarpCols);
+                h0 = make_float2(hA[0], gray_of<EXACT>(r2b.x, g2b.x, b2b.x));
+                h1 = make_float2(hA[1], gray_of<EXACT>(r2b.y, g2b.y, b2b.y));
+                h2 = make_float2(hA[2], gray_of<EXACT>(r2b.z, g2b.z, b2b.z));
+                h3 = make_float2(hA[3], gray_of<EXACT>(r2b.w, g2b.w, b2b.w));
+            }, out);
         } else {
             core.template step<R>(gown, lane, [&](float2& h0, float2& h1, float2& h2, float2& h3) {
                 const float4 r2a = lds128(a + o_r + kWarpCols), g2a = lds128(a + o_g + kWarpCols),
@@ -274,6 +286,11 @@ struct HarrisF32x2Op {
                 h3 = make_float2(gray_of<EXACT>(r2a.w, g2a.w, b2a.w), gray_of<EXACT>(r2b.w, g2b.w, b2b.w));
             }, out);
         }
+    }
+
+    bool adjacent = false;  // strip B is strip A + 1 of the same image (per tile)
+    __device__ __forceinline__ void begin_tile(const int (&col0)[2], int, const int (&image)[2]) {
+        adjacent = image[0] == image[1] && col0[1] == col0[0] + SC;
     }
 };
 

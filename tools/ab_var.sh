@@ -8,7 +8,7 @@ for i in 1 2; do
       python -c "
 import json
 d=json.loads(open('gpurun_out/var_tmp.txt').read().strip().splitlines()[-1]); ms=d['ms']
-print('$v cfg$c', 'first5', round(sum(ms[:5])/5,3), 'last20', round(sum(ms[-20:])/20,3), 'min', min(ms), 'sm', d['sm_mhz'][-3:], d.get('reasons_or'))"
+print('$v cfg$c', 'bench-window(3:23)', round(sum(ms[3:23])/20,3), 'first5', round(sum(ms[:5])/5,3), 'last20', round(sum(ms[-20:])/20,3), 'min', min(ms), 'sm', d['sm_mhz'][-3:], d.get('reasons_or'))"
     done
   done
 done
