@@ -79,9 +79,11 @@ cudaError_t launch_sep_ldg(bool exact, const float* in, int64_t in_pitch, int64_
 // interleaved RGB u8 (HWC) input: TMA configs + generic fallback (Geom.rgb is then the
 // byte base pointer; in_pitch / in_image_stride are in BYTES, in_chan_stride unused)
 constexpr int kNumU8Configs = 7;
-// 124-column lane-halo strips, scalar core, 16 warps/SM: the u8 op is issue-bound and the
-// halo branch was ~17 % of its instructions (510 k -> 585 k MP/s on configs[4] as u8)
-constexpr int kDefaultU8Config = 5;
+// 124-column lane-halo strips: the u8 op is issue-bound and the halo branch was ~17 % of
+// its instructions.  Config 6 = the packed dual-strip core in that layout (Sobel sharing,
+// producer tile cache): 745.6 k vs 717.8 k MP/s for the scalar core at 16 warps/SM (config 5)
+// on configs[4] as u8 (10 launches after 3 warm-ups, 3 alternations)
+constexpr int kDefaultU8Config = 6;
 extern const TmaConfig kU8Configs[kNumU8Configs];
 size_t u8_smem_bytes(int cfg);
 cudaError_t u8_configure(int cfg);
