@@ -53,3 +53,11 @@ def test_four_rank_row_bands_fused_gather():
     d = _torchrun(["--workload", "image8192", "--steps", "2", "--warmup", "3", "--no-e2e", "--gather", "peer"],
                   nproc=4)
     assert d["n_gpus"] == 4 and d["value"] > 0 and d["config"]["gather"].startswith("fused")
+
+
+def test_eight_rank_row_bands_fused_gather():
+    """The N = 8 decomposition of the scaling run (8 row bands, 8 peer mappings of rank 0's
+    buffer, 8 completion flags), as 8 processes on the one GPU."""
+    d = _torchrun(["--workload", "image8192", "--steps", "2", "--warmup", "3", "--no-e2e", "--gather", "peer"],
+                  nproc=8, timeout=900)
+    assert d["n_gpus"] == 8 and d["value"] > 0 and d["config"]["gather"].startswith("fused")
