@@ -546,9 +546,12 @@ def run_extra(a, ctx, dev) -> dict:
         scratch2.sum()
 
     # the thesis does not state the 1536x2560 orientation: time both
-    for name, flushed in (("image8192", False), ("image1536", True), ("image1536T", True)):
-        wl = WORKLOADS[name] if name in WORKLOADS else dict(WORKLOADS["image1536"], H=2560, W=1536,
-                                                             desc="configs[1] transposed: 2560x1536 RGB f32")
+    # and the thesis's second evaluation image, 4256x2832
+    more = {"image1536T": dict(WORKLOADS["image1536"], H=2560, W=1536, desc="configs[1] transposed: 2560x1536 RGB f32"),
+            "image4256": dict(WORKLOADS["image1536"], H=2832, W=4256,
+                              desc="4256x2832 RGB f32 (the thesis's second evaluation image size)")}
+    for name, flushed in (("image8192", False), ("image1536", True), ("image1536T", True), ("image4256", True)):
+        wl = WORKLOADS[name] if name in WORKLOADS else more[name]
         H, W = wl["H"], wl["W"]
         x = torch.empty((3, H, W), device=dev)
         hb.synth_(x, seed=SEED)
