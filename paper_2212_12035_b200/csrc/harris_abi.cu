@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <atomic>
 #include <mutex>
 #include <cstdio>
 #include <cstdlib>
@@ -46,7 +47,7 @@ struct harris_ctx {
     CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;  // dev knob HARRIS_L2_PROMO
     int occ[kNumTmaConfigs] = {0};
     PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-    int last_path = HARRIS_PATH_NONE;
+    std::atomic<int> last_path{HARRIS_PATH_NONE};  // diagnostic; calls may race on different streams
     char last_err[256] = {0};
     // host-buffer pipeline (harris_run_host)
     static constexpr int kSlots = 3;
@@ -724,7 +725,7 @@ int harris_plan(harris_ctx* ctx, int64_t n, int64_t m, int64_t batch, const floa
     return HARRIS_OK;
 }
 
-int harris_last_path(const harris_ctx* ctx) { return ctx ? ctx->last_path : HARRIS_PATH_NONE; }
+int harris_last_path(const harris_ctx* ctx) { return ctx ? ctx->last_path.load() : HARRIS_PATH_NONE; }
 int harris_device(const harris_ctx* ctx) { return ctx ? ctx->device : -1; }
 int harris_num_sms(const harris_ctx* ctx) { return ctx ? ctx->num_sms : 0; }
 const char* harris_last_cuda_error(const harris_ctx* ctx) { return ctx ? ctx->last_err : ""; }
