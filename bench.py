@@ -296,6 +296,24 @@ def opencv_baseline(wl: dict, images: int = 2) -> dict:
         return {"error": repr(e)}
 
 
+def cpu_oracle_configs(seconds: float = 2.0) -> dict:
+    """The CPU restatement (all host threads) on the other single-image configs, for the
+    per-config GPU/CPU comparison SURVEY.md §8(d) asks for (bounded: ~2 s each)."""
+    try:
+        from oracle import cref
+        res = {}
+        for name, (H, W) in (("configs[0] 512x512", (512, 512)), ("configs[1] 1536x2560", (1536, 2560)),
+                             ("configs[2] 8192x8192", (8192, 8192))):
+            x = cref.synth(3, H, W, seed=SEED).reshape(1, 3, H, W)
+            cpu_time(x, os.cpu_count() or 1, 0.3)  # warm the thread pool / clocks first
+            per, k = cpu_time(x, os.cpu_count() or 1, seconds)
+            res[name] = {"value": (H - 4) * (W - 4) / per / 1e6, "unit": "MP/s", "passes": k}
+        res["cores"] = os.cpu_count() or 1
+        return res
+    except Exception as e:  # informational only
+        return {"error": repr(e)}
+
+
 def cpu_model() -> str:
     try:
         for line in open("/proc/cpuinfo"):
@@ -406,6 +424,7 @@ def run_gpu(a, world, rank, local) -> dict | None:
         cpu = cpu_baseline(a.workload, wl, a.cpu_seconds)
         if not a.no_extra:
             extra["cpu_opencv"] = opencv_baseline(wl)
+            extra["cpu_oracle_configs"] = cpu_oracle_configs()
     if rank != 0:
         return None
     return {
