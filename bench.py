@@ -702,6 +702,11 @@ def run_reference(a, world, rank) -> dict | None:
     outb = np.empty((x.shape[0], x.shape[2] - 4, x.shape[3] - 4), dtype=np.float32)
     for _ in range(a.warmup):
         cref.harris_f32_batched(x, nthreads=threads, out=outb)
+    # the first ~0.5 s of OpenMP work in a fresh process runs far slower (thread pool /
+    # clock ramp): keep warming until a full second has passed so the arm is not understated
+    tw = time.perf_counter()
+    while time.perf_counter() - tw < 1.0:
+        cref.harris_f32_batched(x, nthreads=threads, out=outb)
     t0 = time.perf_counter()
     for _ in range(a.steps):
         cref.harris_f32_batched(x, nthreads=threads, out=outb)
