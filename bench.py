@@ -265,6 +265,7 @@ def cpu_baseline(wl_name: str, wl: dict, min_seconds: float = 10.0) -> dict:
         x, px, desc = cpu_sample(wl, images=16, rows=None)
     else:
         x, px, desc = cpu_sample(wl, images=1, rows=max(64, (32 << 20) // (12 * wl["W"])))
+    cpu_time(x, threads, 1.0)  # warm the OpenMP pool / clocks (a cold start runs far slower)
     per, k = cpu_time(x, threads, min_seconds)
     return {"value": px / per / 1e6, "unit": "MP/s", "cores": threads, "kind": "port",
             "sample": f"{desc}, repeated {k}x over {per * k:.1f} s; oracle/harris_oracle.c f32 "
