@@ -67,6 +67,8 @@ extern "C" {
 #define HARRIS_PATH_NONE    0
 #define HARRIS_PATH_TMA     1  /* K1: TMA-staged warp-strip kernel (W%4==0, aligned) */
 #define HARRIS_PATH_GENERIC 2  /* K0: shared-memory tile kernel (any W, any pitch)   */
+#define HARRIS_PATH_PAIR    4  /* K1p: TMA over pairs of rows, for f32 whose row pitch is 2 (mod 4)
+                                      floats (e.g. 1918 or 8190 wide) with 16-byte aligned planes */
 #define HARRIS_PATH_LDG     3  /* K2: the TMA kernel's engine with cp.async stage fills, for
                                       inputs whose strides / base TMA cannot describe (f32 with
                                       W % 4 != 0 or a 4-byte aligned base; u8 with 3W % 16 != 0) */

@@ -38,6 +38,7 @@ struct harris_ctx {
     int occ_u8[kNumU8Configs] = {0};
     int occ_ldg[kNumLdgConfigs] = {0};
     int occ_u8ldg = 0;
+    int occ_pair = 0;
     int occ_sepldg = 0;
     int u8ldg_chunk = 16;  // HARRIS_U8LDG_CHUNK: 4 or 16-byte copies in the u8 K2 kernel
     int ldg_cfg = 2;  // HARRIS_LDG_CONFIG; 2 = scalar lane-halo core, 16 warps/SM (284 k MP/s on 8190^2)
@@ -114,6 +115,7 @@ struct Call {
     uint32_t notify_epoch = 0;
     int cfg = -1;  // f32 TMA configuration chosen for this call (resolve_cfg)
     bool ldg = false;  // plan for the cp.async (LDG) kernel
+    bool pair = false;  // plan for the pair-row TMA kernel
 };
 
 int validate(const Call& c) {
@@ -166,7 +168,8 @@ bool tma_eligible(const Call& c) {
 // of `gw` warps.  A tile is `groups` 128-column strips: with groups == 2 the strips
 // of one band row of all images are paired consecutively (strip_pipeline.cuh).
 void plan_tiles(int64_t n, int64_t m, int64_t batch, int64_t gw, int rows_per_stage, int64_t force_rows,
-                TileGeom& tg, int halo = 4, int groups = 1, int strip_cols = kWarpCols, bool cap_rows = true) {
+                TileGeom& tg, int halo = 4, int groups = 1, int strip_cols = kWarpCols, bool cap_rows = true,
+                int row_align = 1) {
     const int64_t colsegs = (m + strip_cols - 1) / strip_cols;
     const int64_t units_per_band = groups == 2 ? (batch * colsegs + 1) / 2 : batch * colsegs;
     tg.n = int32_t(n);
@@ -174,7 +177,7 @@ void plan_tiles(int64_t n, int64_t m, int64_t batch, int64_t gw, int rows_per_st
     tg.colsegs = int32_t(colsegs);
     tg.batch = int32_t(batch);
     if (force_rows > 0) {
-        const int64_t rows = std::min(force_rows, n);
+        const int64_t rows = std::min((force_rows + row_align - 1) / row_align * row_align, n);
         tg.band_rows = int32_t(rows);
         tg.bands = int32_t((n + rows - 1) / rows);
         tg.tiles = units_per_band * tg.bands;
@@ -191,7 +194,7 @@ void plan_tiles(int64_t n, int64_t m, int64_t batch, int64_t gw, int rows_per_st
     const int64_t max_bands = std::max<int64_t>(1, std::min<int64_t>(n, 1 + n / 8));
     int64_t best_cost = INT64_MAX, best_rows = n, best_bands = 1;
     for (int64_t nb = 1; nb <= max_bands; ++nb) {
-        const int64_t rows = (n + nb - 1) / nb;
+        const int64_t rows = ((n + nb - 1) / nb + row_align - 1) / row_align * row_align;
         const int64_t bands = (n + rows - 1) / rows;
         if (bands != nb) continue;  // same split as a smaller nb
         if (rows > kMaxBandRows && nb < max_bands) continue;
@@ -219,22 +222,39 @@ bool ldg_eligible(const Call& c) {
     return g.n + 4 <= INT32_MAX && g.m + 4 <= INT32_MAX;
 }
 
+// planar f32 whose row pitch is 2 (mod 4) floats: pairs of rows are 16-byte multiples, so a
+// tensor map over pair-rows serves it (HarrisF32PairRowOp).  Needs 16-byte aligned planes
+// and an even image height (the last pair-row of the last plane must not run past it).
+bool pair_eligible(const Call& c) {
+    const Geom& g = c.g;
+    if (c.fmt != kF32Planar || !aligned16(g.rgb)) return false;
+    if ((g.in_pitch & 3) != 2 || (g.in_chan_stride & 3) || ((g.n + 4) & 1)) return false;
+    if (g.batch > 1 && (g.in_image_stride & 3)) return false;
+    if (2 * g.in_pitch > INT32_MAX || g.batch > INT32_MAX) return false;
+    return g.batch * ((g.m + 123) / 124) < (int64_t(1) << 30);
+}
+
 int choose_path(const Call& c) {
     if (c.flags & HARRIS_FLAG_FORCE_GENERIC) return HARRIS_PATH_GENERIC;
     if (tma_eligible(c)) return HARRIS_PATH_TMA;
+    if (pair_eligible(c)) return HARRIS_PATH_PAIR;
     return ldg_eligible(c) ? HARRIS_PATH_LDG : HARRIS_PATH_GENERIC;
 }
 
 void plan_launch(const harris_ctx* ctx, const Call& c, TileGeom& tg, int64_t& grid) {
     const bool u8 = c.fmt == kU8Interleaved;
     const int fcfg = c.cfg >= 0 ? c.cfg : ctx->tma_cfg;
-    const TmaConfig& cfg = c.ldg ? (u8 ? kU8LdgConfig : kLdgConfigs[ctx->ldg_cfg])
-                                 : u8 ? kU8Configs[ctx->u8_cfg] : kTmaConfigs[fcfg];
-    const int occ = std::max(1, c.ldg ? (u8 ? ctx->occ_u8ldg : ctx->occ_ldg[ctx->ldg_cfg])
-                                      : u8 ? ctx->occ_u8[ctx->u8_cfg] : ctx->occ[fcfg]);
+    const TmaConfig& cfg = c.pair  ? kPairConfig
+                           : c.ldg ? (u8 ? kU8LdgConfig : kLdgConfigs[ctx->ldg_cfg])
+                           : u8    ? kU8Configs[ctx->u8_cfg]
+                                   : kTmaConfigs[fcfg];
+    const int occ = std::max(1, c.pair  ? ctx->occ_pair
+                                : c.ldg ? (u8 ? ctx->occ_u8ldg : ctx->occ_ldg[ctx->ldg_cfg])
+                                : u8    ? ctx->occ_u8[ctx->u8_cfg]
+                                        : ctx->occ[fcfg]);
     const int64_t resident_ctas = int64_t(ctx->num_sms) * occ;
     plan_tiles(c.g.n, c.g.m, c.g.batch, resident_ctas * cfg.warps, cfg.rows, ctx->force_band_rows, tg, 4,
-               cfg.groups, cfg.strip_cols, /*cap_rows=*/!u8);
+               cfg.groups, cfg.strip_cols, /*cap_rows=*/!u8, /*row_align=*/c.pair ? 2 : 1);
     grid = std::min<int64_t>((tg.tiles + cfg.warps - 1) / cfg.warps, resident_ctas);
     tg.out = c.g.out;
     tg.out_pitch = c.g.out_pitch;
@@ -280,8 +300,29 @@ int encode_tmap_u8(harris_ctx* ctx, const Call& c, CUtensorMap* tmap) {
     return HARRIS_OK;
 }
 
+// pair-row view of planar f32 with pitch P = 2 (mod 4): {2P columns, H/2 pair-rows, 3, B}
+int encode_tmap_pair(harris_ctx* ctx, const Call& c, CUtensorMap* tmap) {
+    const Geom& g = c.g;
+    cuuint64_t dims[4] = {cuuint64_t(2 * g.in_pitch), cuuint64_t((g.n + 4) / 2), 3, cuuint64_t(g.batch)};
+    const int64_t img_stride = g.batch > 1 ? g.in_image_stride : 3 * g.in_chan_stride;
+    cuuint64_t strides[3] = {cuuint64_t(2 * g.in_pitch) * 4, cuuint64_t(g.in_chan_stride) * 4,
+                             cuuint64_t(img_stride) * 4};
+    cuuint32_t box[4] = {132, 3, 3, 1};  // HarrisF32PairRowOp::kRow
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = ctx->encode(tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(g.rgb), dims, strides, box,
+                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, ctx->promo,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        std::snprintf(ctx->last_err, sizeof(ctx->last_err), "cuTensorMapEncodeTiled (pair) failed (CUresult %d)",
+                      int(r));
+        return HARRIS_ERR_TMA;
+    }
+    return HARRIS_OK;
+}
+
 int encode_tmap(harris_ctx* ctx, const Call& c, CUtensorMap* tmap) {
     if (c.fmt == kU8Interleaved) return encode_tmap_u8(ctx, c, tmap);
+    if (c.pair) return encode_tmap_pair(ctx, c, tmap);
     const Geom& g = c.g;
     const TmaConfig& cfg = kTmaConfigs[c.cfg >= 0 ? c.cfg : ctx->tma_cfg];
     cuuint64_t dims[4] = {cuuint64_t(g.m + 4), cuuint64_t(g.n + 4), 3, cuuint64_t(g.batch)};
@@ -350,14 +391,16 @@ int run(harris_ctx* ctx, const Call& c, cudaStream_t stream) {
     DeviceGuard guard(ctx->device);
     if (!guard.ok) return cuda_fail(ctx, cudaGetLastError(), "cudaSetDevice");
     cudaError_t e;
-    if (path == HARRIS_PATH_TMA || path == HARRIS_PATH_LDG) {
+    if (path == HARRIS_PATH_TMA || path == HARRIS_PATH_LDG || path == HARRIS_PATH_PAIR) {
         const bool ldg = path == HARRIS_PATH_LDG;
+        const bool pair = path == HARRIS_PATH_PAIR;
         harris_ctx::LaunchEntry ent;
         if (!cache_lookup(ctx, c, ent)) {
             Call cc = c;
             cc.ldg = ldg;
+            cc.pair = pair;
             if (!ldg) {
-                cc.cfg = resolve_cfg(ctx, c);
+                cc.cfg = pair ? 0 : resolve_cfg(ctx, c);
                 rc = encode_tmap(ctx, cc, &ent.tmap);
                 if (rc) return rc;
             }
@@ -372,8 +415,9 @@ int run(harris_ctx* ctx, const Call& c, cudaStream_t stream) {
             tg.notify_flag = c.notify_flag;
             tg.notify_epoch = c.notify_epoch;
         }
-        e = ldg ? (c.fmt == kU8Interleaved ? launch_u8_ldg(exact, ctx->u8ldg_chunk, c.g, tg, ent.grid, stream)
-                                           : launch_ldg(ctx->ldg_cfg, exact, c.g, tg, ent.grid, stream))
+        e = pair ? launch_tma_pair(exact, ent.tmap, tg, ent.grid, int32_t(c.g.in_pitch), stream)
+            : ldg ? (c.fmt == kU8Interleaved ? launch_u8_ldg(exact, ctx->u8ldg_chunk, c.g, tg, ent.grid, stream)
+                                             : launch_ldg(ctx->ldg_cfg, exact, c.g, tg, ent.grid, stream))
             : c.fmt == kU8Interleaved ? launch_tma_u8(ctx->u8_cfg, exact, ent.tmap, tg, ent.grid, stream)
                                       : launch_tma(ent.cfg, exact, ent.tmap, tg, ent.grid, stream);
     } else {
@@ -381,8 +425,10 @@ int run(harris_ctx* ctx, const Call& c, cudaStream_t stream) {
         if (e == cudaSuccess && c.notify_flag) e = launch_peer_signal(c.notify_flag, c.notify_epoch, stream);
     }
     if (e != cudaSuccess)
-        return cuda_fail(ctx, e, path == HARRIS_PATH_TMA ? "launch tma" : path == HARRIS_PATH_LDG ? "launch ldg"
-                                                                                              : "launch generic");
+        return cuda_fail(ctx, e, path == HARRIS_PATH_TMA    ? "launch tma"
+                                 : path == HARRIS_PATH_PAIR ? "launch tma pair"
+                                 : path == HARRIS_PATH_LDG  ? "launch ldg"
+                                                            : "launch generic");
     ctx->last_path = path;
     return HARRIS_OK;
 }
@@ -513,7 +559,8 @@ int harris_init(harris_ctx** out_ctx, int cuda_device) {
             return rc;
         }
     }
-    e = sep_ldg_configure(&ctx->occ_sepldg);
+    e = pair_configure(&ctx->occ_pair);
+    if (e == cudaSuccess) e = sep_ldg_configure(&ctx->occ_sepldg);
     if (e == cudaSuccess) e = u8_ldg_configure(&ctx->occ_u8ldg);
     if (e != cudaSuccess) {
         int rc = cuda_fail(ctx, e, "configure u8 ldg kernel");
@@ -705,8 +752,9 @@ int harris_plan(harris_ctx* ctx, int64_t n, int64_t m, int64_t batch, const floa
     std::memset(info, 0, sizeof(*info));
     info->path = choose_path(c);
     c.ldg = info->path == HARRIS_PATH_LDG;
-    c.cfg = c.ldg ? -1 : resolve_cfg(ctx, c);
-    const TmaConfig& cfg = c.ldg ? kLdgConfigs[ctx->ldg_cfg] : kTmaConfigs[c.cfg];
+    c.pair = info->path == HARRIS_PATH_PAIR;
+    c.cfg = (c.ldg || c.pair) ? -1 : resolve_cfg(ctx, c);
+    const TmaConfig& cfg = c.pair ? kPairConfig : c.ldg ? kLdgConfigs[ctx->ldg_cfg] : kTmaConfigs[c.cfg];
     info->warps_per_cta = cfg.warps;
     info->stages = cfg.stages;
     info->rows_per_stage = cfg.rows;
@@ -718,7 +766,7 @@ int harris_plan(harris_ctx* ctx, int64_t n, int64_t m, int64_t batch, const floa
     info->col_segments = tg.colsegs;
     info->tiles = tg.tiles;
     info->grid_ctas = grid;
-    info->smem_bytes = c.ldg ? 0 : int64_t(tma_smem_bytes(c.cfg));
+    info->smem_bytes = (c.ldg || c.pair) ? 0 : int64_t(tma_smem_bytes(c.cfg));
     info->groups = cfg.groups;
     info->tma_config = c.cfg;  // -1: the LDG kernel
     info->strip_cols = cfg.strip_cols;

@@ -128,6 +128,11 @@ __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
 
 // plain C++ load (ordered after mbar_wait's "memory" clobber, free to schedule
 // otherwise); p must be 16-byte aligned shared memory
+__device__ __forceinline__ float2 lds64(const float* p) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(smem_u32(p)));
+    return v;
+}
 __device__ __forceinline__ float4 lds128(const float* p) {
     return *reinterpret_cast<const float4*>(p);
 }

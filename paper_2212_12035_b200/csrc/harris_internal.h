@@ -58,6 +58,12 @@ cudaError_t launch_tma(int cfg, bool exact, const CUtensorMap& tmap, const TileG
 
 cudaError_t launch_generic(bool exact, const Geom& g, cudaStream_t stream);
 
+// pair-row TMA kernel for planar f32 whose row pitch is 2 (mod 4) floats (HarrisF32PairRowOp)
+extern const TmaConfig kPairConfig;
+cudaError_t pair_configure(int* ctas_per_sm);
+cudaError_t launch_tma_pair(bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid, int32_t pitch,
+                            cudaStream_t stream);
+
 // cp.async (LDGSTS) warp-strip kernel for f32 inputs TMA cannot describe (row pitch or
 // base not 16-byte aligned): same engine and dual-strip core as the TMA path
 constexpr int kNumLdgConfigs = 3;

@@ -252,6 +252,61 @@ struct HarrisF32Op {
     }
 };
 
+// ------------------------------------- planar f32 with row pitch = 2 (mod 4) floats
+// Row starts alternate between 16-byte aligned and 8-byte aligned, so TMA cannot address
+// single rows — but a PAIR of rows (2P floats) is a 16-byte multiple.  The tensor map views
+// each plane as H/2 pair-rows of 2P floats: image row 2j is pair-row j at column x, row
+// 2j+1 is pair-row j at column P + x.  A stage of CH = 6 image rows is two boxes of 3
+// pair-rows each.  TMA box starts must be 16-byte aligned, so the odd rows' box starts 2
+// floats early (P + x0 - 2) and the consumer reads them 2 floats in, with 8-byte loads.
+// Scalar lane-halo core (124-column strips), vertical box sums on row pairs.
+template <bool EXACT>
+struct HarrisF32PairRowOp : HarrisF32Op<EXACT, 6, 124> {
+    using Base = HarrisF32Op<EXACT, 6, 124>;
+    static constexpr int CH = 6;
+    static constexpr int kRow = 132;                                   // box width (16-byte multiple)
+    static constexpr uint32_t kBoxBytes = 3u * 3u * kRow * 4u;         // 3 channels x 3 pair-rows
+    static constexpr uint32_t kBoxStride = (kBoxBytes + 127u) / 128u * 128u;  // TMA destinations: 128-B aligned
+    static constexpr uint32_t kTxBytes = 2u * kBoxBytes;
+    static constexpr uint32_t kStageBytes = 2u * kBoxStride;
+    struct Params {
+        float kappa;
+        int32_t pitch;  // P: the odd rows' column offset inside a pair-row
+    };
+    __device__ __forceinline__ explicit HarrisF32PairRowOp(const Params& p) : Base(typename Base::Params{p.kappa}) {}
+
+    __device__ __forceinline__ static void load_p(void* smem, const CUtensorMap* tmap, uint64_t* bar,
+                                                  const int (&col0)[1], int row0, const int (&image)[1],
+                                                  uint64_t policy, const Params& p) {
+        const int j0 = row0 >> 1;  // row0 is even: tiles start at even rows (planner)
+        tma_load_4d(smem, tmap, bar, col0[0], j0, 0, image[0], policy);
+        tma_load_4d(static_cast<unsigned char*>(smem) + kBoxStride, tmap, bar, p.pitch + col0[0] - 2, j0, 0,
+                    image[0], policy);
+    }
+
+    template <int R>
+    __device__ __forceinline__ void row(const unsigned char* stage, int lane, float (&out)[1][4]) {
+        // row R of the stage: parity box R & 1, pair-row R >> 1
+        const float* sm = reinterpret_cast<const float*>(stage + (R & 1) * kBoxStride);
+        constexpr int rr = R >> 1;
+        float c[3][4];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+            const float* q = sm + (ch * 3 + rr) * kRow + 4 * lane;
+            if constexpr ((R & 1) == 0) {
+                const float4 v = lds128(q);
+                c[ch][0] = v.x, c[ch][1] = v.y, c[ch][2] = v.z, c[ch][3] = v.w;
+            } else {  // odd rows sit 2 floats into their box
+                const float2 v0 = lds64(q + 2), v1 = lds64(q + 4);
+                c[ch][0] = v0.x, c[ch][1] = v0.y, c[ch][2] = v1.x, c[ch][3] = v1.y;
+            }
+        }
+        const float gown[4] = {gray_of<EXACT>(c[0][0], c[1][0], c[2][0]), gray_of<EXACT>(c[0][1], c[1][1], c[2][1]),
+                               gray_of<EXACT>(c[0][2], c[1][2], c[2][2]), gray_of<EXACT>(c[0][3], c[1][3], c[2][3])};
+        this->core.template step<R, NoHalo, true>(gown, lane, NoHalo{}, out[0]);
+    }
+};
+
 // --------------------------------------------------- interleaved RGB u8 (HWC)
 // byte k of w as an exact float: 0x4B0000bb is 2^23 + b, minus 2^23 (PRMT + FADD)
 __device__ __forceinline__ float u8f(uint32_t w, int k) {

@@ -180,4 +180,38 @@ cudaError_t launch_tma(int cfg, bool exact, const CUtensorMap& tmap, const TileG
     return cudaErrorInvalidValue;
 }
 
+// ---- pair-row TMA kernel (row pitch = 2 mod 4 floats, HarrisF32PairRowOp) ----
+constexpr int kPairNW = 8, kPairNS = 2;
+const TmaConfig kPairConfig = {kPairNW, kPairNS, 6, 1, 124};
+
+template <bool EXACT>
+static constexpr auto pair_kernel() {
+    return strip_kernel<HarrisF32PairRowOp<EXACT>, kPairNW, kPairNS, 1>;
+}
+static constexpr size_t pair_smem() { return StripShape<kPairNW, kPairNS, HarrisF32PairRowOp<false>>::kSmemBytes; }
+static_assert(pair_smem() <= 227 * 1024, "pair-row config exceeds 227 KB of shared memory");
+
+cudaError_t pair_configure(int* ctas_per_sm) {
+    cudaError_t e = cudaFuncSetAttribute(pair_kernel<false>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(pair_smem()));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(pair_kernel<true>(), cudaFuncAttributeMaxDynamicSharedMemorySize, int(pair_smem()));
+    if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, pair_kernel<false>(), kPairNW * 32,
+                                                          pair_smem());
+    return e;
+}
+
+cudaError_t launch_tma_pair(bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid, int32_t pitch,
+                            cudaStream_t stream) {
+    const dim3 block{unsigned(kPairNW * 32)}, gridd{unsigned(grid)};
+    if (exact)
+        pair_kernel<true>()<<<gridd, block, pair_smem(), stream>>>(tmap, tg,
+                                                                  typename HarrisF32PairRowOp<true>::Params{tg.kappa, pitch});
+    else
+        pair_kernel<false>()<<<gridd, block, pair_smem(), stream>>>(
+            tmap, tg, typename HarrisF32PairRowOp<false>::Params{tg.kappa, pitch});
+    return cudaGetLastError();
+}
+
 }  // namespace harris

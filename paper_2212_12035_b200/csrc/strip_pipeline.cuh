@@ -100,6 +100,13 @@ struct WarpLoadOf : std::false_type {};
 template <class Op>
 struct WarpLoadOf<Op, std::void_t<decltype(Op::kWarpLoad)>> : std::integral_constant<bool, Op::kWarpLoad> {};
 
+// Op::load_p(smem, tmap, bar, cols, row0, imgs, policy, params) is optional: a TMA stage fill
+// that needs the kernel parameters (the pair-row op's odd-row column offset)
+template <class Op, class = void>
+struct HasLoadP : std::false_type {};
+template <class Op>
+struct HasLoadP<Op, std::void_t<decltype(&Op::load_p)>> : std::true_type {};
+
 // Op::kCacheProducer is optional (default true): decode the producer's tile once per tile
 template <class Op, class = void>
 struct CacheProducerOf : std::true_type {};
@@ -208,7 +215,12 @@ __global__ void __launch_bounds__(NW * 32, MINB)
             } else if (lane == 0) {
                 if constexpr (kCacheP) {
                     mbar_arrive_expect_tx(&bars[s], Op::kTxBytes);
-                    Op::load(ring + s * Op::kStageBytes, &tmap, &bars[s], pcols, prow0 + pc * CH, pimgs, policy);
+                    if constexpr (HasLoadP<Op>::value)
+                        Op::load_p(ring + s * Op::kStageBytes, &tmap, &bars[s], pcols, prow0 + pc * CH, pimgs,
+                                   policy, p);
+                    else
+                        Op::load(ring + s * Op::kStageBytes, &tmap, &bars[s], pcols, prow0 + pc * CH, pimgs,
+                                 policy);
                 } else {
                     const TileCoord<G> c = decode_tile<G>(pt, g);
                     int cols[G], imgs[G];

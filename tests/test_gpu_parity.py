@@ -482,7 +482,8 @@ def test_ldg_exact_bitexact(cuda_ctx, H, W):
     fills runs, bit-identical to the C oracle in EXACT order, within tolerance in FAST."""
     rgb = synth.synth_numpy(3, H, W, seed=H * 31 + W)
     got = _run(rgb, exact=True)
-    assert cuda_ctx.last_path == _lib.PATH_LDG
+    pair = W % 4 == 2 and H % 2 == 0 and (H * W) % 4 == 0
+    assert cuda_ctx.last_path == (_lib.PATH_PAIR if pair else _lib.PATH_LDG)
     assert np.array_equal(got, cref.harris_f32(rgb))
     ok, m = synth.within_tolerance(_run(rgb), cref.harris_f64(rgb))
     assert ok, m
@@ -662,3 +663,44 @@ def test_host_path_honours_out(cuda_ctx):
     pinned = torch.empty((36, 64), dtype=torch.float32).pin_memory()
     r = hb.harris(torch.from_numpy(rgb), out=pinned, exact=True)
     assert r is pinned and np.array_equal(pinned.numpy(), cref.harris_f32(rgb))
+
+
+
+# ------------------------------- K1p: TMA over pairs of rows (row pitch = 2 mod 4 floats)
+@pytest.mark.parametrize("H,W", [(6, 10), (40, 130), (70, 266), (300, 1918), (132, 518), (1082, 1922)])
+def test_pair_row_tma_bitexact(cuda_ctx, H, W):
+    rgb = synth.synth_numpy(3, H, W, seed=H * 7 + W)
+    got = _run(rgb, exact=True)
+    assert cuda_ctx.last_path == _lib.PATH_PAIR
+    assert np.array_equal(got, cref.harris_f32(rgb))
+    ok, m = synth.within_tolerance(_run(rgb), cref.harris_f64(rgb))
+    assert ok, m
+
+
+def test_pair_row_tma_batch_bands_and_fallbacks(cuda_ctx):
+    B, H, W = 3, 40, 262
+    rgb = synth.synth_numpy(3 * B, H, W, seed=61).reshape(B, 3, H, W)
+    x = _dev(rgb)
+    ex = hb.harris(x, exact=True)
+    assert cuda_ctx.last_path == _lib.PATH_PAIR
+    fast = hb.harris(x)
+    torch.cuda.synchronize()
+    for b in range(B):
+        assert np.array_equal(ex[b].cpu().numpy(), cref.harris_f32(rgb[b])), b
+        assert torch.equal(fast[b], hb.harris(x[b]))
+    # row bands: an even start row keeps the pair-row path, an odd one falls to K2; all equal
+    from paper_2212_12035_b200 import shard
+    img = x[1]
+    full = hb.harris(img)
+    parts, paths = [], []
+    for bnd in shard.row_bands(H - 4, 3):
+        parts.append(hb.harris(shard.band_view(img, bnd)))
+        paths.append(cuda_ctx.last_path)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(parts, 0), full)
+    assert _lib.PATH_PAIR in paths
+    # odd height: the last pair-row would run past the plane -> K2
+    odd = synth.synth_numpy(3, 41, 130, seed=3)
+    got = _run(odd, exact=True)
+    assert cuda_ctx.last_path == _lib.PATH_LDG
+    assert np.array_equal(got, cref.harris_f32(odd))
