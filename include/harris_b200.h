@@ -69,6 +69,7 @@ extern "C" {
 #define HARRIS_PATH_GENERIC 2  /* K0: shared-memory tile kernel (any W, any pitch)   */
 #define HARRIS_PATH_PAIR    4  /* K1p: TMA over pairs of rows, for f32 whose row pitch is 2 (mod 4)
                                       floats (e.g. 1918 or 8190 wide) with 16-byte aligned planes */
+#define HARRIS_PATH_QUAD    5  /* K1q: TMA over quads of rows, for f32 with an odd row pitch */
 #define HARRIS_PATH_LDG     3  /* K2: the TMA kernel's engine with cp.async stage fills, for
                                       inputs whose strides / base TMA cannot describe (f32 with
                                       W % 4 != 0 or a 4-byte aligned base; u8 with 3W % 16 != 0) */

@@ -29,7 +29,7 @@ FLAG_EXACT_ORDER = 0x1
 FLAG_FORCE_GENERIC = 0x2
 FLAG_FORCE_TMA = 0x4
 
-PATH_NONE, PATH_TMA, PATH_GENERIC, PATH_LDG, PATH_PAIR = 0, 1, 2, 3, 4
+PATH_NONE, PATH_TMA, PATH_GENERIC, PATH_LDG, PATH_PAIR, PATH_QUAD = 0, 1, 2, 3, 4, 5
 
 # every symbol include/harris_b200.h declares (checked by tests/test_abi.py)
 EXPORTED_SYMBOLS = (

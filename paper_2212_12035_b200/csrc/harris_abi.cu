@@ -39,6 +39,7 @@ struct harris_ctx {
     int occ_ldg[kNumLdgConfigs] = {0};
     int occ_u8ldg = 0;
     int occ_pair = 0;
+    int occ_quad = 0;
     int occ_sepldg = 0;
     int u8ldg_chunk = 16;  // HARRIS_U8LDG_CHUNK: 4 or 16-byte copies in the u8 K2 kernel
     int ldg_cfg = 2;  // HARRIS_LDG_CONFIG; 2 = scalar lane-halo core, 16 warps/SM (284 k MP/s on 8190^2)
@@ -115,7 +116,8 @@ struct Call {
     uint32_t notify_epoch = 0;
     int cfg = -1;  // f32 TMA configuration chosen for this call (resolve_cfg)
     bool ldg = false;  // plan for the cp.async (LDG) kernel
-    bool pair = false;  // plan for the pair-row TMA kernel
+    bool pair = false;  // plan for a row-group TMA kernel (pair- or quad-rows)
+    int group = 0;      // rows per group: 2 (pitch = 2 mod 4) or 4 (odd pitch)
 };
 
 int validate(const Call& c) {
@@ -225,36 +227,40 @@ bool ldg_eligible(const Call& c) {
 // planar f32 whose row pitch is 2 (mod 4) floats: pairs of rows are 16-byte multiples, so a
 // tensor map over pair-rows serves it (HarrisF32PairRowOp).  Needs 16-byte aligned planes
 // and an even image height (the last pair-row of the last plane must not run past it).
-bool pair_eligible(const Call& c) {
+// Returns the rows per group (2 or 4) when a row-group tensor map can serve the call, else 0.
+// An odd pitch groups 4 rows (4P floats is a 16-byte multiple): HarrisF32QuadRowOp.
+int row_group(const Call& c) {
     const Geom& g = c.g;
-    if (c.fmt != kF32Planar || !aligned16(g.rgb)) return false;
-    if ((g.in_pitch & 3) != 2 || (g.in_chan_stride & 3) || ((g.n + 4) & 1)) return false;
-    if (g.batch > 1 && (g.in_image_stride & 3)) return false;
-    if (2 * g.in_pitch > INT32_MAX || g.batch > INT32_MAX) return false;
-    return g.batch * ((g.m + 123) / 124) < (int64_t(1) << 30);
+    if (c.fmt != kF32Planar || !aligned16(g.rgb)) return 0;
+    const int k = (g.in_pitch & 3) == 2 ? 2 : (g.in_pitch & 1) ? 4 : 0;
+    if (!k || (g.in_chan_stride & 3) || ((g.n + 4) % k)) return 0;
+    if (g.batch > 1 && (g.in_image_stride & 3)) return 0;
+    if (int64_t(k) * g.in_pitch > INT32_MAX || g.batch > INT32_MAX) return 0;
+    return g.batch * ((g.m + 123) / 124) < (int64_t(1) << 30) ? k : 0;
 }
+bool pair_eligible(const Call& c) { return row_group(c) != 0; }
 
 int choose_path(const Call& c) {
     if (c.flags & HARRIS_FLAG_FORCE_GENERIC) return HARRIS_PATH_GENERIC;
     if (tma_eligible(c)) return HARRIS_PATH_TMA;
-    if (pair_eligible(c)) return HARRIS_PATH_PAIR;
+    if (const int k = row_group(c)) return k == 2 ? HARRIS_PATH_PAIR : HARRIS_PATH_QUAD;
     return ldg_eligible(c) ? HARRIS_PATH_LDG : HARRIS_PATH_GENERIC;
 }
 
 void plan_launch(const harris_ctx* ctx, const Call& c, TileGeom& tg, int64_t& grid) {
     const bool u8 = c.fmt == kU8Interleaved;
     const int fcfg = c.cfg >= 0 ? c.cfg : ctx->tma_cfg;
-    const TmaConfig& cfg = c.pair  ? kPairConfig
+    const TmaConfig& cfg = c.pair  ? (c.group == 4 ? kQuadConfig : kPairConfig)
                            : c.ldg ? (u8 ? kU8LdgConfig : kLdgConfigs[ctx->ldg_cfg])
                            : u8    ? kU8Configs[ctx->u8_cfg]
                                    : kTmaConfigs[fcfg];
-    const int occ = std::max(1, c.pair  ? ctx->occ_pair
+    const int occ = std::max(1, c.pair  ? (c.group == 4 ? ctx->occ_quad : ctx->occ_pair)
                                 : c.ldg ? (u8 ? ctx->occ_u8ldg : ctx->occ_ldg[ctx->ldg_cfg])
                                 : u8    ? ctx->occ_u8[ctx->u8_cfg]
                                         : ctx->occ[fcfg]);
     const int64_t resident_ctas = int64_t(ctx->num_sms) * occ;
     plan_tiles(c.g.n, c.g.m, c.g.batch, resident_ctas * cfg.warps, cfg.rows, ctx->force_band_rows, tg, 4,
-               cfg.groups, cfg.strip_cols, /*cap_rows=*/!u8, /*row_align=*/c.pair ? 2 : 1);
+               cfg.groups, cfg.strip_cols, /*cap_rows=*/!u8, /*row_align=*/c.pair ? c.group : 1);
     grid = std::min<int64_t>((tg.tiles + cfg.warps - 1) / cfg.warps, resident_ctas);
     tg.out = c.g.out;
     tg.out_pitch = c.g.out_pitch;
@@ -300,12 +306,14 @@ int encode_tmap_u8(harris_ctx* ctx, const Call& c, CUtensorMap* tmap) {
     return HARRIS_OK;
 }
 
-// pair-row view of planar f32 with pitch P = 2 (mod 4): {2P columns, H/2 pair-rows, 3, B}
+// row-group view of planar f32 (K = 2 for pitch P = 2 mod 4, K = 4 for odd P):
+// {K*P columns, H/K groups, 3, B}
 int encode_tmap_pair(harris_ctx* ctx, const Call& c, CUtensorMap* tmap) {
     const Geom& g = c.g;
-    cuuint64_t dims[4] = {cuuint64_t(2 * g.in_pitch), cuuint64_t((g.n + 4) / 2), 3, cuuint64_t(g.batch)};
+    const int64_t k = c.group;
+    cuuint64_t dims[4] = {cuuint64_t(k * g.in_pitch), cuuint64_t((g.n + 4) / k), 3, cuuint64_t(g.batch)};
     const int64_t img_stride = g.batch > 1 ? g.in_image_stride : 3 * g.in_chan_stride;
-    cuuint64_t strides[3] = {cuuint64_t(2 * g.in_pitch) * 4, cuuint64_t(g.in_chan_stride) * 4,
+    cuuint64_t strides[3] = {cuuint64_t(k * g.in_pitch) * 4, cuuint64_t(g.in_chan_stride) * 4,
                              cuuint64_t(img_stride) * 4};
     cuuint32_t box[4] = {132, 3, 3, 1};  // HarrisF32PairRowOp::kRow
     cuuint32_t estr[4] = {1, 1, 1, 1};
@@ -391,14 +399,17 @@ int run(harris_ctx* ctx, const Call& c, cudaStream_t stream) {
     DeviceGuard guard(ctx->device);
     if (!guard.ok) return cuda_fail(ctx, cudaGetLastError(), "cudaSetDevice");
     cudaError_t e;
-    if (path == HARRIS_PATH_TMA || path == HARRIS_PATH_LDG || path == HARRIS_PATH_PAIR) {
+    if (path == HARRIS_PATH_TMA || path == HARRIS_PATH_LDG || path == HARRIS_PATH_PAIR ||
+        path == HARRIS_PATH_QUAD) {
         const bool ldg = path == HARRIS_PATH_LDG;
-        const bool pair = path == HARRIS_PATH_PAIR;
+        const bool pair = path == HARRIS_PATH_PAIR || path == HARRIS_PATH_QUAD;
+        const int group = path == HARRIS_PATH_QUAD ? 4 : 2;
         harris_ctx::LaunchEntry ent;
         if (!cache_lookup(ctx, c, ent)) {
             Call cc = c;
             cc.ldg = ldg;
             cc.pair = pair;
+            cc.group = group;
             if (!ldg) {
                 cc.cfg = pair ? 0 : resolve_cfg(ctx, c);
                 rc = encode_tmap(ctx, cc, &ent.tmap);
@@ -415,7 +426,8 @@ int run(harris_ctx* ctx, const Call& c, cudaStream_t stream) {
             tg.notify_flag = c.notify_flag;
             tg.notify_epoch = c.notify_epoch;
         }
-        e = pair ? launch_tma_pair(exact, ent.tmap, tg, ent.grid, int32_t(c.g.in_pitch), stream)
+        e = pair ? (group == 4 ? launch_tma_quad(exact, ent.tmap, tg, ent.grid, int32_t(c.g.in_pitch), stream)
+                               : launch_tma_pair(exact, ent.tmap, tg, ent.grid, int32_t(c.g.in_pitch), stream))
             : ldg ? (c.fmt == kU8Interleaved ? launch_u8_ldg(exact, ctx->u8ldg_chunk, c.g, tg, ent.grid, stream)
                                              : launch_ldg(ctx->ldg_cfg, exact, c.g, tg, ent.grid, stream))
             : c.fmt == kU8Interleaved ? launch_tma_u8(ctx->u8_cfg, exact, ent.tmap, tg, ent.grid, stream)
@@ -427,6 +439,7 @@ int run(harris_ctx* ctx, const Call& c, cudaStream_t stream) {
     if (e != cudaSuccess)
         return cuda_fail(ctx, e, path == HARRIS_PATH_TMA    ? "launch tma"
                                  : path == HARRIS_PATH_PAIR ? "launch tma pair"
+                                 : path == HARRIS_PATH_QUAD ? "launch tma quad"
                                  : path == HARRIS_PATH_LDG  ? "launch ldg"
                                                             : "launch generic");
     ctx->last_path = path;
@@ -560,6 +573,7 @@ int harris_init(harris_ctx** out_ctx, int cuda_device) {
         }
     }
     e = pair_configure(&ctx->occ_pair);
+    if (e == cudaSuccess) e = quad_configure(&ctx->occ_quad);
     if (e == cudaSuccess) e = sep_ldg_configure(&ctx->occ_sepldg);
     if (e == cudaSuccess) e = u8_ldg_configure(&ctx->occ_u8ldg);
     if (e != cudaSuccess) {
@@ -752,9 +766,12 @@ int harris_plan(harris_ctx* ctx, int64_t n, int64_t m, int64_t batch, const floa
     std::memset(info, 0, sizeof(*info));
     info->path = choose_path(c);
     c.ldg = info->path == HARRIS_PATH_LDG;
-    c.pair = info->path == HARRIS_PATH_PAIR;
+    c.pair = info->path == HARRIS_PATH_PAIR || info->path == HARRIS_PATH_QUAD;
+    c.group = info->path == HARRIS_PATH_QUAD ? 4 : 2;
     c.cfg = (c.ldg || c.pair) ? -1 : resolve_cfg(ctx, c);
-    const TmaConfig& cfg = c.pair ? kPairConfig : c.ldg ? kLdgConfigs[ctx->ldg_cfg] : kTmaConfigs[c.cfg];
+    const TmaConfig& cfg = c.pair ? (c.group == 4 ? kQuadConfig : kPairConfig)
+                           : c.ldg ? kLdgConfigs[ctx->ldg_cfg]
+                                   : kTmaConfigs[c.cfg];
     info->warps_per_cta = cfg.warps;
     info->stages = cfg.stages;
     info->rows_per_stage = cfg.rows;

@@ -63,6 +63,11 @@ extern const TmaConfig kPairConfig;
 cudaError_t pair_configure(int* ctas_per_sm);
 cudaError_t launch_tma_pair(bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid, int32_t pitch,
                             cudaStream_t stream);
+// quad-row TMA kernel for planar f32 with an odd row pitch (HarrisF32QuadRowOp)
+extern const TmaConfig kQuadConfig;
+cudaError_t quad_configure(int* ctas_per_sm);
+cudaError_t launch_tma_quad(bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid, int32_t pitch,
+                            cudaStream_t stream);
 
 // cp.async (LDGSTS) warp-strip kernel for f32 inputs TMA cannot describe (row pitch or
 // base not 16-byte aligned): same engine and dual-strip core as the TMA path

@@ -303,7 +303,70 @@ struct HarrisF32PairRowOp : HarrisF32Op<EXACT, 6, 124> {
         }
         const float gown[4] = {gray_of<EXACT>(c[0][0], c[1][0], c[2][0]), gray_of<EXACT>(c[0][1], c[1][1], c[2][1]),
                                gray_of<EXACT>(c[0][2], c[1][2], c[2][2]), gray_of<EXACT>(c[0][3], c[1][3], c[2][3])};
-        this->core.template step<R, NoHalo, true>(gown, lane, NoHalo{}, out[0]);
+        // no row-pair box sums: FAST stays bit-identical to the other f32 paths
+        this->core.template step<R, NoHalo, false>(gown, lane, NoHalo{}, out[0]);
+    }
+};
+
+// ------------------------------------------------- planar f32 with an odd row pitch
+// The pair-row idea one level up: 4 rows (4P floats) are a 16-byte multiple.  The tensor
+// map views each plane as H/4 quad-rows; image row 4j + r is quad-row j at column rP + x.
+// A stage of CH = 12 rows is four boxes (one per r) of 3 quad-rows.  Each class's box starts
+// s_r = rP mod 4 floats early (16-byte aligned) and the consumer reads it s_r floats in
+// (s_0 = 0: 16-byte loads; otherwise scalar loads at a warp-uniform skew).
+template <bool EXACT>
+struct HarrisF32QuadRowOp : HarrisF32Op<EXACT, 12, 124> {
+    using Base = HarrisF32Op<EXACT, 12, 124>;
+    static constexpr int CH = 12;
+    static constexpr int kRow = 132;
+    static constexpr uint32_t kBoxBytes = 3u * 3u * kRow * 4u;
+    static constexpr uint32_t kBoxStride = (kBoxBytes + 127u) / 128u * 128u;
+    static constexpr uint32_t kTxBytes = 4u * kBoxBytes;
+    static constexpr uint32_t kStageBytes = 4u * kBoxStride;
+    struct Params {
+        float kappa;
+        int32_t pitch;  // P (odd)
+    };
+    int skew[4];  // s_r: float offset of class r's data in its box
+
+    __device__ __forceinline__ explicit HarrisF32QuadRowOp(const Params& p) : Base(typename Base::Params{p.kappa}) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) skew[r] = (r * p.pitch) & 3;
+    }
+
+    __device__ __forceinline__ static void load_p(void* smem, const CUtensorMap* tmap, uint64_t* bar,
+                                                  const int (&col0)[1], int row0, const int (&image)[1],
+                                                  uint64_t policy, const Params& p) {
+        const int j0 = row0 >> 2;  // row0 is a multiple of 4 (planner)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int x = r * p.pitch;
+            tma_load_4d(static_cast<unsigned char*>(smem) + r * kBoxStride, tmap, bar, x - (x & 3) + col0[0], j0, 0,
+                        image[0], policy);
+        }
+    }
+
+    template <int R>
+    __device__ __forceinline__ void row(const unsigned char* stage, int lane, float (&out)[1][4]) {
+        constexpr int cls = R & 3, qr = R >> 2;
+        const float* sm = reinterpret_cast<const float*>(stage + cls * kBoxStride);
+        float c[3][4];
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+            const float* q = sm + (ch * 3 + qr) * kRow + 4 * lane;
+            if constexpr (cls == 0) {
+                const float4 v = lds128(q);
+                c[ch][0] = v.x, c[ch][1] = v.y, c[ch][2] = v.z, c[ch][3] = v.w;
+            } else {
+                const float* qs = q + skew[cls];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) c[ch][i] = qs[i];
+            }
+        }
+        const float gown[4] = {gray_of<EXACT>(c[0][0], c[1][0], c[2][0]), gray_of<EXACT>(c[0][1], c[1][1], c[2][1]),
+                               gray_of<EXACT>(c[0][2], c[1][2], c[2][2]), gray_of<EXACT>(c[0][3], c[1][3], c[2][3])};
+        // no row-pair box sums: FAST stays bit-identical to the other f32 paths
+        this->core.template step<R, NoHalo, false>(gown, lane, NoHalo{}, out[0]);
     }
 };
 

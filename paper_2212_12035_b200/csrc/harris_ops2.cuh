@@ -163,15 +163,17 @@ struct HarrisCore2 {
             prodsum4(ix, ix, HB[s2][0], HB[s2][1], HB[s2][2], HB[s2][3]);
             prodsum4(ix, iy, HB[s2][4], HB[s2][5], HB[s2][6], HB[s2][7]);
             prodsum4(iy, iy, HB[s2][8], HB[s2][9], HB[s2][10], HB[s2][11]);
-            const float2 kk = f2(kappa);
+            const float2 nk = f2(-kappa);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const float2 sxx = add2(add2(HB[s0][0 + j], HB[s1][0 + j]), HB[s2][0 + j]);
                 const float2 sxy = add2(add2(HB[s0][4 + j], HB[s1][4 + j]), HB[s2][4 + j]);
                 const float2 syy = add2(add2(HB[s0][8 + j], HB[s1][8 + j]), HB[s2][8 + j]);
+                // same op order as the scalar core's coarsity_fast, so FAST results are
+                // bit-identical across every kernel path / configuration
+                const float2 det = fma2(make_float2(-sxy.x, -sxy.y), sxy, mul2(sxx, syy));
                 const float2 tr = add2(sxx, syy);
-                const float2 t2 = fma2(sxy, sxy, mul2(mul2(kk, tr), tr));
-                const float2 o = sub2(mul2(sxx, syy), t2);
+                const float2 o = fma2(mul2(nk, tr), tr, det);
                 out[0][j] = o.x;
                 out[1][j] = o.y;
             }

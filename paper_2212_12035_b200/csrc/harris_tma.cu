@@ -214,4 +214,38 @@ cudaError_t launch_tma_pair(bool exact, const CUtensorMap& tmap, const TileGeom&
     return cudaGetLastError();
 }
 
+// ---- quad-row TMA kernel (odd row pitch, HarrisF32QuadRowOp): 12-row stages, 5 warps ----
+constexpr int kQuadNW = 5, kQuadNS = 2;
+const TmaConfig kQuadConfig = {kQuadNW, kQuadNS, 12, 1, 124};
+
+template <bool EXACT>
+static constexpr auto quad_kernel() {
+    return strip_kernel<HarrisF32QuadRowOp<EXACT>, kQuadNW, kQuadNS, 1>;
+}
+static constexpr size_t quad_smem() { return StripShape<kQuadNW, kQuadNS, HarrisF32QuadRowOp<false>>::kSmemBytes; }
+static_assert(quad_smem() <= 227 * 1024, "quad-row config exceeds 227 KB of shared memory");
+
+cudaError_t quad_configure(int* ctas_per_sm) {
+    cudaError_t e = cudaFuncSetAttribute(quad_kernel<false>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(quad_smem()));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(quad_kernel<true>(), cudaFuncAttributeMaxDynamicSharedMemorySize, int(quad_smem()));
+    if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, quad_kernel<false>(), kQuadNW * 32,
+                                                          quad_smem());
+    return e;
+}
+
+cudaError_t launch_tma_quad(bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid, int32_t pitch,
+                            cudaStream_t stream) {
+    const dim3 block{unsigned(kQuadNW * 32)}, gridd{unsigned(grid)};
+    if (exact)
+        quad_kernel<true>()<<<gridd, block, quad_smem(), stream>>>(tmap, tg,
+                                                                  typename HarrisF32QuadRowOp<true>::Params{tg.kappa, pitch});
+    else
+        quad_kernel<false>()<<<gridd, block, quad_smem(), stream>>>(
+            tmap, tg, typename HarrisF32QuadRowOp<false>::Params{tg.kappa, pitch});
+    return cudaGetLastError();
+}
+
 }  // namespace harris

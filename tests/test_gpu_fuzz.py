@@ -53,10 +53,10 @@ def test_fuzz_f32_layouts(cuda_ctx, seed):
     for b in range(B):
         assert np.array_equal(got[b], cref.harris_f32(rgb[b])), (seed, H, W, B, pad, gap, off, opad, generic, path, b)
     aligned = off % 4 == 0 and pitch % 4 == 0 and chan % 4 == 0 and (B == 1 or img_stride % 4 == 0)
-    pair = (off % 4 == 0 and pitch % 4 == 2 and chan % 4 == 0 and H % 2 == 0 and
-            (B == 1 or img_stride % 4 == 0))
+    k = 2 if pitch % 4 == 2 else 4 if pitch % 2 else 0
+    grouped = bool(k) and off % 4 == 0 and chan % 4 == 0 and H % k == 0 and (B == 1 or img_stride % 4 == 0)
     assert path == (_lib.PATH_GENERIC if generic else _lib.PATH_TMA if aligned else
-                    _lib.PATH_PAIR if pair else _lib.PATH_LDG)
+                    (_lib.PATH_PAIR if k == 2 else _lib.PATH_QUAD) if grouped else _lib.PATH_LDG)
     # padding columns of the output were never written
     if opad:
         assert torch.all(obuf[: B * n * (m + opad)].view(B, n, m + opad)[:, :, m:] == -3.0)

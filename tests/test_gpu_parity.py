@@ -482,8 +482,9 @@ def test_ldg_exact_bitexact(cuda_ctx, H, W):
     fills runs, bit-identical to the C oracle in EXACT order, within tolerance in FAST."""
     rgb = synth.synth_numpy(3, H, W, seed=H * 31 + W)
     got = _run(rgb, exact=True)
-    pair = W % 4 == 2 and H % 2 == 0 and (H * W) % 4 == 0
-    assert cuda_ctx.last_path == (_lib.PATH_PAIR if pair else _lib.PATH_LDG)
+    k = 2 if W % 4 == 2 else 4 if W % 2 else 0
+    grouped = k and H % k == 0 and (H * W) % 4 == 0
+    assert cuda_ctx.last_path == ((_lib.PATH_PAIR if k == 2 else _lib.PATH_QUAD) if grouped else _lib.PATH_LDG)
     assert np.array_equal(got, cref.harris_f32(rgb))
     ok, m = synth.within_tolerance(_run(rgb), cref.harris_f64(rgb))
     assert ok, m
@@ -526,7 +527,7 @@ def test_ldg_unaligned_base_batch_and_bands(cuda_ctx):
 @pytest.mark.parametrize("cfg", [0, 1, 2])
 def test_every_ldg_config_bitexact(cuda_ctx, cfg):
     ctx = _ctx_with({"HARRIS_LDG_CONFIG": cfg})
-    for B, H, W in [(1, 9, 131), (1, 70, 261), (3, 41, 387), (1, 300, 2563), (5, 21, 137)]:
+    for B, H, W in [(1, 9, 131), (1, 70, 261), (3, 41, 387), (1, 302, 2563), (5, 21, 137)]:
         rgb = synth.synth_numpy(3 * B, H, W, seed=cfg * 13 + H).reshape(B, 3, H, W)
         x = _dev(rgb if B > 1 else rgb[0])
         ex = hb.harris(x, exact=True, ctx=ctx)
@@ -704,3 +705,63 @@ def test_pair_row_tma_batch_bands_and_fallbacks(cuda_ctx):
     got = _run(odd, exact=True)
     assert cuda_ctx.last_path == _lib.PATH_LDG
     assert np.array_equal(got, cref.harris_f32(odd))
+
+
+
+# ------------------------------- K1q: TMA over quads of rows (odd row pitch)
+@pytest.mark.parametrize("H,W", [(8, 9), (64, 133), (300, 2563), (132, 517), (1084, 1921)])
+def test_quad_row_tma_bitexact(cuda_ctx, H, W):
+    rgb = synth.synth_numpy(3, H, W, seed=H * 5 + W)
+    got = _run(rgb, exact=True)
+    assert cuda_ctx.last_path == _lib.PATH_QUAD
+    assert np.array_equal(got, cref.harris_f32(rgb))
+    ok, m = synth.within_tolerance(_run(rgb), cref.harris_f64(rgb))
+    assert ok, m
+
+
+def test_quad_row_tma_batch_and_bands(cuda_ctx):
+    B, H, W = 3, 40, 263
+    rgb = synth.synth_numpy(3 * B, H, W, seed=67).reshape(B, 3, H, W)
+    x = _dev(rgb)
+    ex = hb.harris(x, exact=True)
+    assert cuda_ctx.last_path == _lib.PATH_QUAD
+    fast = hb.harris(x)
+    torch.cuda.synchronize()
+    for b in range(B):
+        assert np.array_equal(ex[b].cpu().numpy(), cref.harris_f32(rgb[b])), b
+        assert torch.equal(fast[b], hb.harris(x[b]))
+    from paper_2212_12035_b200 import shard
+    img = x[2]
+    full = hb.harris(img)
+    parts = [hb.harris(shard.band_view(img, bnd)) for bnd in shard.row_bands(H - 4, 4)]
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(parts, 0), full)
+
+
+def test_fast_order_identical_across_kernel_paths(cuda_ctx):
+    """The shipped (FAST) arithmetic is the same on every f32 path — TMA dual-strip, TMA
+    scalar (short tiles), pair-row and quad-row TMA, cp.async K2 — so ANY decomposition
+    (multi-GPU bands of any height, views, copies at other alignments) is bit-identical."""
+    from paper_2212_12035_b200 import shard
+    for H, W in [(72, 264), (72, 262), (72, 263)]:       # TMA, PAIR, QUAD for the full image
+        rgb = synth.synth_numpy(3, H, W, seed=W)
+        x = _dev(rgb)
+        full = hb.harris(x)
+        paths = {cuda_ctx.last_path}
+        # 4-byte aligned (not 16) copy: K2
+        buf = torch.zeros(rgb.size + 1, device="cuda")
+        mis = buf[1:].view(3, H, W)
+        mis.copy_(x)
+        r = hb.harris(mis)
+        paths.add(cuda_ctx.last_path)
+        torch.cuda.synchronize()
+        assert torch.equal(r, full), (H, W)
+        # bands of many heights (odd / even starts, short tiles)
+        for G in (2, 3, 5, 7):
+            parts = []
+            for bnd in shard.row_bands(H - 4, G):
+                parts.append(hb.harris(shard.band_view(x, bnd)))
+                paths.add(cuda_ctx.last_path)
+            torch.cuda.synchronize()
+            assert torch.equal(torch.cat(parts, 0), full), (H, W, G)
+        assert len(paths) >= 2, paths
