@@ -102,6 +102,8 @@ struct HarrisCore2 {
 
     __device__ __forceinline__ explicit HarrisCore2(float k) : kappa(k) {
 #pragma unroll
+#pragma unroll
+        for (int q = 0; q < 12; ++q) PV[q] = f2(0.f);
         for (int a = 0; a < 3; ++a) {
 #pragma unroll
             for (int j = 0; j < 6; ++j) D[a][j] = Hs[a][j] = f2(0.f);
@@ -127,7 +129,10 @@ struct HarrisCore2 {
 
     // gown: (A, B) gray of this lane's 4 columns; halo(h0..h3) fills the right halo of
     // both strips for lane 31
-    template <int R, class HaloFn>
+    float2 PV[12];  // row-pair partial box sums (kPairRows: the u8 op, where rounding parity
+                    // with the f32 paths is not required and instructions are the bound)
+
+    template <int R, class HaloFn, bool kPairRows = false>
     __device__ __forceinline__ void step(const float2 (&gown)[4], int lane, HaloFn&& halo, float (&out)[2][4]) {
         constexpr int s2 = R % 3, s0 = (R + 1) % 3, s1 = (R + 2) % 3;
         constexpr bool kLaneHalo = std::is_same_v<std::decay_t<HaloFn>, NoHalo>;
@@ -164,11 +169,26 @@ struct HarrisCore2 {
             prodsum4(ix, iy, HB[s2][4], HB[s2][5], HB[s2][6], HB[s2][7]);
             prodsum4(iy, iy, HB[s2][8], HB[s2][9], HB[s2][10], HB[s2][11]);
             const float2 nk = f2(-kappa);
+            float2 v[12];
+            if constexpr (kPairRows) {
+                // odd row r: PV = H[r-1] + H[r], V = H[r-2] + PV; even row: V = PV + H[r]
+                if constexpr (R % 2 == 1) {
+#pragma unroll
+                    for (int q = 0; q < 12; ++q) {
+                        PV[q] = add2(HB[s1][q], HB[s2][q]);
+                        v[q] = add2(HB[s0][q], PV[q]);
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 12; ++q) v[q] = add2(PV[q], HB[s2][q]);
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 12; ++q) v[q] = add2(add2(HB[s0][q], HB[s1][q]), HB[s2][q]);
+            }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const float2 sxx = add2(add2(HB[s0][0 + j], HB[s1][0 + j]), HB[s2][0 + j]);
-                const float2 sxy = add2(add2(HB[s0][4 + j], HB[s1][4 + j]), HB[s2][4 + j]);
-                const float2 syy = add2(add2(HB[s0][8 + j], HB[s1][8 + j]), HB[s2][8 + j]);
+                const float2 sxx = v[0 + j], sxy = v[4 + j], syy = v[8 + j];
                 // same op order as the scalar core's coarsity_fast, so FAST results are
                 // bit-identical across every kernel path / configuration
                 const float2 det = fma2(make_float2(-sxy.x, -sxy.y), sxy, mul2(sxx, syy));
@@ -374,7 +394,7 @@ struct HarrisU8x2Op {
         float2 gown[4];
         gray4_u8x2<EXACT>(a, b, gown[0], gown[1], gown[2], gown[3]);
         if constexpr (L::kLaneHalo) {
-            core.template step<R>(gown, lane, NoHalo{}, out);
+            core.template step<R, NoHalo, (CH % 2 == 0)>(gown, lane, NoHalo{}, out);
         } else {
             core.template step<R>(gown, lane, [&](float2& h0, float2& h1, float2& h2, float2& h3) {
                 const uint32_t ha[3] = {wa[96], wa[97], wa[98]};
