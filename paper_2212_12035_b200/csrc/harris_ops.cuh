@@ -390,16 +390,23 @@ __device__ __forceinline__ float gray_u8(float r, float g, float b) {
 }
 
 // 4 pixels = 12 bytes = 3 words: w0 = R0 G0 B0 R1, w1 = G1 B1 R2 G2, w2 = B2 R3 G3 B3
-// FAST: the red channel's 2^23 offset is cancelled inside the first FFMA —
-// fma(kR, 2^23 + b, -kR * 2^23) is exactly kR * b rounded once, i.e. the same value as
-// kR * float(b) — so only green and blue need the FADD of u8f
-__device__ __forceinline__ float u8raw(uint32_t w, int k) {
-    return __int_as_float(__byte_perm(w, 0x4B000000u, 0x7440u | uint32_t(k)));
+// FAST: N = 299 R + 587 G + 114 B exactly in integers — two IDP.2A (16-bit weights x
+// byte pairs) per pixel straight on the interleaved words, no byte extraction — summed
+// onto 0x4B000000 so the bit pattern is the float 2^23 + N (N <= 255000 < 2^23); then
+// gray = fma(2^23 + N, s, -s * 2^23) = RN(s * N), s = 1/(12 * 255 * 1000) (the Sobel 1/12
+// folded in).  One rounding, so it is closer to the f64 oracle than the three-FMA form.
+constexpr float kGrayU8Scale = 1.0f / (12.0f * 255.0f * 1000.0f);
+__device__ __forceinline__ void gray4_u8_bits(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t& n0, uint32_t& n1,
+                                              uint32_t& n2, uint32_t& n3) {
+    constexpr uint32_t kRG = 299u | (587u << 16), kB0 = 114u, k0R = 299u << 16, kGB = 587u | (114u << 16);
+    constexpr uint32_t kBias = 0x4B000000u;
+    n0 = __dp2a_hi(kB0, w0, __dp2a_lo(kRG, w0, kBias));   // R0 G0 | B0
+    n1 = __dp2a_lo(kGB, w1, __dp2a_hi(k0R, w0, kBias));   // R1 | G1 B1
+    n2 = __dp2a_lo(kB0, w2, __dp2a_hi(kRG, w1, kBias));   // R2 G2 | B2
+    n3 = __dp2a_hi(kGB, w2, __dp2a_lo(k0R, w2, kBias));   // R3 | G3 B3
 }
-__device__ __forceinline__ float gray_u8_fast_raw(float r_raw, float g, float b) {
-    constexpr float kR = 0.299f / (12.0f * 255.0f), kG = 0.587f / (12.0f * 255.0f),
-                    kB = 0.114f / (12.0f * 255.0f);
-    return fmaf(kB, b, fmaf(kG, g, fmaf(kR, r_raw, -kR * 8388608.0f)));
+__device__ __forceinline__ float gray_u8_from_bits(uint32_t n) {
+    return fmaf(__uint_as_float(n), kGrayU8Scale, -kGrayU8Scale * 8388608.0f);
 }
 
 template <bool EXACT>
@@ -411,10 +418,12 @@ __device__ __forceinline__ void gray4_u8(uint32_t w0, uint32_t w1, uint32_t w2, 
         g2 = gray_u8<EXACT>(u8f(w1, 2), u8f(w1, 3), u8f(w2, 0));
         g3 = gray_u8<EXACT>(u8f(w2, 1), u8f(w2, 2), u8f(w2, 3));
     } else {
-        g0 = gray_u8_fast_raw(u8raw(w0, 0), u8f(w0, 1), u8f(w0, 2));
-        g1 = gray_u8_fast_raw(u8raw(w0, 3), u8f(w1, 0), u8f(w1, 1));
-        g2 = gray_u8_fast_raw(u8raw(w1, 2), u8f(w1, 3), u8f(w2, 0));
-        g3 = gray_u8_fast_raw(u8raw(w2, 1), u8f(w2, 2), u8f(w2, 3));
+        uint32_t n0, n1, n2, n3;
+        gray4_u8_bits(w0, w1, w2, n0, n1, n2, n3);
+        g0 = gray_u8_from_bits(n0);
+        g1 = gray_u8_from_bits(n1);
+        g2 = gray_u8_from_bits(n2);
+        g3 = gray_u8_from_bits(n3);
     }
 }
 

@@ -339,26 +339,19 @@ __device__ __forceinline__ float2 gray2_u8(float2 r, float2 g, float2 b) {
 }
 
 // 4 pixels of strips A and B from their 3 words each
-// (byte k of wa, byte k of wb) as 2^23 + byte (no offset removal: folded into the FFMA2)
-__device__ __forceinline__ float2 u8raw2(uint32_t wa, uint32_t wb, int k) {
-    return make_float2(__int_as_float(__byte_perm(wa, 0x4B000000u, 0x7440u | uint32_t(k))),
-                       __int_as_float(__byte_perm(wb, 0x4B000000u, 0x7440u | uint32_t(k))));
-}
-// FAST: the red channel's 2^23 offset cancels inside the first FFMA2 (bit-identical to
-// kR * float(byte), as in the scalar op's gray_u8_fast_raw)
-__device__ __forceinline__ float2 gray2_u8_fast_raw(float2 r_raw, float2 g, float2 b) {
-    constexpr float kR = 0.299f / (12.0f * 255.0f), kG = 0.587f / (12.0f * 255.0f), kB = 0.114f / (12.0f * 255.0f);
-    return fma2(f2(kB), b, fma2(f2(kG), g, fma2(f2(kR), r_raw, f2(-kR * 8388608.0f))));
-}
-
 template <bool EXACT>
 __device__ __forceinline__ void gray4_u8x2(const uint32_t (&a)[3], const uint32_t (&b)[3], float2& g0, float2& g1,
                                            float2& g2, float2& g3) {
     if constexpr (!EXACT) {
-        g0 = gray2_u8_fast_raw(u8raw2(a[0], b[0], 0), u8f2(a[0], b[0], 1), u8f2(a[0], b[0], 2));
-        g1 = gray2_u8_fast_raw(u8raw2(a[0], b[0], 3), u8f2(a[1], b[1], 0), u8f2(a[1], b[1], 1));
-        g2 = gray2_u8_fast_raw(u8raw2(a[1], b[1], 2), u8f2(a[1], b[1], 3), u8f2(a[2], b[2], 0));
-        g3 = gray2_u8_fast_raw(u8raw2(a[2], b[2], 1), u8f2(a[2], b[2], 2), u8f2(a[2], b[2], 3));
+        // strips A and B: integer gray sums (harris_ops.cuh gray4_u8_bits), one FFMA2 per pair
+        uint32_t na[4], nb[4];
+        gray4_u8_bits(a[0], a[1], a[2], na[0], na[1], na[2], na[3]);
+        gray4_u8_bits(b[0], b[1], b[2], nb[0], nb[1], nb[2], nb[3]);
+        const float2 s = f2(kGrayU8Scale), c = f2(-kGrayU8Scale * 8388608.0f);
+        g0 = fma2(make_float2(__uint_as_float(na[0]), __uint_as_float(nb[0])), s, c);
+        g1 = fma2(make_float2(__uint_as_float(na[1]), __uint_as_float(nb[1])), s, c);
+        g2 = fma2(make_float2(__uint_as_float(na[2]), __uint_as_float(nb[2])), s, c);
+        g3 = fma2(make_float2(__uint_as_float(na[3]), __uint_as_float(nb[3])), s, c);
         return;
     }
     g0 = gray2_u8<EXACT>(u8f2(a[0], b[0], 0), u8f2(a[0], b[0], 1), u8f2(a[0], b[0], 2));
