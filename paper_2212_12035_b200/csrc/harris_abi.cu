@@ -38,10 +38,11 @@ struct harris_ctx {
     int occ_u8[kNumU8Configs] = {0};
     int occ_ldg[kNumLdgConfigs] = {0};
     int occ_u8ldg = 0;
+    int occ_u8bulk = 0;
     int occ_pair = 0;
     int occ_quad = 0;
     int occ_sepldg = 0;
-    int u8ldg_chunk = 16;  // HARRIS_U8LDG_CHUNK: 4 or 16-byte copies in the u8 K2 kernel
+    int u8ldg_chunk = 0;  // HARRIS_U8LDG_CHUNK: 0 bulk-copy kernel (K1b); 4 / 16-byte cp.async (K2)
     int ldg_cfg = 2;  // HARRIS_LDG_CONFIG; 2 = scalar lane-halo core, 16 warps/SM (284 k MP/s on 8190^2)
     int sync_waves = 1;  // dev knob HARRIS_SYNC_WAVES=0 disables the per-tile CTA barrier
     int l2_policy = 1;  // evict_normal: the 4-column halo sectors are re-read by the neighbouring strip
@@ -251,11 +252,11 @@ void plan_launch(const harris_ctx* ctx, const Call& c, TileGeom& tg, int64_t& gr
     const bool u8 = c.fmt == kU8Interleaved;
     const int fcfg = c.cfg >= 0 ? c.cfg : ctx->tma_cfg;
     const TmaConfig& cfg = c.pair  ? (c.group == 4 ? kQuadConfig : kPairConfig)
-                           : c.ldg ? (u8 ? kU8LdgConfig : kLdgConfigs[ctx->ldg_cfg])
+                           : c.ldg ? (u8 ? (ctx->u8ldg_chunk ? kU8LdgConfig : kU8BulkConfig) : kLdgConfigs[ctx->ldg_cfg])
                            : u8    ? kU8Configs[ctx->u8_cfg]
                                    : kTmaConfigs[fcfg];
     const int occ = std::max(1, c.pair  ? (c.group == 4 ? ctx->occ_quad : ctx->occ_pair)
-                                : c.ldg ? (u8 ? ctx->occ_u8ldg : ctx->occ_ldg[ctx->ldg_cfg])
+                                : c.ldg ? (u8 ? (ctx->u8ldg_chunk ? ctx->occ_u8ldg : ctx->occ_u8bulk) : ctx->occ_ldg[ctx->ldg_cfg])
                                 : u8    ? ctx->occ_u8[ctx->u8_cfg]
                                         : ctx->occ[fcfg]);
     const int64_t resident_ctas = int64_t(ctx->num_sms) * occ;
@@ -532,7 +533,7 @@ int harris_init(harris_ctx** out_ctx, int cuda_device) {
         if (v >= 0 && v < kNumSepConfigs) ctx->sep_cfg = v;
     }
     env = std::getenv("HARRIS_U8LDG_CHUNK");
-    if (env) ctx->u8ldg_chunk = std::atoi(env) == 4 ? 4 : 16;
+    if (env) ctx->u8ldg_chunk = std::atoi(env) == 4 ? 4 : std::atoi(env) == 16 ? 16 : 0;
     env = std::getenv("HARRIS_LDG_CONFIG");
     if (env) {
         int v = std::atoi(env);
@@ -575,7 +576,7 @@ int harris_init(harris_ctx** out_ctx, int cuda_device) {
     e = pair_configure(&ctx->occ_pair);
     if (e == cudaSuccess) e = quad_configure(&ctx->occ_quad);
     if (e == cudaSuccess) e = sep_ldg_configure(&ctx->occ_sepldg);
-    if (e == cudaSuccess) e = u8_ldg_configure(&ctx->occ_u8ldg);
+    if (e == cudaSuccess) e = u8_ldg_configure(&ctx->occ_u8ldg, &ctx->occ_u8bulk);
     if (e != cudaSuccess) {
         int rc = cuda_fail(ctx, e, "configure u8 ldg kernel");
         delete ctx;

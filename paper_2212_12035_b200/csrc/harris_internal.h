@@ -77,7 +77,8 @@ cudaError_t ldg_configure(int cfg, int* ctas_per_sm);
 cudaError_t launch_ldg(int cfg, bool exact, const Geom& g, const TileGeom& tg, int64_t grid, cudaStream_t stream);
 // interleaved u8 inputs whose byte strides TMA cannot describe (3W % 16 != 0)
 extern const TmaConfig kU8LdgConfig;
-cudaError_t u8_ldg_configure(int* ctas_per_sm);
+extern const TmaConfig kU8BulkConfig;
+cudaError_t u8_ldg_configure(int* ctas_per_sm, int* bulk_ctas_per_sm);
 cudaError_t launch_u8_ldg(bool exact, int chunk, const Geom& g, const TileGeom& tg, int64_t grid,
                           cudaStream_t stream);
 // separable stencil planes TMA cannot describe

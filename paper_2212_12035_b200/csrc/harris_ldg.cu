@@ -200,6 +200,125 @@ struct U8LdgOp : HarrisU8Op<EXACT, CH, 124> {
     }
 };
 
+// u8 rows at any byte alignment through the bulk-copy engine (K1b).  TMA tensor maps need
+// 16-byte row strides, which an interleaved row of 3W bytes has only when W % 16 == 0; a
+// plain bulk copy (cp.async.bulk, no tensor map) needs only a 16-byte aligned source and
+// a 16-byte multiple length.  So each stage row of each strip is ONE bulk copy of
+// up to 400 bytes from the row's 16-byte aligned-down start, issued by its own lane
+// (lane = strip * CH + row: the whole stage is one warp instruction), completing on the
+// stage mbarrier as transaction bytes like a TMA box.  The consumer undoes the per-row
+// skew (0..15 bytes, advancing by pitch mod 16 per row) with a word offset and a funnel
+// shift, then runs the packed dual-strip u8 core of the TMA path unchanged.  The copy is
+// clamped to the 16-byte block holding the row's last byte, so it never leaves the page of
+// a valid byte; rows below the image are not copied and columns beyond the row end are
+// stale — neither reaches a stored output.
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(smem)),
+                 "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+template <bool EXACT, int CH, int G>
+struct U8BulkOp : std::conditional_t<G == 2, HarrisU8x2Op<EXACT, CH, 124>, HarrisU8Op<EXACT, CH, 124>> {
+    using Base = std::conditional_t<G == 2, HarrisU8x2Op<EXACT, CH, 124>, HarrisU8Op<EXACT, CH, 124>>;
+    static_assert(G * CH <= 32, "one lane per stage row");
+    static constexpr bool kWarpLoad = true;
+    static constexpr int kBarArrivals = 1;  // lane 0's arrive.expect_tx; the copies count as tx bytes
+    static constexpr bool kCacheProducer = true;
+    static constexpr int kRowWords = 100;  // 400 B >= 15 skew bytes + 128 px * 3 B, 16-byte multiple
+    static constexpr uint32_t kBoxBytes = uint32_t(CH) * kRowWords * 4u;
+    static constexpr uint32_t kBoxStride = (kBoxBytes + 127u) / 128u * 128u;
+    static constexpr uint32_t kStageBytes = uint32_t(G) * kBoxStride;
+    struct Params {
+        float kappa;
+        const uint8_t* rgb;
+        int64_t in_pitch, in_image_stride;  // bytes
+        int32_t W, H;                       // input pixels per row / rows per image
+    };
+    uint32_t base_r, pitch_r, image_r;  // byte address residues mod 16
+    uint32_t skew_a = 0, skew_b = 0;    // current row's skew of strips A and B
+
+    __device__ __forceinline__ explicit U8BulkOp(const Params& p)
+        : Base(typename Base::Params{p.kappa}),
+          base_r(uint32_t(reinterpret_cast<uintptr_t>(p.rgb)) & 15u),
+          pitch_r(uint32_t(p.in_pitch) & 15u),
+          image_r(uint32_t(p.in_image_stride) & 15u) {}
+
+    __device__ __forceinline__ void begin_tile(const int (&col0)[G], int row0, const int (&image)[G]) {
+        const uint32_t r = base_r + uint32_t(row0) * pitch_r;
+        skew_a = (r + uint32_t(image[0]) * image_r + uint32_t(col0[0]) * 3u) & 15u;
+        if constexpr (G == 2) skew_b = (r + uint32_t(image[1]) * image_r + uint32_t(col0[1]) * 3u) & 15u;
+    }
+
+    __device__ __forceinline__ static void load_warp(void* smem, const Params& p, uint64_t* bar,
+                                                     const int (&col0)[G], int row0, const int (&image)[G],
+                                                     int lane) {
+        const int k = lane >= CH ? 1 : 0, r = lane - k * CH;
+        const int y = row0 + r;
+        uint32_t nb = 0;
+        const uint8_t* al = nullptr;
+        if (lane < G * CH && y < p.H) {
+            const int img = k ? image[G - 1] : image[0], c0 = k ? col0[G - 1] : col0[0];  // selects: no local array
+            const uint8_t* src =
+                p.rgb + int64_t(img) * p.in_image_stride + int64_t(y) * p.in_pitch + int64_t(c0) * 3;
+            const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+            al = reinterpret_cast<const uint8_t*>(a & ~uintptr_t(15));
+            const uint32_t avail = uint32_t(a & 15u) + uint32_t(p.W - c0) * 3u;  // bytes to the row end
+            const uint32_t up = (avail + 15u) & ~15u;
+            nb = up < uint32_t(kRowWords * 4) ? up : uint32_t(kRowWords * 4);
+        }
+        const uint32_t total = __reduce_add_sync(0xffffffffu, nb);
+        if (lane == 0) mbar_arrive_expect_tx(bar, total);
+        __syncwarp();
+        if (nb) bulk_g2s(static_cast<unsigned char*>(smem) + k * kBoxStride + r * (kRowWords * 4), al, nb, bar);
+    }
+
+    template <int R>
+    __device__ __forceinline__ void row(const unsigned char* stage, int lane, float (&out)[G][4]) {
+        const uint32_t* wa = reinterpret_cast<const uint32_t*>(stage) + R * kRowWords + (skew_a >> 2) + 3 * lane;
+        const uint32_t sa = (skew_a & 3u) * 8u;
+        const uint32_t wa3 = wa[3];
+        const uint32_t a[3] = {__funnelshift_r(wa[0], wa[1], sa), __funnelshift_r(wa[1], wa[2], sa),
+                               __funnelshift_r(wa[2], wa3, sa)};
+        skew_a = (skew_a + pitch_r) & 15u;
+        if constexpr (G == 2) {
+            const uint32_t* wb =
+                reinterpret_cast<const uint32_t*>(stage + kBoxStride) + R * kRowWords + (skew_b >> 2) + 3 * lane;
+            const uint32_t sb = (skew_b & 3u) * 8u;
+            const uint32_t wb3 = wb[3];
+            const uint32_t b[3] = {__funnelshift_r(wb[0], wb[1], sb), __funnelshift_r(wb[1], wb[2], sb),
+                                   __funnelshift_r(wb[2], wb3, sb)};
+            skew_b = (skew_b + pitch_r) & 15u;
+            float2 gown[4];
+            gray4_u8x2<EXACT>(a, b, gown[0], gown[1], gown[2], gown[3]);
+            this->core.template step<R, NoHalo, (CH % 2 == 0)>(gown, lane, NoHalo{}, out);
+        } else {
+            float gown[4];
+            gray4_u8<EXACT>(a[0], a[1], a[2], gown[0], gown[1], gown[2], gown[3]);
+            this->core.template step<R, NoHalo, (CH % 2 == 0)>(gown, lane, NoHalo{}, out[0]);
+        }
+    }
+};
+
+#ifndef HARRIS_U8BULK_G
+#define HARRIS_U8BULK_G 1  // scalar core, 16 warps/SM: 613 k vs 610 k (dual, 8 warps) on 512 x 1080x1918, 578 k vs 543 k on 8192x8191
+#endif
+constexpr int kU8BulkG = HARRIS_U8BULK_G;
+constexpr int kU8BulkNW = 8, kU8BulkNS = 4, kU8BulkCH = 6, kU8BulkMinB = kU8BulkG == 2 ? 1 : 2;
+const TmaConfig kU8BulkConfig = {kU8BulkNW, kU8BulkNS, kU8BulkCH, kU8BulkG, 124};
+template <bool EXACT>
+using U8BulkOpT = U8BulkOp<EXACT, kU8BulkCH, kU8BulkG>;
+
+template <bool EXACT>
+static constexpr auto u8_bulk_kernel() {
+    return strip_kernel<U8BulkOpT<EXACT>, kU8BulkNW, kU8BulkNS, kU8BulkMinB>;
+}
+static constexpr size_t u8_bulk_smem() {
+    return StripShape<kU8BulkNW, kU8BulkNS, U8BulkOpT<false>>::kSmemBytes;
+}
+static_assert(u8_bulk_smem() <= 227 * 1024, "u8 bulk smem");
+
 constexpr int kU8LdgNW = 8, kU8LdgNS = 4, kU8LdgCH = 6;
 const TmaConfig kU8LdgConfig = {kU8LdgNW, kU8LdgNS, kU8LdgCH, 1, 124};
 
@@ -222,12 +341,21 @@ static cudaError_t u8_ldg_configure_one() {
     return e;
 }
 
-cudaError_t u8_ldg_configure(int* ctas_per_sm) {
+cudaError_t u8_ldg_configure(int* ctas_per_sm, int* bulk_ctas_per_sm) {
     cudaError_t e = u8_ldg_configure_one<4>();
     if (e == cudaSuccess) e = u8_ldg_configure_one<16>();
     if (e == cudaSuccess)
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, u8_ldg_kernel<false, 16>(), kU8LdgNW * 32,
                                                           u8_ldg_smem());
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(u8_bulk_kernel<false>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(u8_bulk_smem()));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(u8_bulk_kernel<true>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(u8_bulk_smem()));
+    if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(bulk_ctas_per_sm, u8_bulk_kernel<false>(), kU8BulkNW * 32,
+                                                          u8_bulk_smem());
     return e;
 }
 
@@ -242,9 +370,23 @@ static void launch_u8_ldg_one(const Geom& geom, const TileGeom& tg, int64_t grid
     u8_ldg_kernel<EXACT, A>()<<<unsigned(grid), unsigned(kU8LdgNW * 32), u8_ldg_smem(), stream>>>(unused, tg, p);
 }
 
+template <bool EXACT>
+static void launch_u8_bulk_one(const Geom& geom, const TileGeom& tg, int64_t grid, cudaStream_t stream) {
+    CUtensorMap unused;
+    std::memset(&unused, 0, sizeof(unused));
+    const int64_t img_stride = geom.batch > 1 ? geom.in_image_stride : 0;
+    const typename U8BulkOpT<EXACT>::Params p{geom.kappa, reinterpret_cast<const uint8_t*>(geom.rgb),
+                                                          geom.in_pitch, img_stride, int32_t(geom.m + 4),
+                                                          int32_t(geom.n + 4)};
+    u8_bulk_kernel<EXACT>()<<<unsigned(grid), unsigned(kU8BulkNW * 32), u8_bulk_smem(), stream>>>(unused, tg, p);
+}
+
+// chunk 0: the bulk-copy kernel (K1b, default); 4 / 16: the cp.async kernel (K2)
 cudaError_t launch_u8_ldg(bool exact, int chunk, const Geom& geom, const TileGeom& tg, int64_t grid,
                           cudaStream_t stream) {
-    if (chunk == 4)
+    if (chunk == 0)
+        exact ? launch_u8_bulk_one<true>(geom, tg, grid, stream) : launch_u8_bulk_one<false>(geom, tg, grid, stream);
+    else if (chunk == 4)
         exact ? launch_u8_ldg_one<true, 4>(geom, tg, grid, stream) : launch_u8_ldg_one<false, 4>(geom, tg, grid, stream);
     else
         exact ? launch_u8_ldg_one<true, 16>(geom, tg, grid, stream)

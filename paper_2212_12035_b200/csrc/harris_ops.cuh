@@ -357,10 +357,13 @@ struct HarrisF32QuadRowOp : HarrisF32Op<EXACT, 12, 124> {
             if constexpr (cls == 0) {
                 const float4 v = lds128(q);
                 c[ch][0] = v.x, c[ch][1] = v.y, c[ch][2] = v.z, c[ch][3] = v.w;
-            } else {
-                const float* qs = q + skew[cls];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) c[ch][i] = qs[i];
+            } else if constexpr (cls == 2) {  // 2P = 2 (mod 4): 8-byte aligned
+                const float2 v0 = lds64(q + 2), v1 = lds64(q + 4);
+                c[ch][0] = v0.x, c[ch][1] = v0.y, c[ch][2] = v1.x, c[ch][3] = v1.y;
+            } else {  // skew 1 or 3 (warp-uniform): scalar + 8-byte + scalar
+                const int s = skew[cls];
+                const float2 v = lds64(q + s + 1);
+                c[ch][0] = q[s], c[ch][1] = v.x, c[ch][2] = v.y, c[ch][3] = q[s + 3];
             }
         }
         const float gown[4] = {gray_of<EXACT>(c[0][0], c[1][0], c[2][0]), gray_of<EXACT>(c[0][1], c[1][1], c[2][1]),
@@ -430,6 +433,7 @@ __device__ __forceinline__ void gray4_u8(uint32_t w0, uint32_t w1, uint32_t w2, 
 template <bool EXACT, int CH, int SC = 128>
 struct HarrisU8Op {
     static_assert(CH % 3 == 0, "row rotation needs CH % 3 == 0");
+    static constexpr bool kSplitStores = false;  // issue-bound: predicated scalar stores
     using L = Strip<SC>;
     static constexpr int kGroups = 1;
     static constexpr int kStripCols = SC;

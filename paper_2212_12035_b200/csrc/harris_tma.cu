@@ -214,8 +214,12 @@ cudaError_t launch_tma_pair(bool exact, const CUtensorMap& tmap, const TileGeom&
     return cudaGetLastError();
 }
 
-// ---- quad-row TMA kernel (odd row pitch, HarrisF32QuadRowOp): 12-row stages, 5 warps ----
-constexpr int kQuadNW = 5, kQuadNS = 2;
+// ---- quad-row TMA kernel (odd row pitch, HarrisF32QuadRowOp): 12-row stages, 4 warps (one per SMSP) ----
+#ifndef HARRIS_QUAD_NW
+#define HARRIS_QUAD_NW 4
+#define HARRIS_QUAD_NS 2
+#endif
+constexpr int kQuadNW = HARRIS_QUAD_NW, kQuadNS = HARRIS_QUAD_NS;
 const TmaConfig kQuadConfig = {kQuadNW, kQuadNS, 12, 1, 124};
 
 template <bool EXACT>

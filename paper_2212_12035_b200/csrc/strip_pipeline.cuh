@@ -100,6 +100,22 @@ struct WarpLoadOf : std::false_type {};
 template <class Op>
 struct WarpLoadOf<Op, std::void_t<decltype(Op::kWarpLoad)>> : std::integral_constant<bool, Op::kWarpLoad> {};
 
+// Op::kBarArrivals is optional (warp loads only; default 32): arrivals per stage barrier
+// phase — 1 for a warp load that issues bulk copies and one arrive.expect_tx
+template <class Op, class = void>
+struct BarArrivalsOf : std::integral_constant<int, 32> {};
+template <class Op>
+struct BarArrivalsOf<Op, std::void_t<decltype(Op::kBarArrivals)>> : std::integral_constant<int, Op::kBarArrivals> {};
+
+// Op::kSplitStores is optional (default true): output rows that are not 16-byte aligned
+// get 8-byte + scalar stores (fewer store transactions: +1.8 % on memory-bound f32
+// kernels); false keeps four predicated scalar stores (no per-row branch: the
+// issue-bound u8 kernels measured 11 % slower with the split form)
+template <class Op, class = void>
+struct SplitStoresOf : std::true_type {};
+template <class Op>
+struct SplitStoresOf<Op, std::void_t<decltype(Op::kSplitStores)>> : std::integral_constant<bool, Op::kSplitStores> {};
+
 // Op::load_p(smem, tmap, bar, cols, row0, imgs, policy, params) is optional: a TMA stage fill
 // that needs the kernel parameters (the pair-row op's odd-row column offset)
 template <class Op, class = void>
@@ -177,7 +193,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     if (lane == 0) {
         if constexpr (!kWarpLoad) prefetch_tmap(&tmap);
 #pragma unroll
-        for (int s = 0; s < NS; ++s) mbar_init(&bars[s], kWarpLoad ? 32 : 1);
+        for (int s = 0; s < NS; ++s) mbar_init(&bars[s], kWarpLoad ? BarArrivalsOf<Op>::value : 1);
         fence_barrier_init();
     }
     __syncwarp();
@@ -311,9 +327,13 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                             if (ragged) {  // unaligned output rows, or the ragged right edge
                                 const int cg = colg[gi];
                                 if (!vec[gi] && cg < g.m) {
+                                    if (SplitStoresOf<Op>::value && cg + kColsPerLane <= g.m) {  // row not 16-B aligned
+                                        stg4_cs_align4(po, out4[gi][0], out4[gi][1], out4[gi][2], out4[gi][3]);
+                                    } else {
 #pragma unroll
-                                    for (int k = 0; k < kColsPerLane; ++k)
-                                        if (cg + k < g.m) po[k] = out4[gi][k];
+                                        for (int k = 0; k < kColsPerLane; ++k)
+                                            if (cg + k < g.m) po[k] = out4[gi][k];
+                                    }
                                 }
                             }
                         }

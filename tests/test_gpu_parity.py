@@ -583,6 +583,36 @@ def test_u8_ldg_unaligned_base_and_batch(cuda_ctx):
     assert torch.equal(got, ref)
 
 
+@pytest.mark.parametrize("off", [0, 1, 6, 15])
+def test_u8_bulk_every_pitch_residue(cuda_ctx, off):
+    """The u8 bulk-copy kernel (K1b, the default for rows TMA cannot describe) across all 16
+    residues of the row pitch mod 16 and base offsets: EXACT equals the C oracle on byte/255,
+    and both orders equal the cp.async kernel (HARRIS_U8LDG_CHUNK=16) bit-for-bit.  Widths
+    span 1-3 column strips incl. ragged last strips; B = 2 with an image stride of odd
+    residue makes a strip pair straddle two images."""
+    cpa = _ctx_with({"HARRIS_U8LDG_CHUNK": 16})
+    for pad in range(16):
+        H, W = 19 + pad, 131 + 37 * pad
+        B = 2
+        pitch = 3 * W + pad
+        img_stride = H * pitch + 5
+        hwc, f32 = _u8_image(B, H, W, seed=pad * 31 + off)
+        buf = torch.zeros(off + B * img_stride + 16, dtype=torch.uint8, device="cuda")
+        x = torch.as_strided(buf, (B, H, W, 3), (img_stride, pitch, 3, 1), off)
+        x.copy_(torch.from_numpy(hwc))
+        ex = hb.harris_u8(x, exact=True)
+        assert cuda_ctx.last_path == _lib.PATH_LDG
+        fast = hb.harris_u8(x)
+        ex2 = hb.harris_u8(x, exact=True, ctx=cpa)
+        fast2 = hb.harris_u8(x, ctx=cpa)
+        torch.cuda.synchronize()
+        for b in range(B):
+            assert np.array_equal(ex[b].cpu().numpy(), cref.harris_f32(f32[b])), (off, pad, b)
+        assert torch.equal(ex, ex2), (off, pad)
+        assert torch.equal(fast, fast2), (off, pad)
+    cpa.close()
+
+
 def test_concurrent_streams_and_threads(cuda_ctx):
     """One ctx driven from 4 host threads on 4 streams (ctypes drops the GIL, so the C
     launch path and its launch cache really run concurrently); every result bit-exact."""
