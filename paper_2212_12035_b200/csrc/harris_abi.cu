@@ -43,7 +43,8 @@ struct harris_ctx {
     int occ_quad = 0;
     int occ_sepldg = 0;
     int u8ldg_chunk = 0;  // HARRIS_U8LDG_CHUNK: 0 bulk-copy kernel (K1b); 4 / 16-byte cp.async (K2)
-    int ldg_cfg = 2;  // HARRIS_LDG_CONFIG; 2 = scalar lane-halo core, 16 warps/SM (284 k MP/s on 8190^2)
+    int ldg_cfg = 3;  // HARRIS_LDG_CONFIG; 3 = bulk-copy rows + scalar lane-halo core, 16 warps/SM (K1b:
+                      // 404 k MP/s on a column-crop view of 256 x 1080p; the cp.async config 2: 296 k)
     int sync_waves = 1;  // dev knob HARRIS_SYNC_WAVES=0 disables the per-tile CTA barrier
     int l2_policy = 1;  // evict_normal: the 4-column halo sectors are re-read by the neighbouring strip
     int64_t force_band_rows = 0;  // dev knob (HARRIS_BAND_ROWS): override the planner

@@ -71,7 +71,7 @@ cudaError_t launch_tma_quad(bool exact, const CUtensorMap& tmap, const TileGeom&
 
 // cp.async (LDGSTS) warp-strip kernel for f32 inputs TMA cannot describe (row pitch or
 // base not 16-byte aligned): same engine and dual-strip core as the TMA path
-constexpr int kNumLdgConfigs = 3;
+constexpr int kNumLdgConfigs = 5;
 extern const TmaConfig kLdgConfigs[kNumLdgConfigs];
 cudaError_t ldg_configure(int cfg, int* ctas_per_sm);
 cudaError_t launch_ldg(int cfg, bool exact, const Geom& g, const TileGeom& tg, int64_t grid, cudaStream_t stream);

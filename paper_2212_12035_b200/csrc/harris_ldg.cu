@@ -123,6 +123,121 @@ struct LdgOp : BaseOp {
     }
 };
 
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(smem)),
+                 "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// ---- planar f32 through the bulk-copy engine (K1b): every (channel, row) of a stage is
+// ONE cp.async.bulk of <= 544 bytes from the row's 16-byte aligned-down start, issued by
+// its own lane (G * 3 * CH <= 32 copies: the stage fill is one warp instruction), counted
+// as transaction bytes on the stage mbarrier.  The consumer reads each lane's 4 floats
+// at the row's float skew s (0..3; per strip and channel, advancing by pitch mod 4 per
+// row): s even -> two 8-byte loads, s odd -> scalar + 8-byte + scalar, then the unchanged
+// TMA-path core (no row-pair sums: FAST bit-identical to every other f32 path).
+template <bool EXACT, int CH, int G>
+struct F32BulkOp : std::conditional_t<G == 2, HarrisF32x2Op<EXACT, CH, 124>, HarrisF32Op<EXACT, CH, 124>> {
+    using Base = std::conditional_t<G == 2, HarrisF32x2Op<EXACT, CH, 124>, HarrisF32Op<EXACT, CH, 124>>;
+    static_assert(G * 3 * CH <= 32, "one lane per stage row");
+    static constexpr bool kWarpLoad = true;
+    static constexpr int kBarArrivals = 1;
+    static constexpr bool kCacheProducer = true;
+    static constexpr int kRowFloats = 136;  // 544 B >= 3 skew floats + 128 columns, 16-byte multiple
+    static constexpr uint32_t kBoxBytes = 3u * CH * kRowFloats * 4u;
+    static constexpr uint32_t kBoxStride = (kBoxBytes + 127u) / 128u * 128u;
+    static constexpr uint32_t kStageBytes = uint32_t(G) * kBoxStride;
+    struct Params {
+        typename Base::Params base;
+        const float* src;
+        int64_t in_pitch, in_plane_stride, in_image_stride;  // elements
+        int32_t W, H;                                        // input columns / rows per image
+    };
+    uint32_t base_r, pitch_r, plane_r, image_r;  // float-index residues mod 4
+    uint32_t sk[G][3];                           // current row's skew per strip and channel
+
+    __device__ __forceinline__ explicit F32BulkOp(const Params& p)
+        : Base(p.base),
+          base_r(uint32_t(reinterpret_cast<uintptr_t>(p.src) >> 2) & 3u),
+          pitch_r(uint32_t(p.in_pitch) & 3u),
+          plane_r(uint32_t(p.in_plane_stride) & 3u),
+          image_r(uint32_t(p.in_image_stride) & 3u) {}
+
+    __device__ __forceinline__ void begin_tile(const int (&col0)[G], int row0, const int (&image)[G]) {
+#pragma unroll
+        for (int k = 0; k < G; ++k) {
+            const uint32_t s = base_r + uint32_t(image[k]) * image_r + uint32_t(row0) * pitch_r + uint32_t(col0[k]);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) sk[k][c] = (s + uint32_t(c) * plane_r) & 3u;
+        }
+    }
+
+    __device__ __forceinline__ static void load_warp(void* smem, const Params& p, uint64_t* bar,
+                                                     const int (&col0)[G], int row0, const int (&image)[G],
+                                                     int lane) {
+        const int k = lane >= 3 * CH ? 1 : 0, rem = lane - k * 3 * CH;
+        const int ch = rem / CH, r = rem - ch * CH;
+        const int y = row0 + r;
+        uint32_t nb = 0;
+        const float* al = nullptr;
+        if (lane < G * 3 * CH && y < p.H) {
+            const int img = k ? image[G - 1] : image[0], c0 = k ? col0[G - 1] : col0[0];  // selects: no local array
+            const float* src = p.src + int64_t(img) * p.in_image_stride + int64_t(ch) * p.in_plane_stride +
+                               int64_t(y) * p.in_pitch + c0;
+            const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+            al = reinterpret_cast<const float*>(a & ~uintptr_t(15));
+            const uint32_t avail = uint32_t(a & 15u) + uint32_t(p.W - c0) * 4u;  // bytes to the row end
+            const uint32_t up = (avail + 15u) & ~15u;
+            nb = up < uint32_t(kRowFloats * 4) ? up : uint32_t(kRowFloats * 4);
+        }
+        const uint32_t total = __reduce_add_sync(0xffffffffu, nb);
+        if (lane == 0) mbar_arrive_expect_tx(bar, total);
+        __syncwarp();
+        if (nb)
+            bulk_g2s(static_cast<unsigned char*>(smem) + k * kBoxStride + (ch * CH + r) * (kRowFloats * 4), al, nb,
+                     bar);
+    }
+
+    // 4 floats at q + s (q 16-byte aligned, s warp-uniform in 0..3)
+    __device__ __forceinline__ static void read4(const float* q, uint32_t s, float (&c)[4]) {
+        if (s & 1u) {
+            const float2 v = lds64(q + s + 1);
+            c[0] = q[s], c[1] = v.x, c[2] = v.y, c[3] = q[s + 3];
+        } else {
+            const float2 v0 = lds64(q + s), v1 = lds64(q + s + 2);
+            c[0] = v0.x, c[1] = v0.y, c[2] = v1.x, c[3] = v1.y;
+        }
+    }
+
+    template <int R>
+    __device__ __forceinline__ void row(const unsigned char* stage, int lane, float (&out)[G][4]) {
+        float v[G][3][4];
+#pragma unroll
+        for (int k = 0; k < G; ++k) {
+            const float* box = reinterpret_cast<const float*>(stage + k * kBoxStride);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                read4(box + (c * CH + R) * kRowFloats + 4 * lane, sk[k][c], v[k][c]);
+                sk[k][c] = (sk[k][c] + pitch_r) & 3u;
+            }
+        }
+        if constexpr (G == 2) {
+            float2 gown[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                gown[i] = make_float2(gray_of<EXACT>(v[0][0][i], v[0][1][i], v[0][2][i]),
+                                      gray_of<EXACT>(v[1][0][i], v[1][1][i], v[1][2][i]));
+            this->core.template step<R>(gown, lane, NoHalo{}, out);
+        } else {
+            float gown[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) gown[i] = gray_of<EXACT>(v[0][0][i], v[0][1][i], v[0][2][i]);
+            this->core.template step<R, NoHalo, false>(gown, lane, NoHalo{}, out[0]);
+        }
+    }
+};
+
 // ---- interleaved u8 (HWC) rows at any byte alignment.  TMA needs 16-byte row strides
 // (3W % 16 == 0); other widths get 4-byte cp.async of the row's words from its 4-byte
 // aligned-down start, and the consumer realigns each lane's 3 words with funnel shifts by
@@ -212,12 +327,6 @@ struct U8LdgOp : HarrisU8Op<EXACT, CH, 124> {
 // clamped to the 16-byte block holding the row's last byte, so it never leaves the page of
 // a valid byte; rows below the image are not copied and columns beyond the row end are
 // stale — neither reaches a stored output.
-__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(smem)),
-                 "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
 
 template <bool EXACT, int CH, int G>
 struct U8BulkOp : std::conditional_t<G == 2, HarrisU8x2Op<EXACT, CH, 124>, HarrisU8Op<EXACT, CH, 124>> {
@@ -419,7 +528,22 @@ struct LdgCfg<2> {
     using Op = LdgOp<HarrisF32Op<EXACT, CH, 124>, 4>;
 };
 
-const TmaConfig kLdgConfigs[kNumLdgConfigs] = {{8, 2, 3, 2, 128}, {8, 2, 3, 1, 128}, {8, 2, 3, 1, 124}};
+// 3 / 4 = the bulk-copy engine (K1b) with the scalar / packed dual-strip core
+template <>
+struct LdgCfg<3> {
+    static constexpr int NW = 8, NS = 2, CH = 3, MINB = 2, G = 1;
+    template <bool EXACT>
+    using Op = F32BulkOp<EXACT, CH, 1>;
+};
+template <>
+struct LdgCfg<4> {
+    static constexpr int NW = 8, NS = 2, CH = 3, MINB = 1, G = 2;
+    template <bool EXACT>
+    using Op = F32BulkOp<EXACT, CH, 2>;
+};
+
+const TmaConfig kLdgConfigs[kNumLdgConfigs] = {
+    {8, 2, 3, 2, 128}, {8, 2, 3, 1, 128}, {8, 2, 3, 1, 124}, {8, 2, 3, 1, 124}, {8, 2, 3, 2, 124}};
 
 template <int CFG, bool EXACT>
 static constexpr auto ldg_kernel() {
@@ -431,7 +555,8 @@ static constexpr size_t ldg_smem() {
     using C = LdgCfg<CFG>;
     return StripShape<C::NW, C::NS, typename C::template Op<false>>::kSmemBytes;
 }
-static_assert(ldg_smem<0>() <= 227 * 1024 && ldg_smem<1>() <= 227 * 1024 && ldg_smem<2>() <= 227 * 1024,
+static_assert(ldg_smem<0>() <= 227 * 1024 && ldg_smem<1>() <= 227 * 1024 && ldg_smem<2>() <= 227 * 1024 &&
+                  ldg_smem<3>() <= 227 * 1024 && ldg_smem<4>() <= 227 * 1024,
               "ldg smem");
 
 template <int CFG>
@@ -448,9 +573,11 @@ static cudaError_t ldg_configure_one(int* ctas_per_sm) {
 }
 
 cudaError_t ldg_configure(int cfg, int* ctas_per_sm) {
-    return cfg == 0 ? ldg_configure_one<0>(ctas_per_sm)
+    return cfg == 0   ? ldg_configure_one<0>(ctas_per_sm)
            : cfg == 1 ? ldg_configure_one<1>(ctas_per_sm)
-                      : ldg_configure_one<2>(ctas_per_sm);
+           : cfg == 2 ? ldg_configure_one<2>(ctas_per_sm)
+           : cfg == 3 ? ldg_configure_one<3>(ctas_per_sm)
+                      : ldg_configure_one<4>(ctas_per_sm);
 }
 
 template <int CFG, bool EXACT>
@@ -470,21 +597,100 @@ cudaError_t launch_ldg(int cfg, bool exact, const Geom& geom, const TileGeom& tg
         exact ? launch_ldg_one<0, true>(geom, tg, grid, stream) : launch_ldg_one<0, false>(geom, tg, grid, stream);
     else if (cfg == 1)
         exact ? launch_ldg_one<1, true>(geom, tg, grid, stream) : launch_ldg_one<1, false>(geom, tg, grid, stream);
-    else
+    else if (cfg == 2)
         exact ? launch_ldg_one<2, true>(geom, tg, grid, stream) : launch_ldg_one<2, false>(geom, tg, grid, stream);
+    else if (cfg == 3)
+        exact ? launch_ldg_one<3, true>(geom, tg, grid, stream) : launch_ldg_one<3, false>(geom, tg, grid, stream);
+    else
+        exact ? launch_ldg_one<4, true>(geom, tg, grid, stream) : launch_ldg_one<4, false>(geom, tg, grid, stream);
     return cudaGetLastError();
 }
+
+// ---- separable 3x3 stencil through the bulk-copy engine (K1b): one cp.async.bulk per
+// stage row (<= 544 B from the 16-byte aligned-down start), the consumer reads its 6
+// floats at the row's float skew (even: three 8-byte loads; odd: scalar + 2 x 8-byte +
+// scalar) and runs the unchanged Sep3x3Op arithmetic
+template <bool EXACT, int CH>
+struct SepBulkOp : Sep3x3Op<EXACT, CH> {
+    using Base = Sep3x3Op<EXACT, CH>;
+    static_assert(CH <= 32, "one lane per stage row");
+    static constexpr bool kWarpLoad = true;
+    static constexpr int kBarArrivals = 1;
+    static constexpr bool kCacheProducer = true;
+    static constexpr int kRowFloats = 136;  // 3 skew floats + 130 columns, 16-byte multiple
+    static constexpr uint32_t kStageBytes = (uint32_t(CH) * kRowFloats * 4u + 127u) / 128u * 128u;
+    struct Params {
+        typename Base::Params base;
+        const float* src;
+        int64_t in_pitch, in_plane_stride, in_image_stride;  // elements (plane stride unused)
+        int32_t W, H;
+    };
+    uint32_t base_r, pitch_r, image_r, sk = 0;
+
+    __device__ __forceinline__ explicit SepBulkOp(const Params& p)
+        : Base(p.base),
+          base_r(uint32_t(reinterpret_cast<uintptr_t>(p.src) >> 2) & 3u),
+          pitch_r(uint32_t(p.in_pitch) & 3u),
+          image_r(uint32_t(p.in_image_stride) & 3u) {}
+
+    __device__ __forceinline__ void begin_tile(const int (&col0)[1], int row0, const int (&image)[1]) {
+        sk = (base_r + uint32_t(image[0]) * image_r + uint32_t(row0) * pitch_r + uint32_t(col0[0])) & 3u;
+    }
+
+    __device__ __forceinline__ static void load_warp(void* smem, const Params& p, uint64_t* bar,
+                                                     const int (&col0)[1], int row0, const int (&image)[1],
+                                                     int lane) {
+        const int y = row0 + lane;
+        uint32_t nb = 0;
+        const float* al = nullptr;
+        if (lane < CH && y < p.H) {
+            const float* src = p.src + int64_t(image[0]) * p.in_image_stride + int64_t(y) * p.in_pitch + col0[0];
+            const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+            al = reinterpret_cast<const float*>(a & ~uintptr_t(15));
+            const uint32_t avail = uint32_t(a & 15u) + uint32_t(p.W - col0[0]) * 4u;
+            const uint32_t up = (avail + 15u) & ~15u;
+            nb = up < uint32_t(kRowFloats * 4) ? up : uint32_t(kRowFloats * 4);
+        }
+        const uint32_t total = __reduce_add_sync(0xffffffffu, nb);
+        if (lane == 0) mbar_arrive_expect_tx(bar, total);
+        __syncwarp();
+        if (nb) bulk_g2s(static_cast<unsigned char*>(smem) + lane * (kRowFloats * 4), al, nb, bar);
+    }
+
+    template <int R>
+    __device__ __forceinline__ void row(const unsigned char* stage, int lane, float (&out4)[1][4]) {
+        const float* q = reinterpret_cast<const float*>(stage) + R * kRowFloats + 4 * lane;
+        float x[6];
+        if (sk & 1u) {
+            const float2 u = lds64(q + sk + 1), v = lds64(q + sk + 3);
+            x[0] = q[sk], x[1] = u.x, x[2] = u.y, x[3] = v.x, x[4] = v.y, x[5] = q[sk + 5];
+        } else {
+            const float2 u = lds64(q + sk), v = lds64(q + sk + 2), w = lds64(q + sk + 4);
+            x[0] = u.x, x[1] = u.y, x[2] = v.x, x[3] = v.y, x[4] = w.x, x[5] = w.y;
+        }
+        sk = (sk + pitch_r) & 3u;
+        this->template compute<R>(x, out4[0]);
+    }
+};
 
 // ---- separable 3x3 stencil on planes TMA cannot describe (pitch % 4 != 0 / base) ----
 constexpr int kSepLdgNW = 8, kSepLdgNS = 8, kSepLdgCH = 6;
 const TmaConfig kSepLdgConfig = {kSepLdgNW, kSepLdgNS, kSepLdgCH, 1, 128};
 
+#ifndef HARRIS_SEP_CPASYNC
+template <bool EXACT>
+using SepLdgOpT = SepBulkOp<EXACT, kSepLdgCH>;
+#else
+template <bool EXACT>
+using SepLdgOpT = LdgOp<Sep3x3Op<EXACT, kSepLdgCH>, 4>;
+#endif
+
 template <bool EXACT>
 static constexpr auto sep_ldg_kernel() {
-    return strip_kernel<LdgOp<Sep3x3Op<EXACT, kSepLdgCH>, 4>, kSepLdgNW, kSepLdgNS, 1>;
+    return strip_kernel<SepLdgOpT<EXACT>, kSepLdgNW, kSepLdgNS, 1>;
 }
 static constexpr size_t sep_ldg_smem() {
-    return StripShape<kSepLdgNW, kSepLdgNS, LdgOp<Sep3x3Op<false, kSepLdgCH>, 4>>::kSmemBytes;
+    return StripShape<kSepLdgNW, kSepLdgNS, SepLdgOpT<false>>::kSmemBytes;
 }
 static_assert(sep_ldg_smem() <= 227 * 1024, "stencil ldg smem");
 
@@ -506,7 +712,7 @@ static void launch_sep_ldg_one(const float* in, int64_t in_pitch, int64_t in_ima
                                cudaStream_t stream) {
     CUtensorMap unused;
     std::memset(&unused, 0, sizeof(unused));
-    using Op = LdgOp<Sep3x3Op<EXACT, kSepLdgCH>, 4>;
+    using Op = SepLdgOpT<EXACT>;
     const typename Op::Params p{{{wv[0], wv[1], wv[2]}, {wh[0], wh[1], wh[2]}}, in, in_pitch, 0, in_image_stride, W,
                                 H};
     sep_ldg_kernel<EXACT>()<<<unsigned(grid), unsigned(kSepLdgNW * 32), sep_ldg_smem(), stream>>>(unused, tg, p);

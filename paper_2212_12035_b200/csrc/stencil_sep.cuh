@@ -43,17 +43,19 @@ struct Sep3x3Op {
 
     template <int R>
     __device__ __forceinline__ void row(const unsigned char* stage, int lane, float (&out4)[1][4]) {
-        float(&out)[4] = out4[0];
-        constexpr int s2 = R % 3, s0 = (R + 1) % 3, s1 = (R + 2) % 3;
         const float* rp = reinterpret_cast<const float*>(stage) + R * kBoxCols + lane * 4;
         const float4 a = lds128(rp);
         const float2 b = *reinterpret_cast<const float2*>(rp + 4);
-        X[s2][0] = a.x;
-        X[s2][1] = a.y;
-        X[s2][2] = a.z;
-        X[s2][3] = a.w;
-        X[s2][4] = b.x;
-        X[s2][5] = b.y;
+        const float x[6] = {a.x, a.y, a.z, a.w, b.x, b.y};
+        compute<R>(x, out4[0]);
+    }
+
+    // input row R (6 columns of this lane: its 4 + the 2-column halo) -> 4 outputs
+    template <int R>
+    __device__ __forceinline__ void compute(const float (&x)[6], float (&out)[4]) {
+        constexpr int s2 = R % 3, s0 = (R + 1) % 3, s1 = (R + 2) % 3;
+#pragma unroll
+        for (int j = 0; j < 6; ++j) X[s2][j] = x[j];
         float v[6];
 #pragma unroll
         for (int j = 0; j < 6; ++j) {

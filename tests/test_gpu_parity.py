@@ -370,6 +370,26 @@ def test_stencil_batched_and_views(cuda_ctx):
     assert torch.equal(band, got[1, 10:28])
 
 
+@pytest.mark.parametrize("off", [0, 1, 2, 3])
+def test_stencil_unaligned_layouts(cuda_ctx, off):
+    """Planes TMA cannot describe (base offset, pitch residues 1..3, odd image stride): the
+    bulk-copy stencil kernel equals the C oracle bit-for-bit in EXACT order."""
+    for pad in range(4):
+        B, H, W = 2, 23 + pad, 130 + 61 * pad
+        pitch = W + pad
+        img_stride = H * pitch + 3
+        imgs = synth.synth_numpy(B, H, W, seed=11 * pad + off)
+        buf = torch.zeros(off + B * img_stride + 8, device="cuda")
+        x = torch.as_strided(buf, (B, H, W), (img_stride, pitch, 1), off)
+        x.copy_(torch.from_numpy(imgs))
+        got = hb.stencil3x3_sep(x, exact=True)
+        aligned = off == 0 and pitch % 4 == 0 and img_stride % 4 == 0
+        assert cuda_ctx.last_path == (_lib.PATH_TMA if aligned else _lib.PATH_LDG)
+        torch.cuda.synchronize()
+        for b in range(B):
+            assert np.array_equal(got[b].cpu().numpy(), cref.sep3x3_f32(imgs[b])), (off, pad, b)
+
+
 def _ctx_with(env: dict):
     import os
     old = {k: os.environ.get(k) for k in env}
@@ -524,7 +544,7 @@ def test_ldg_unaligned_base_batch_and_bands(cuda_ctx):
     assert torch.equal(r_ldg, r_tma)
 
 
-@pytest.mark.parametrize("cfg", [0, 1, 2])
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3, 4])
 def test_every_ldg_config_bitexact(cuda_ctx, cfg):
     ctx = _ctx_with({"HARRIS_LDG_CONFIG": cfg})
     for B, H, W in [(1, 9, 131), (1, 70, 261), (3, 41, 387), (1, 302, 2563), (5, 21, 137)]:
