@@ -95,6 +95,7 @@ struct LdgOp : BaseOp {
         const float* src;
         int64_t in_pitch, in_plane_stride, in_image_stride;  // elements
         int32_t W, H;                                        // input columns / rows per image
+        const void* limit;  // one past the view's last element (used by the bulk-copy ops)
     };
 
     __device__ __forceinline__ explicit LdgOp(const Params& p) : BaseOp(p.base) {}
@@ -130,6 +131,58 @@ __device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t 
                  : "memory");
 }
 
+// The stage fill of the bulk-copy ops: each active lane copies one stage row — the bytes
+// [src, src + need) (need: to the row end, capped by the slot) — as ONE bulk copy from the
+// 16-byte aligned-down start, rounded up to whole 16-byte blocks.  Where that rounding would
+// read past the view's last byte (`limit`; only an image's last row can reach it, flagged
+// by `last_row`, so the test stays off every other row's path), the bulk part stops at the
+// last whole block and the lane copies the < 16-byte tail itself with plain loads and
+// shared stores, so no byte outside the view is ever read (compute-sanitizer memcheck
+// clean with exact-size allocations).  The warp then syncs (ordering the tail stores before
+// lane 0's release) and lane 0 arms the barrier with the warp's bulk bytes.
+constexpr int kBulkBarArrivals = 1;
+// cold path of bulk_stage_fill, out of line so the stage-fill path stays straight-line:
+// shrink the bulk part to the whole 16-byte blocks before `limit` and copy the rest of the
+// view's last bytes with plain loads / shared stores; returns the new bulk size
+__device__ __noinline__ uint32_t bulk_tail_fix(unsigned char* dst, const unsigned char* al, const void* limit,
+                                               uint32_t nb) {
+    const uintptr_t room = reinterpret_cast<uintptr_t>(limit) - reinterpret_cast<uintptr_t>(al);
+    if (room >= nb) return nb;
+    const uint32_t whole = uint32_t(room) & ~15u;
+    for (uint32_t i = whole; i < uint32_t(room); ++i) {
+        uint32_t v;
+        asm volatile("ld.global.nc.u8 %0, [%1];" : "=r"(v) : "l"(al + i));
+        asm volatile("st.shared.u8 [%0], %1;" ::"r"(smem_u32(dst + i)), "r"(v));
+    }
+    return whole;
+}
+
+// STRICT (chosen by the host only when the view's end is not 16-byte aligned, i.e. when the
+// rounding can reach past it): the stage that holds an image's last row (warp-uniform test)
+// sends that row's lane through bulk_tail_fix.  A separate instantiation because even the
+// untaken test measured 2-6 % slower on every other stage.
+template <bool STRICT>
+__device__ __forceinline__ void bulk_stage_fill(unsigned char* dst, const void* src, uint32_t need, uint32_t cap,
+                                                const void* limit, uint64_t* bar, bool active,
+                                                bool stage_has_last_row, bool last_row, int lane) {
+    uint32_t nb = 0;
+    const unsigned char* al = nullptr;
+    if (active) {
+        const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+        al = reinterpret_cast<const unsigned char*>(a & ~uintptr_t(15));
+        const uint32_t up0 = (uint32_t(a & 15u) + need + 15u) & ~15u;
+        nb = up0 < cap ? up0 : cap;
+    }
+    if constexpr (STRICT) {
+        if (stage_has_last_row && active && last_row) nb = bulk_tail_fix(dst, al, limit, nb);
+    }
+    const uint32_t total = __reduce_add_sync(0xffffffffu, nb);
+    if constexpr (STRICT) __syncwarp();  // the tail's shared stores before lane 0's release
+    if (lane == 0) mbar_arrive_expect_tx(bar, total);
+    __syncwarp();
+    if (nb) bulk_g2s(dst, al, nb, bar);
+}
+
 // ---- planar f32 through the bulk-copy engine (K1b): every (channel, row) of a stage is
 // ONE cp.async.bulk of <= 544 bytes from the row's 16-byte aligned-down start, issued by
 // its own lane (G * 3 * CH <= 32 copies: the stage fill is one warp instruction), counted
@@ -137,12 +190,12 @@ __device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t 
 // at the row's float skew s (0..3; per strip and channel, advancing by pitch mod 4 per
 // row): s even -> two 8-byte loads, s odd -> scalar + 8-byte + scalar, then the unchanged
 // TMA-path core (no row-pair sums: FAST bit-identical to every other f32 path).
-template <bool EXACT, int CH, int G>
+template <bool EXACT, int CH, int G, bool STRICT = false>
 struct F32BulkOp : std::conditional_t<G == 2, HarrisF32x2Op<EXACT, CH, 124>, HarrisF32Op<EXACT, CH, 124>> {
     using Base = std::conditional_t<G == 2, HarrisF32x2Op<EXACT, CH, 124>, HarrisF32Op<EXACT, CH, 124>>;
     static_assert(G * 3 * CH <= 32, "one lane per stage row");
     static constexpr bool kWarpLoad = true;
-    static constexpr int kBarArrivals = 1;
+    static constexpr int kBarArrivals = kBulkBarArrivals;
     static constexpr bool kCacheProducer = true;
     static constexpr int kRowFloats = 136;  // 544 B >= 3 skew floats + 128 columns, 16-byte multiple
     static constexpr uint32_t kBoxBytes = 3u * CH * kRowFloats * 4u;
@@ -153,6 +206,7 @@ struct F32BulkOp : std::conditional_t<G == 2, HarrisF32x2Op<EXACT, CH, 124>, Har
         const float* src;
         int64_t in_pitch, in_plane_stride, in_image_stride;  // elements
         int32_t W, H;                                        // input columns / rows per image
+        const void* limit;                                   // one past the view's last element
     };
     uint32_t base_r, pitch_r, plane_r, image_r;  // float-index residues mod 4
     uint32_t sk[G][3];                           // current row's skew per strip and channel
@@ -179,24 +233,12 @@ struct F32BulkOp : std::conditional_t<G == 2, HarrisF32x2Op<EXACT, CH, 124>, Har
         const int k = lane >= 3 * CH ? 1 : 0, rem = lane - k * 3 * CH;
         const int ch = rem / CH, r = rem - ch * CH;
         const int y = row0 + r;
-        uint32_t nb = 0;
-        const float* al = nullptr;
-        if (lane < G * 3 * CH && y < p.H) {
-            const int img = k ? image[G - 1] : image[0], c0 = k ? col0[G - 1] : col0[0];  // selects: no local array
-            const float* src = p.src + int64_t(img) * p.in_image_stride + int64_t(ch) * p.in_plane_stride +
-                               int64_t(y) * p.in_pitch + c0;
-            const uintptr_t a = reinterpret_cast<uintptr_t>(src);
-            al = reinterpret_cast<const float*>(a & ~uintptr_t(15));
-            const uint32_t avail = uint32_t(a & 15u) + uint32_t(p.W - c0) * 4u;  // bytes to the row end
-            const uint32_t up = (avail + 15u) & ~15u;
-            nb = up < uint32_t(kRowFloats * 4) ? up : uint32_t(kRowFloats * 4);
-        }
-        const uint32_t total = __reduce_add_sync(0xffffffffu, nb);
-        if (lane == 0) mbar_arrive_expect_tx(bar, total);
-        __syncwarp();
-        if (nb)
-            bulk_g2s(static_cast<unsigned char*>(smem) + k * kBoxStride + (ch * CH + r) * (kRowFloats * 4), al, nb,
-                     bar);
+        const int img = k ? image[G - 1] : image[0], c0 = k ? col0[G - 1] : col0[0];  // selects: no local array
+        const float* src =
+            p.src + int64_t(img) * p.in_image_stride + int64_t(ch) * p.in_plane_stride + int64_t(y) * p.in_pitch + c0;
+        bulk_stage_fill<STRICT>(static_cast<unsigned char*>(smem) + k * kBoxStride + (ch * CH + r) * (kRowFloats * 4), src,
+                        uint32_t(p.W - c0) * 4u, kRowFloats * 4, p.limit, bar, lane < G * 3 * CH && y < p.H,
+                        row0 + CH > p.H - 1 && row0 <= p.H - 1, y == p.H - 1, lane);
     }
 
     // 4 floats at q + s (q 16-byte aligned, s warp-uniform in 0..3)
@@ -323,17 +365,16 @@ struct U8LdgOp : HarrisU8Op<EXACT, CH, 124> {
 // (lane = strip * CH + row: the whole stage is one warp instruction), completing on the
 // stage mbarrier as transaction bytes like a TMA box.  The consumer undoes the per-row
 // skew (0..15 bytes, advancing by pitch mod 16 per row) with a word offset and a funnel
-// shift, then runs the packed dual-strip u8 core of the TMA path unchanged.  The copy is
-// clamped to the 16-byte block holding the row's last byte, so it never leaves the page of
-// a valid byte; rows below the image are not copied and columns beyond the row end are
-// stale — neither reaches a stored output.
+// shift, then runs the u8 core of the TMA path unchanged (G = 1: scalar, G = 2: packed
+// dual-strip).  The view's end: bulk_stage_fill (STRICT).  Rows below the image are not
+// copied and columns beyond the row end are stale — neither reaches a stored output.
 
-template <bool EXACT, int CH, int G>
+template <bool EXACT, int CH, int G, bool STRICT = false>
 struct U8BulkOp : std::conditional_t<G == 2, HarrisU8x2Op<EXACT, CH, 124>, HarrisU8Op<EXACT, CH, 124>> {
     using Base = std::conditional_t<G == 2, HarrisU8x2Op<EXACT, CH, 124>, HarrisU8Op<EXACT, CH, 124>>;
     static_assert(G * CH <= 32, "one lane per stage row");
     static constexpr bool kWarpLoad = true;
-    static constexpr int kBarArrivals = 1;  // lane 0's arrive.expect_tx; the copies count as tx bytes
+    static constexpr int kBarArrivals = kBulkBarArrivals;
     static constexpr bool kCacheProducer = true;
     static constexpr int kRowWords = 100;  // 400 B >= 15 skew bytes + 128 px * 3 B, 16-byte multiple
     static constexpr uint32_t kBoxBytes = uint32_t(CH) * kRowWords * 4u;
@@ -344,6 +385,7 @@ struct U8BulkOp : std::conditional_t<G == 2, HarrisU8x2Op<EXACT, CH, 124>, Harri
         const uint8_t* rgb;
         int64_t in_pitch, in_image_stride;  // bytes
         int32_t W, H;                       // input pixels per row / rows per image
+        const void* limit;                  // one past the view's last byte
     };
     uint32_t base_r, pitch_r, image_r;  // byte address residues mod 16
     uint32_t skew_a = 0, skew_b = 0;    // current row's skew of strips A and B
@@ -365,22 +407,11 @@ struct U8BulkOp : std::conditional_t<G == 2, HarrisU8x2Op<EXACT, CH, 124>, Harri
                                                      int lane) {
         const int k = lane >= CH ? 1 : 0, r = lane - k * CH;
         const int y = row0 + r;
-        uint32_t nb = 0;
-        const uint8_t* al = nullptr;
-        if (lane < G * CH && y < p.H) {
-            const int img = k ? image[G - 1] : image[0], c0 = k ? col0[G - 1] : col0[0];  // selects: no local array
-            const uint8_t* src =
-                p.rgb + int64_t(img) * p.in_image_stride + int64_t(y) * p.in_pitch + int64_t(c0) * 3;
-            const uintptr_t a = reinterpret_cast<uintptr_t>(src);
-            al = reinterpret_cast<const uint8_t*>(a & ~uintptr_t(15));
-            const uint32_t avail = uint32_t(a & 15u) + uint32_t(p.W - c0) * 3u;  // bytes to the row end
-            const uint32_t up = (avail + 15u) & ~15u;
-            nb = up < uint32_t(kRowWords * 4) ? up : uint32_t(kRowWords * 4);
-        }
-        const uint32_t total = __reduce_add_sync(0xffffffffu, nb);
-        if (lane == 0) mbar_arrive_expect_tx(bar, total);
-        __syncwarp();
-        if (nb) bulk_g2s(static_cast<unsigned char*>(smem) + k * kBoxStride + r * (kRowWords * 4), al, nb, bar);
+        const int img = k ? image[G - 1] : image[0], c0 = k ? col0[G - 1] : col0[0];  // selects: no local array
+        const uint8_t* src = p.rgb + int64_t(img) * p.in_image_stride + int64_t(y) * p.in_pitch + int64_t(c0) * 3;
+        bulk_stage_fill<STRICT>(static_cast<unsigned char*>(smem) + k * kBoxStride + r * (kRowWords * 4), src,
+                        uint32_t(p.W - c0) * 3u, kRowWords * 4, p.limit, bar, lane < G * CH && y < p.H,
+                        row0 + CH > p.H - 1 && row0 <= p.H - 1, y == p.H - 1, lane);
     }
 
     template <int R>
@@ -416,12 +447,12 @@ struct U8BulkOp : std::conditional_t<G == 2, HarrisU8x2Op<EXACT, CH, 124>, Harri
 constexpr int kU8BulkG = HARRIS_U8BULK_G;
 constexpr int kU8BulkNW = 8, kU8BulkNS = 4, kU8BulkCH = 6, kU8BulkMinB = kU8BulkG == 2 ? 1 : 2;
 const TmaConfig kU8BulkConfig = {kU8BulkNW, kU8BulkNS, kU8BulkCH, kU8BulkG, 124};
-template <bool EXACT>
-using U8BulkOpT = U8BulkOp<EXACT, kU8BulkCH, kU8BulkG>;
+template <bool EXACT, bool STRICT = false>
+using U8BulkOpT = U8BulkOp<EXACT, kU8BulkCH, kU8BulkG, STRICT>;
 
-template <bool EXACT>
+template <bool EXACT, bool STRICT = false>
 static constexpr auto u8_bulk_kernel() {
-    return strip_kernel<U8BulkOpT<EXACT>, kU8BulkNW, kU8BulkNS, kU8BulkMinB>;
+    return strip_kernel<U8BulkOpT<EXACT, STRICT>, kU8BulkNW, kU8BulkNS, kU8BulkMinB>;
 }
 static constexpr size_t u8_bulk_smem() {
     return StripShape<kU8BulkNW, kU8BulkNS, U8BulkOpT<false>>::kSmemBytes;
@@ -456,12 +487,8 @@ cudaError_t u8_ldg_configure(int* ctas_per_sm, int* bulk_ctas_per_sm) {
     if (e == cudaSuccess)
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, u8_ldg_kernel<false, 16>(), kU8LdgNW * 32,
                                                           u8_ldg_smem());
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(u8_bulk_kernel<false>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(u8_bulk_smem()));
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(u8_bulk_kernel<true>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(u8_bulk_smem()));
+    for (const void* k : {reinterpret_cast<const void*>(u8_bulk_kernel<false, false>()), reinterpret_cast<const void*>(u8_bulk_kernel<true, false>()), reinterpret_cast<const void*>(u8_bulk_kernel<false, true>()), reinterpret_cast<const void*>(u8_bulk_kernel<true, true>())})
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(u8_bulk_smem()));
     if (e == cudaSuccess)
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(bulk_ctas_per_sm, u8_bulk_kernel<false>(), kU8BulkNW * 32,
                                                           u8_bulk_smem());
@@ -484,10 +511,16 @@ static void launch_u8_bulk_one(const Geom& geom, const TileGeom& tg, int64_t gri
     CUtensorMap unused;
     std::memset(&unused, 0, sizeof(unused));
     const int64_t img_stride = geom.batch > 1 ? geom.in_image_stride : 0;
-    const typename U8BulkOpT<EXACT>::Params p{geom.kappa, reinterpret_cast<const uint8_t*>(geom.rgb),
-                                                          geom.in_pitch, img_stride, int32_t(geom.m + 4),
-                                                          int32_t(geom.n + 4)};
-    u8_bulk_kernel<EXACT>()<<<unsigned(grid), unsigned(kU8BulkNW * 32), u8_bulk_smem(), stream>>>(unused, tg, p);
+    const uint8_t* rgb = reinterpret_cast<const uint8_t*>(geom.rgb);
+    const uint8_t* limit = rgb + (geom.batch - 1) * img_stride + (geom.n + 3) * geom.in_pitch + 3 * (geom.m + 4);
+    auto go = [&](auto strict) {
+        constexpr bool S = decltype(strict)::value;
+        const typename U8BulkOpT<EXACT, S>::Params p{geom.kappa, rgb, geom.in_pitch, img_stride, int32_t(geom.m + 4),
+                                                     int32_t(geom.n + 4), limit};
+        u8_bulk_kernel<EXACT, S>()<<<unsigned(grid), unsigned(kU8BulkNW * 32), u8_bulk_smem(), stream>>>(unused, tg, p);
+    };
+    // STRICT only when the 16-byte rounding could pass the view's end
+    (reinterpret_cast<uintptr_t>(limit) & 15u) ? go(std::true_type{}) : go(std::false_type{});
 }
 
 // chunk 0: the bulk-copy kernel (K1b, default); 4 / 16: the cp.async kernel (K2)
@@ -509,13 +542,13 @@ struct LdgCfg;
 template <>
 struct LdgCfg<0> {
     static constexpr int NW = 8, NS = 2, CH = 3, MINB = 1, G = 2;
-    template <bool EXACT>
+    template <bool EXACT, bool STRICT = false>
     using Op = LdgOp<HarrisF32x2Op<EXACT, CH, 128>, 4>;
 };
 template <>
 struct LdgCfg<1> {
     static constexpr int NW = 8, NS = 2, CH = 3, MINB = 2, G = 1;
-    template <bool EXACT>
+    template <bool EXACT, bool STRICT = false>
     using Op = LdgOp<HarrisF32Op<EXACT, CH, 128>, 4>;
 };
 
@@ -524,7 +557,7 @@ struct LdgCfg<1> {
 template <>
 struct LdgCfg<2> {
     static constexpr int NW = 8, NS = 2, CH = 3, MINB = 2, G = 1;
-    template <bool EXACT>
+    template <bool EXACT, bool STRICT = false>
     using Op = LdgOp<HarrisF32Op<EXACT, CH, 124>, 4>;
 };
 
@@ -532,23 +565,23 @@ struct LdgCfg<2> {
 template <>
 struct LdgCfg<3> {
     static constexpr int NW = 8, NS = 2, CH = 3, MINB = 2, G = 1;
-    template <bool EXACT>
-    using Op = F32BulkOp<EXACT, CH, 1>;
+    template <bool EXACT, bool STRICT = false>
+    using Op = F32BulkOp<EXACT, CH, 1, STRICT>;
 };
 template <>
 struct LdgCfg<4> {
     static constexpr int NW = 8, NS = 2, CH = 3, MINB = 1, G = 2;
-    template <bool EXACT>
-    using Op = F32BulkOp<EXACT, CH, 2>;
+    template <bool EXACT, bool STRICT = false>
+    using Op = F32BulkOp<EXACT, CH, 2, STRICT>;
 };
 
 const TmaConfig kLdgConfigs[kNumLdgConfigs] = {
     {8, 2, 3, 2, 128}, {8, 2, 3, 1, 128}, {8, 2, 3, 1, 124}, {8, 2, 3, 1, 124}, {8, 2, 3, 2, 124}};
 
-template <int CFG, bool EXACT>
+template <int CFG, bool EXACT, bool STRICT = false>
 static constexpr auto ldg_kernel() {
     using C = LdgCfg<CFG>;
-    return strip_kernel<typename C::template Op<EXACT>, C::NW, C::NS, C::MINB>;
+    return strip_kernel<typename C::template Op<EXACT, STRICT>, C::NW, C::NS, C::MINB>;
 }
 template <int CFG>
 static constexpr size_t ldg_smem() {
@@ -561,11 +594,9 @@ static_assert(ldg_smem<0>() <= 227 * 1024 && ldg_smem<1>() <= 227 * 1024 && ldg_
 
 template <int CFG>
 static cudaError_t ldg_configure_one(int* ctas_per_sm) {
-    cudaError_t e = cudaFuncSetAttribute(ldg_kernel<CFG, false>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(ldg_smem<CFG>()));
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(ldg_kernel<CFG, true>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(ldg_smem<CFG>()));
+    cudaError_t e = cudaSuccess;
+    for (const void* k : {reinterpret_cast<const void*>(ldg_kernel<CFG, false, false>()), reinterpret_cast<const void*>(ldg_kernel<CFG, true, false>()), reinterpret_cast<const void*>(ldg_kernel<CFG, false, true>()), reinterpret_cast<const void*>(ldg_kernel<CFG, true, true>())})
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ldg_smem<CFG>()));
     if (e == cudaSuccess)
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, ldg_kernel<CFG, false>(), LdgCfg<CFG>::NW * 32,
                                                           ldg_smem<CFG>());
@@ -584,11 +615,18 @@ template <int CFG, bool EXACT>
 static void launch_ldg_one(const Geom& geom, const TileGeom& tg, int64_t grid, cudaStream_t stream) {
     CUtensorMap unused;
     std::memset(&unused, 0, sizeof(unused));
-    using Op = typename LdgCfg<CFG>::template Op<EXACT>;
-    const typename Op::Params p{{geom.kappa}, geom.rgb, geom.in_pitch, geom.in_chan_stride, geom.in_image_stride,
-                                int32_t(geom.m + 4), int32_t(geom.n + 4)};
-    ldg_kernel<CFG, EXACT>()<<<unsigned(grid), unsigned(LdgCfg<CFG>::NW * 32), ldg_smem<CFG>(), stream>>>(unused, tg,
-                                                                                                       p);
+    const int64_t img_stride = geom.batch > 1 ? geom.in_image_stride : 0;
+    const float* limit = geom.rgb + (geom.batch - 1) * img_stride + 2 * geom.in_chan_stride +
+                         (geom.n + 3) * geom.in_pitch + (geom.m + 4);
+    auto go = [&](auto strict) {
+        constexpr bool S = decltype(strict)::value;
+        using Op = typename LdgCfg<CFG>::template Op<EXACT, S>;
+        const typename Op::Params p{{geom.kappa}, geom.rgb, geom.in_pitch, geom.in_chan_stride, img_stride,
+                                    int32_t(geom.m + 4), int32_t(geom.n + 4), limit};
+        ldg_kernel<CFG, EXACT, S>()<<<unsigned(grid), unsigned(LdgCfg<CFG>::NW * 32), ldg_smem<CFG>(), stream>>>(
+            unused, tg, p);
+    };
+    (reinterpret_cast<uintptr_t>(limit) & 15u) ? go(std::true_type{}) : go(std::false_type{});
 }
 
 cudaError_t launch_ldg(int cfg, bool exact, const Geom& geom, const TileGeom& tg, int64_t grid,
@@ -610,12 +648,12 @@ cudaError_t launch_ldg(int cfg, bool exact, const Geom& geom, const TileGeom& tg
 // stage row (<= 544 B from the 16-byte aligned-down start), the consumer reads its 6
 // floats at the row's float skew (even: three 8-byte loads; odd: scalar + 2 x 8-byte +
 // scalar) and runs the unchanged Sep3x3Op arithmetic
-template <bool EXACT, int CH>
+template <bool EXACT, int CH, bool STRICT = false>
 struct SepBulkOp : Sep3x3Op<EXACT, CH> {
     using Base = Sep3x3Op<EXACT, CH>;
     static_assert(CH <= 32, "one lane per stage row");
     static constexpr bool kWarpLoad = true;
-    static constexpr int kBarArrivals = 1;
+    static constexpr int kBarArrivals = kBulkBarArrivals;
     static constexpr bool kCacheProducer = true;
     static constexpr int kRowFloats = 136;  // 3 skew floats + 130 columns, 16-byte multiple
     static constexpr uint32_t kStageBytes = (uint32_t(CH) * kRowFloats * 4u + 127u) / 128u * 128u;
@@ -624,6 +662,7 @@ struct SepBulkOp : Sep3x3Op<EXACT, CH> {
         const float* src;
         int64_t in_pitch, in_plane_stride, in_image_stride;  // elements (plane stride unused)
         int32_t W, H;
+        const void* limit;  // one past the view's last element
     };
     uint32_t base_r, pitch_r, image_r, sk = 0;
 
@@ -641,20 +680,10 @@ struct SepBulkOp : Sep3x3Op<EXACT, CH> {
                                                      const int (&col0)[1], int row0, const int (&image)[1],
                                                      int lane) {
         const int y = row0 + lane;
-        uint32_t nb = 0;
-        const float* al = nullptr;
-        if (lane < CH && y < p.H) {
-            const float* src = p.src + int64_t(image[0]) * p.in_image_stride + int64_t(y) * p.in_pitch + col0[0];
-            const uintptr_t a = reinterpret_cast<uintptr_t>(src);
-            al = reinterpret_cast<const float*>(a & ~uintptr_t(15));
-            const uint32_t avail = uint32_t(a & 15u) + uint32_t(p.W - col0[0]) * 4u;
-            const uint32_t up = (avail + 15u) & ~15u;
-            nb = up < uint32_t(kRowFloats * 4) ? up : uint32_t(kRowFloats * 4);
-        }
-        const uint32_t total = __reduce_add_sync(0xffffffffu, nb);
-        if (lane == 0) mbar_arrive_expect_tx(bar, total);
-        __syncwarp();
-        if (nb) bulk_g2s(static_cast<unsigned char*>(smem) + lane * (kRowFloats * 4), al, nb, bar);
+        const float* src = p.src + int64_t(image[0]) * p.in_image_stride + int64_t(y) * p.in_pitch + col0[0];
+        bulk_stage_fill<STRICT>(static_cast<unsigned char*>(smem) + lane * (kRowFloats * 4), src, uint32_t(p.W - col0[0]) * 4u,
+                        kRowFloats * 4, p.limit, bar, lane < CH && y < p.H,
+                        row0 + CH > p.H - 1 && row0 <= p.H - 1, y == p.H - 1, lane);
     }
 
     template <int R>
@@ -677,17 +706,12 @@ struct SepBulkOp : Sep3x3Op<EXACT, CH> {
 constexpr int kSepLdgNW = 8, kSepLdgNS = 8, kSepLdgCH = 6;
 const TmaConfig kSepLdgConfig = {kSepLdgNW, kSepLdgNS, kSepLdgCH, 1, 128};
 
-#ifndef HARRIS_SEP_CPASYNC
-template <bool EXACT>
-using SepLdgOpT = SepBulkOp<EXACT, kSepLdgCH>;
-#else
-template <bool EXACT>
-using SepLdgOpT = LdgOp<Sep3x3Op<EXACT, kSepLdgCH>, 4>;
-#endif
+template <bool EXACT, bool STRICT = false>
+using SepLdgOpT = SepBulkOp<EXACT, kSepLdgCH, STRICT>;
 
-template <bool EXACT>
+template <bool EXACT, bool STRICT = false>
 static constexpr auto sep_ldg_kernel() {
-    return strip_kernel<SepLdgOpT<EXACT>, kSepLdgNW, kSepLdgNS, 1>;
+    return strip_kernel<SepLdgOpT<EXACT, STRICT>, kSepLdgNW, kSepLdgNS, 1>;
 }
 static constexpr size_t sep_ldg_smem() {
     return StripShape<kSepLdgNW, kSepLdgNS, SepLdgOpT<false>>::kSmemBytes;
@@ -695,11 +719,9 @@ static constexpr size_t sep_ldg_smem() {
 static_assert(sep_ldg_smem() <= 227 * 1024, "stencil ldg smem");
 
 cudaError_t sep_ldg_configure(int* ctas_per_sm) {
-    cudaError_t e = cudaFuncSetAttribute(sep_ldg_kernel<false>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(sep_ldg_smem()));
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(sep_ldg_kernel<true>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(sep_ldg_smem()));
+    cudaError_t e = cudaSuccess;
+    for (const void* k : {reinterpret_cast<const void*>(sep_ldg_kernel<false, false>()), reinterpret_cast<const void*>(sep_ldg_kernel<true, false>()), reinterpret_cast<const void*>(sep_ldg_kernel<false, true>()), reinterpret_cast<const void*>(sep_ldg_kernel<true, true>())})
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sep_ldg_smem()));
     if (e == cudaSuccess)
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, sep_ldg_kernel<false>(), kSepLdgNW * 32,
                                                           sep_ldg_smem());
@@ -712,10 +734,16 @@ static void launch_sep_ldg_one(const float* in, int64_t in_pitch, int64_t in_ima
                                cudaStream_t stream) {
     CUtensorMap unused;
     std::memset(&unused, 0, sizeof(unused));
-    using Op = SepLdgOpT<EXACT>;
-    const typename Op::Params p{{{wv[0], wv[1], wv[2]}, {wh[0], wh[1], wh[2]}}, in, in_pitch, 0, in_image_stride, W,
-                                H};
-    sep_ldg_kernel<EXACT>()<<<unsigned(grid), unsigned(kSepLdgNW * 32), sep_ldg_smem(), stream>>>(unused, tg, p);
+    const int64_t img_stride = tg.batch > 1 ? in_image_stride : 0;
+    const float* limit = in + (tg.batch - 1) * img_stride + int64_t(H - 1) * in_pitch + W;
+    auto go = [&](auto strict) {
+        constexpr bool S = decltype(strict)::value;
+        using Op = SepLdgOpT<EXACT, S>;
+        const typename Op::Params p{{{wv[0], wv[1], wv[2]}, {wh[0], wh[1], wh[2]}}, in, in_pitch, 0, img_stride, W,
+                                    H, limit};
+        sep_ldg_kernel<EXACT, S>()<<<unsigned(grid), unsigned(kSepLdgNW * 32), sep_ldg_smem(), stream>>>(unused, tg, p);
+    };
+    (reinterpret_cast<uintptr_t>(limit) & 15u) ? go(std::true_type{}) : go(std::false_type{});
 }
 
 cudaError_t launch_sep_ldg(bool exact, const float* in, int64_t in_pitch, int64_t in_image_stride, int64_t W,

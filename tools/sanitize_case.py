@@ -32,14 +32,21 @@ def u8(B, H, W, off=0, **kw):
 f32(1, 70, 264)            # TMA, short tiles -> scalar core
 f32(1, 300, 1028)          # TMA dual-strip core
 f32(3, 41, 388)            # TMA dual, strip pairs straddling images
-f32(2, 37, 71)             # K2 cp.async (width % 4 != 0)
-f32(1, 40, 136, off=1)     # K2 (4-byte aligned base)
+f32(2, 37, 71)             # K1b bulk rows (width % 4 != 0, height % 4 != 0)
+f32(1, 40, 136, off=1)     # K1b (4-byte aligned base)
+f32(2, 38, 262)            # K1p pair-row TMA (pitch = 2 mod 4, even height)
+f32(2, 40, 263)            # K1q quad-row TMA (odd pitch, height % 4 == 0)
 f32(1, 37, 71, force_generic=True)  # K0
 u8(2, 40, 400)             # u8 TMA
-u8(2, 37, 263, off=1)      # u8 K2
+u8(2, 37, 263, off=1)      # u8 K1b bulk rows
+u8(1, 29, 131, off=15)     # u8 K1b, ragged last strip, base 15 bytes past alignment
 img = torch.rand(2, 50, 260, device="cuda")
 hb.stencil3x3_sep(img)
 hb.stencil3x3_sep(img, exact=True)
+for off in (1, 3):         # stencil K1b bulk rows (unaligned base, odd pitch)
+    buf = torch.rand(off + 2 * 50 * 263, device="cuda")
+    hb.stencil3x3_sep(buf[off:].view(2, 50, 263))
+    hb.stencil3x3_sep(buf[off:].view(2, 50, 263), exact=True)
 for g in (1, 2, 3, 4):
     hb.harris_grouping(torch.rand(3, 40, 132, device="cuda"), g)
 x = torch.rand(3, 40, 136, device="cuda")
