@@ -682,6 +682,52 @@ def run_extra(a, ctx, dev) -> dict:
                              "frac_of_measured_hbm": nbytes / (med * 1e-3) / 1e9 / peak}
     del xs, out
     torch.cuda.empty_cache()
+
+    # input layouts TMA cannot describe row by row (rows not 16-byte aligned): the pair- /
+    # quad-row TMA kernels and the bulk-copy engine (K1b), 256 images each (inputs >> L2)
+    from paper_2212_12035_b200 import _lib as _pl
+    path_names = {_pl.PATH_TMA: "tma", _pl.PATH_LDG: "ldg/bulk", _pl.PATH_PAIR: "pair-row tma",
+                  _pl.PATH_QUAD: "quad-row tma", _pl.PATH_GENERIC: "generic"}
+    layouts = {}
+    nb = 256
+    for name, (H, W, crop, desc) in {
+            "width1918": (1080, 1918, False, "256 x 1080x1918 f32 (pitch = 2 mod 4 floats)"),
+            "width1919": (1080, 1919, False, "256 x 1080x1919 f32 (odd pitch)"),
+            "width1919_h1081": (1081, 1919, False, "256 x 1081x1919 f32 (odd pitch, height not a multiple of 4)"),
+            "crop1920": (1080, 1920, True, "256 x 1080x1920 column-crop view x[..., 1:] of 1080x1921 (base 4-byte "
+                                           "aligned)")}.items():
+        base = torch.empty((nb, 3, H, W + 1 if crop else W), device=dev)
+        hb.synth_(base.view(nb * 3, H, -1), seed=SEED)
+        x = base[..., 1:] if crop else base
+        out = torch.empty((nb, H - 4, W - 4), device=dev)
+        for _ in range(3):
+            hb.harris(x, out=out)
+        torch.cuda.synchronize()
+        path = path_names.get(ctx.last_path, str(ctx.last_path))
+        ts = sorted(time_launches(lambda: hb.harris(x, out=out), 10))
+        med = ts[len(ts) // 2]
+        gbs = hb.algorithmic_bytes(H - 4, W - 4, nb) / (med * 1e-3) / 1e9
+        layouts[name] = {"workload": desc, "path": path, "ms_median_of_10": med,
+                         "value": nb * (H - 4) * (W - 4) / (med * 1e-3) / 1e6, "unit": "MP/s",
+                         "frac_of_measured_hbm": gbs / peak}
+        del base, x, out
+    H, W = 1080, 1918
+    x8 = torch.randint(0, 256, (2 * nb, H, W, 3), dtype=torch.uint8, device=dev, generator=g)
+    out = torch.empty((2 * nb, H - 4, W - 4), device=dev)
+    for _ in range(3):
+        hb.harris_u8(x8, out=out)
+    torch.cuda.synchronize()
+    path = path_names.get(ctx.last_path, str(ctx.last_path))
+    ts = sorted(time_launches(lambda: hb.harris_u8(x8, out=out), 10))
+    med = ts[len(ts) // 2]
+    nbytes = 2 * nb * (3 * H * W + 4 * (H - 4) * (W - 4))
+    layouts["u8_width1918"] = {"workload": "512 x 1080x1918 interleaved RGB u8 (rows 16-byte aligned only every "
+                                           "8th row)", "path": path, "ms_median_of_10": med,
+                               "value": 2 * nb * (H - 4) * (W - 4) / (med * 1e-3) / 1e6, "unit": "MP/s",
+                               "frac_of_measured_hbm": nbytes / (med * 1e-3) / 1e9 / peak}
+    del x8, out
+    torch.cuda.empty_cache()
+    res["layouts"] = layouts
     return res
 
 

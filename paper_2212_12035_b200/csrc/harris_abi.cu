@@ -108,6 +108,15 @@ int cuda_fail(harris_ctx* ctx, cudaError_t e, const char* where) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// TileGeom::vec_store: 2 = every output row 16-byte aligned (float4 stores); 1 = every row
+// 8-byte aligned (two float2 stores per lane: e.g. 1914-float rows); 0 = scalar stores
+int32_t store_mode(const float* out, int64_t out_pitch, int64_t batch, int64_t out_image_stride) {
+    if (aligned16(out) && (out_pitch & 3) == 0 && (batch == 1 || (out_image_stride & 3) == 0)) return 2;
+    if ((reinterpret_cast<uintptr_t>(out) & 7u) == 0 && (out_pitch & 1) == 0 && (batch == 1 || (out_image_stride & 1) == 0))
+        return 1;
+    return 0;
+}
+
 enum Format { kF32Planar = 0, kU8Interleaved = 1 };
 
 struct Call {
@@ -269,7 +278,7 @@ void plan_launch(const harris_ctx* ctx, const Call& c, TileGeom& tg, int64_t& gr
     tg.out_image_stride = c.g.out_image_stride;
     tg.kappa = c.g.kappa;
     tg.l2_policy = ctx->l2_policy;
-    tg.vec_store = aligned16(c.g.out) && (c.g.out_pitch & 3) == 0 && (c.g.batch == 1 || (c.g.out_image_stride & 3) == 0);
+    tg.vec_store = store_mode(c.g.out, c.g.out_pitch, c.g.batch, c.g.out_image_stride);
     tg.sync_waves = ctx->sync_waves;
 }
 
@@ -716,7 +725,7 @@ int harris_stencil3x3_sep(harris_ctx* ctx, float* out, int64_t out_pitch, int64_
         tg.out_image_stride = batch > 1 ? out_image_stride : n * out_pitch;
         tg.kappa = 0.f;
         tg.l2_policy = ctx->l2_policy;
-        tg.vec_store = aligned16(out) && (out_pitch & 3) == 0 && (batch == 1 || (out_image_stride & 3) == 0);
+        tg.vec_store = store_mode(out, out_pitch, batch, out_image_stride);
         tg.sync_waves = ctx->sync_waves;
         if (tg.tiles > INT32_MAX) return HARRIS_ERR_SIZE;
         e = launch_sep_ldg(exact, in, in_pitch, img_stride, m + 2, n + 2, tg, grid, wv, wh, stream);
@@ -743,7 +752,7 @@ int harris_stencil3x3_sep(harris_ctx* ctx, float* out, int64_t out_pitch, int64_
         tg.out_image_stride = batch > 1 ? out_image_stride : n * out_pitch;
         tg.kappa = 0.f;
         tg.l2_policy = ctx->l2_policy;
-        tg.vec_store = aligned16(out) && (out_pitch & 3) == 0 && (batch == 1 || (out_image_stride & 3) == 0);
+        tg.vec_store = store_mode(out, out_pitch, batch, out_image_stride);
         tg.sync_waves = ctx->sync_waves;
         if (tg.tiles > INT32_MAX) return HARRIS_ERR_SIZE;  // beyond the engine's 32-bit tile index
         e = launch_tma_sep(ctx->sep_cfg, exact, tmap, tg, grid, wv, wh, stream);

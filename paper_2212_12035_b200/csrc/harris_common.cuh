@@ -150,17 +150,10 @@ __device__ __forceinline__ void stg128_cs(float* p, float a, float b, float c, f
                  : "memory");
 }
 
-// 4 floats to a 4-byte aligned address (output rows whose pitch is not a multiple of 4
-// floats): 8-byte aligned -> two 8-byte stores; otherwise scalar + 8-byte + scalar
-__device__ __forceinline__ void stg4_cs_align4(float* p, float a, float b, float c, float d) {
-    if (reinterpret_cast<uintptr_t>(p) & 4u) {
-        asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p), "f"(a) : "memory");
-        asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p + 1), "f"(b), "f"(c) : "memory");
-        asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p + 3), "f"(d) : "memory");
-    } else {
-        asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(a), "f"(b) : "memory");
-        asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p + 2), "f"(c), "f"(d) : "memory");
-    }
+// 4 floats to an 8-byte aligned address: two 8-byte streaming stores
+__device__ __forceinline__ void stg2x2_cs(float* p, float a, float b, float c, float d) {
+    asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(a), "f"(b) : "memory");
+    asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p + 2), "f"(c), "f"(d) : "memory");
 }
 
 // system-scope release store / acquire load (cross-GPU flags of the fused gather)

@@ -264,6 +264,7 @@ template <bool EXACT>
 struct HarrisF32PairRowOp : HarrisF32Op<EXACT, 6, 124> {
     using Base = HarrisF32Op<EXACT, 6, 124>;
     static constexpr int CH = 6;
+    static constexpr bool kSplitStores = true;  // its outputs are typically 2 (mod 4) floats wide
     static constexpr int kRow = 132;                                   // box width (16-byte multiple)
     static constexpr uint32_t kBoxBytes = 3u * 3u * kRow * 4u;         // 3 channels x 3 pair-rows
     static constexpr uint32_t kBoxStride = (kBoxBytes + 127u) / 128u * 128u;  // TMA destinations: 128-B aligned
@@ -433,7 +434,6 @@ __device__ __forceinline__ void gray4_u8(uint32_t w0, uint32_t w1, uint32_t w2, 
 template <bool EXACT, int CH, int SC = 128>
 struct HarrisU8Op {
     static_assert(CH % 3 == 0, "row rotation needs CH % 3 == 0");
-    static constexpr bool kSplitStores = false;  // issue-bound: predicated scalar stores
     using L = Strip<SC>;
     static constexpr int kGroups = 1;
     static constexpr int kStripCols = SC;

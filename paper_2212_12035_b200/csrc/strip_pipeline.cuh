@@ -107,12 +107,14 @@ struct BarArrivalsOf : std::integral_constant<int, 32> {};
 template <class Op>
 struct BarArrivalsOf<Op, std::void_t<decltype(Op::kBarArrivals)>> : std::integral_constant<int, Op::kBarArrivals> {};
 
-// Op::kSplitStores is optional (default true): output rows that are not 16-byte aligned
-// get 8-byte + scalar stores (fewer store transactions: +1.8 % on memory-bound f32
-// kernels); false keeps four predicated scalar stores (no per-row branch: the
-// issue-bound u8 kernels measured 11 % slower with the split form)
+// Op::kSplitStores is optional (default false): with true, output rows that are all 8-byte
+// aligned but not 16-byte aligned (TileGeom::vec_store == 1, e.g. 1914-float rows) get two
+// 8-byte stores per lane (fewer store transactions: +1.8 % on the pair-row kernel, whose
+// outputs are typically that wide).  Off elsewhere: even the untaken second store variant
+// in the unrolled row loop measured 23 % slower on the quad-row kernel (odd-width outputs,
+// 404 -> 311 k) and 11 % on the issue-bound u8 kernels.
 template <class Op, class = void>
-struct SplitStoresOf : std::true_type {};
+struct SplitStoresOf : std::false_type {};
 template <class Op>
 struct SplitStoresOf<Op, std::void_t<decltype(Op::kSplitStores)>> : std::integral_constant<bool, Op::kSplitStores> {};
 
@@ -305,7 +307,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
         bool ragged = false;
 #pragma unroll
         for (int k = 0; k < G; ++k) {
-            vec[k] = g.vec_store && colg[k] + kColsPerLane <= g.m;
+            vec[k] = g.vec_store == 2 && colg[k] + kColsPerLane <= g.m;
             ragged |= !vec[k] && colg[k] < g.m;
         }
         ragged = __any_sync(0xffffffffu, ragged);
@@ -327,8 +329,8 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                             if (ragged) {  // unaligned output rows, or the ragged right edge
                                 const int cg = colg[gi];
                                 if (!vec[gi] && cg < g.m) {
-                                    if (SplitStoresOf<Op>::value && cg + kColsPerLane <= g.m) {  // row not 16-B aligned
-                                        stg4_cs_align4(po, out4[gi][0], out4[gi][1], out4[gi][2], out4[gi][3]);
+                                    if (SplitStoresOf<Op>::value && g.vec_store == 1 && cg + kColsPerLane <= g.m) {
+                                        stg2x2_cs(po, out4[gi][0], out4[gi][1], out4[gi][2], out4[gi][3]);
                                     } else {
 #pragma unroll
                                         for (int k = 0; k < kColsPerLane; ++k)
