@@ -46,6 +46,7 @@ struct harris_ctx {
     int ldg_cfg = 3;  // HARRIS_LDG_CONFIG; 3 = bulk-copy rows + scalar lane-halo core, 16 warps/SM (K1b:
                       // 404 k MP/s on a column-crop view of 256 x 1080p; the cp.async config 2: 296 k)
     int sync_waves = 1;  // dev knob HARRIS_SYNC_WAVES=0 disables the per-tile CTA barrier
+    int sep_bulk = 0;  // HARRIS_SEP_BULK: aligned stencil planes through the bulk-copy kernel too
     int l2_policy = 1;  // evict_normal: the 4-column halo sectors are re-read by the neighbouring strip
     int64_t force_band_rows = 0;  // dev knob (HARRIS_BAND_ROWS): override the planner
     CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;  // dev knob HARRIS_L2_PROMO
@@ -537,6 +538,8 @@ int harris_init(harris_ctx** out_ctx, int cuda_device) {
         int v = std::atoi(env);
         if (v >= 0 && v < kNumU8Configs) ctx->u8_cfg = v;
     }
+    env = std::getenv("HARRIS_SEP_BULK");
+    if (env) ctx->sep_bulk = std::atoi(env) != 0;
     env = std::getenv("HARRIS_SEP_CONFIG");
     if (env) {
         int v = std::atoi(env);
@@ -706,9 +709,11 @@ int harris_stencil3x3_sep(harris_ctx* ctx, float* out, int64_t out_pitch, int64_
     cudaStream_t stream = static_cast<cudaStream_t>(stream_);
     const bool exact = (flags & HARRIS_FLAG_EXACT_ORDER) != 0;
     const int64_t img_stride = batch > 1 ? in_image_stride : (n + 2) * in_pitch;
-    const bool tma = !(flags & HARRIS_FLAG_FORCE_GENERIC) && aligned16(in) && (in_pitch & 3) == 0 &&
-                     (batch == 1 || (in_image_stride & 3) == 0) && batch <= INT32_MAX;
-    if (!tma && (flags & HARRIS_FLAG_FORCE_TMA)) return HARRIS_ERR_ALIGNMENT;
+    const bool tma_ok = !(flags & HARRIS_FLAG_FORCE_GENERIC) && aligned16(in) && (in_pitch & 3) == 0 &&
+                        (batch == 1 || (in_image_stride & 3) == 0) && batch <= INT32_MAX;
+    if (!tma_ok && (flags & HARRIS_FLAG_FORCE_TMA)) return HARRIS_ERR_ALIGNMENT;
+    // aligned planes too go through the bulk-copy kernel when ctx->sep_bulk (HARRIS_SEP_BULK)
+    const bool tma = tma_ok && (!ctx->sep_bulk || (flags & HARRIS_FLAG_FORCE_TMA));
     // other 4-byte aligned planes: the same strip engine with cp.async stage fills
     const bool ldg = !tma && !(flags & HARRIS_FLAG_FORCE_GENERIC) && (reinterpret_cast<uintptr_t>(in) & 3) == 0 &&
                      batch * ((m + 127) / 128) < (int64_t(1) << 30);
