@@ -70,9 +70,10 @@ extern "C" {
 #define HARRIS_PATH_PAIR    4  /* K1p: TMA over pairs of rows, for f32 whose row pitch is 2 (mod 4)
                                       floats (e.g. 1918 or 8190 wide) with 16-byte aligned planes */
 #define HARRIS_PATH_QUAD    5  /* K1q: TMA over quads of rows, for f32 with an odd row pitch */
-#define HARRIS_PATH_LDG     3  /* K2: the TMA kernel's engine with cp.async stage fills, for
-                                      inputs whose strides / base TMA cannot describe (f32 with
-                                      W % 4 != 0 or a 4-byte aligned base; u8 with 3W % 16 != 0) */
+#define HARRIS_PATH_LDG     3  /* K1b / K2: the TMA kernel's engine with one bulk copy per stage
+                                      row (K1b, default) or cp.async stage fills (K2), for inputs
+                                      whose strides / base TMA cannot describe (f32 with W % 4 != 0
+                                      or a 4-byte aligned base; u8 with 3W % 16 != 0) */
 
 typedef struct harris_ctx harris_ctx;
 
