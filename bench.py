@@ -711,21 +711,24 @@ def run_extra(a, ctx, dev) -> dict:
                          "value": nb * (H - 4) * (W - 4) / (med * 1e-3) / 1e6, "unit": "MP/s",
                          "frac_of_measured_hbm": gbs / peak}
         del base, x, out
-    H, W = 1080, 1918
-    x8 = torch.randint(0, 256, (2 * nb, H, W, 3), dtype=torch.uint8, device=dev, generator=g)
-    out = torch.empty((2 * nb, H - 4, W - 4), device=dev)
-    for _ in range(3):
-        hb.harris_u8(x8, out=out)
-    torch.cuda.synchronize()
-    path = path_names.get(ctx.last_path, str(ctx.last_path))
-    ts = sorted(time_launches(lambda: hb.harris_u8(x8, out=out), 10))
-    med = ts[len(ts) // 2]
-    nbytes = 2 * nb * (3 * H * W + 4 * (H - 4) * (W - 4))
-    layouts["u8_width1918"] = {"workload": "512 x 1080x1918 interleaved RGB u8 (rows 16-byte aligned only every "
-                                           "8th row)", "path": path, "ms_median_of_10": med,
-                               "value": 2 * nb * (H - 4) * (W - 4) / (med * 1e-3) / 1e6, "unit": "MP/s",
-                               "frac_of_measured_hbm": nbytes / (med * 1e-3) / 1e9 / peak}
-    del x8, out
+    for name, (H, W, desc) in {
+            "u8_width1080": (1920, 1080, "512 x 1920x1080 (portrait) interleaved RGB u8: 3240-byte rows, TMA over row "
+                                         "pairs"),
+            "u8_width1918": (1080, 1918, "512 x 1080x1918 interleaved RGB u8 (rows 16-byte aligned only every 8th "
+                                         "row): bulk-copy rows")}.items():
+        x8 = torch.randint(0, 256, (2 * nb, H, W, 3), dtype=torch.uint8, device=dev, generator=g)
+        out = torch.empty((2 * nb, H - 4, W - 4), device=dev)
+        for _ in range(3):
+            hb.harris_u8(x8, out=out)
+        torch.cuda.synchronize()
+        path = path_names.get(ctx.last_path, str(ctx.last_path))
+        ts = sorted(time_launches(lambda: hb.harris_u8(x8, out=out), 10))
+        med = ts[len(ts) // 2]
+        nbytes = 2 * nb * (3 * H * W + 4 * (H - 4) * (W - 4))
+        layouts[name] = {"workload": desc, "path": path, "ms_median_of_10": med,
+                         "value": 2 * nb * (H - 4) * (W - 4) / (med * 1e-3) / 1e6, "unit": "MP/s",
+                         "frac_of_measured_hbm": nbytes / (med * 1e-3) / 1e9 / peak}
+        del x8, out
     torch.cuda.empty_cache()
     res["layouts"] = layouts
     return res

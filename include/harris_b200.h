@@ -68,8 +68,10 @@ extern "C" {
 #define HARRIS_PATH_TMA     1  /* K1: TMA-staged warp-strip kernel (W%4==0, aligned) */
 #define HARRIS_PATH_GENERIC 2  /* K0: shared-memory tile kernel (any W, any pitch)   */
 #define HARRIS_PATH_PAIR    4  /* K1p: TMA over pairs of rows, for f32 whose row pitch is 2 (mod 4)
-                                      floats (e.g. 1918 or 8190 wide) with 16-byte aligned planes */
-#define HARRIS_PATH_QUAD    5  /* K1q: TMA over quads of rows, for f32 with an odd row pitch */
+                                      floats (e.g. 1918 or 8190 wide) with 16-byte aligned planes,
+                                      and u8 whose row pitch is 8 (mod 16) bytes (e.g. 1080 wide) */
+#define HARRIS_PATH_QUAD    5  /* K1q: TMA over quads of rows, for f32 with an odd row pitch and
+                                      u8 whose row pitch is 4 (mod 8) bytes (e.g. 1916 wide) */
 #define HARRIS_PATH_LDG     3  /* K1b / K2: the TMA kernel's engine with one bulk copy per stage
                                       row (K1b, default) or cp.async stage fills (K2), for inputs
                                       whose strides / base TMA cannot describe (f32 with W % 4 != 0

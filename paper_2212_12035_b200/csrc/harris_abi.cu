@@ -39,6 +39,7 @@ struct harris_ctx {
     int occ_ldg[kNumLdgConfigs] = {0};
     int occ_u8ldg = 0;
     int occ_u8bulk = 0;
+    int occ_u8pair = 0, occ_u8quad = 0;
     int occ_pair = 0;
     int occ_quad = 0;
     int occ_sepldg = 0;
@@ -243,7 +244,13 @@ bool ldg_eligible(const Call& c) {
 // An odd pitch groups 4 rows (4P floats is a 16-byte multiple): HarrisF32QuadRowOp.
 int row_group(const Call& c) {
     const Geom& g = c.g;
-    if (c.fmt != kF32Planar || !aligned16(g.rgb)) return 0;
+    if (!aligned16(g.rgb)) return 0;
+    if (c.fmt == kU8Interleaved) {  // byte pitch 8 (mod 16): pairs; 4 (mod 8): quads (K*P % 16 == 0)
+        const int k = (g.in_pitch & 15) == 8 ? 2 : (g.in_pitch & 7) == 4 ? 4 : 0;
+        if (!k || ((g.n + 4) % k) || (g.batch > 1 && (g.in_image_stride & 15))) return 0;
+        if (int64_t(k) * g.in_pitch > INT32_MAX || g.batch > INT32_MAX) return 0;
+        return g.batch * ((g.m + 123) / 124) < (int64_t(1) << 30) ? k : 0;
+    }
     const int k = (g.in_pitch & 3) == 2 ? 2 : (g.in_pitch & 1) ? 4 : 0;
     if (!k || (g.in_chan_stride & 3) || ((g.n + 4) % k)) return 0;
     if (g.batch > 1 && (g.in_image_stride & 3)) return 0;
@@ -262,11 +269,13 @@ int choose_path(const Call& c) {
 void plan_launch(const harris_ctx* ctx, const Call& c, TileGeom& tg, int64_t& grid) {
     const bool u8 = c.fmt == kU8Interleaved;
     const int fcfg = c.cfg >= 0 ? c.cfg : ctx->tma_cfg;
-    const TmaConfig& cfg = c.pair  ? (c.group == 4 ? kQuadConfig : kPairConfig)
+    const TmaConfig& cfg = c.pair  ? (u8 ? (c.group == 4 ? kU8QuadConfig : kU8PairConfig)
+                                         : (c.group == 4 ? kQuadConfig : kPairConfig))
                            : c.ldg ? (u8 ? (ctx->u8ldg_chunk ? kU8LdgConfig : kU8BulkConfig) : kLdgConfigs[ctx->ldg_cfg])
                            : u8    ? kU8Configs[ctx->u8_cfg]
                                    : kTmaConfigs[fcfg];
-    const int occ = std::max(1, c.pair  ? (c.group == 4 ? ctx->occ_quad : ctx->occ_pair)
+    const int occ = std::max(1, c.pair  ? (u8 ? (c.group == 4 ? ctx->occ_u8quad : ctx->occ_u8pair)
+                                                : (c.group == 4 ? ctx->occ_quad : ctx->occ_pair))
                                 : c.ldg ? (u8 ? (ctx->u8ldg_chunk ? ctx->occ_u8ldg : ctx->occ_u8bulk) : ctx->occ_ldg[ctx->ldg_cfg])
                                 : u8    ? ctx->occ_u8[ctx->u8_cfg]
                                         : ctx->occ[fcfg]);
@@ -340,8 +349,28 @@ int encode_tmap_pair(harris_ctx* ctx, const Call& c, CUtensorMap* tmap) {
     return HARRIS_OK;
 }
 
+// row-group view of interleaved u8 (K = 2 / 4 rows): {K*P/4 words, H/K groups, B}
+int encode_tmap_u8_group(harris_ctx* ctx, const Call& c, CUtensorMap* tmap) {
+    const Geom& g = c.g;
+    const int64_t k = c.group;
+    cuuint64_t dims[3] = {cuuint64_t(k * g.in_pitch / 4), cuuint64_t((g.n + 4) / k), cuuint64_t(g.batch)};
+    const int64_t img_stride = g.batch > 1 ? g.in_image_stride : (g.n + 4) * g.in_pitch;
+    cuuint64_t strides[2] = {cuuint64_t(k * g.in_pitch), cuuint64_t(img_stride)};
+    cuuint32_t box[3] = {cuuint32_t(kU8BoxWords), cuuint32_t((k == 2 ? 6 : 12) / k), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = ctx->encode(tmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<float*>(g.rgb), dims, strides, box,
+                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, ctx->promo,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        std::snprintf(ctx->last_err, sizeof(ctx->last_err), "cuTensorMapEncodeTiled (u8 rows) failed (CUresult %d)",
+                      int(r));
+        return HARRIS_ERR_TMA;
+    }
+    return HARRIS_OK;
+}
+
 int encode_tmap(harris_ctx* ctx, const Call& c, CUtensorMap* tmap) {
-    if (c.fmt == kU8Interleaved) return encode_tmap_u8(ctx, c, tmap);
+    if (c.fmt == kU8Interleaved) return c.pair ? encode_tmap_u8_group(ctx, c, tmap) : encode_tmap_u8(ctx, c, tmap);
     if (c.pair) return encode_tmap_pair(ctx, c, tmap);
     const Geom& g = c.g;
     const TmaConfig& cfg = kTmaConfigs[c.cfg >= 0 ? c.cfg : ctx->tma_cfg];
@@ -438,8 +467,10 @@ int run(harris_ctx* ctx, const Call& c, cudaStream_t stream) {
             tg.notify_flag = c.notify_flag;
             tg.notify_epoch = c.notify_epoch;
         }
-        e = pair ? (group == 4 ? launch_tma_quad(exact, ent.tmap, tg, ent.grid, int32_t(c.g.in_pitch), stream)
-                               : launch_tma_pair(exact, ent.tmap, tg, ent.grid, int32_t(c.g.in_pitch), stream))
+        e = pair ? (c.fmt == kU8Interleaved
+                        ? launch_tma_u8_group(group, exact, ent.tmap, tg, ent.grid, int32_t(c.g.in_pitch / 4), stream)
+                    : group == 4 ? launch_tma_quad(exact, ent.tmap, tg, ent.grid, int32_t(c.g.in_pitch), stream)
+                                 : launch_tma_pair(exact, ent.tmap, tg, ent.grid, int32_t(c.g.in_pitch), stream))
             : ldg ? (c.fmt == kU8Interleaved ? launch_u8_ldg(exact, ctx->u8ldg_chunk, c.g, tg, ent.grid, stream)
                                              : launch_ldg(ctx->ldg_cfg, exact, c.g, tg, ent.grid, stream))
             : c.fmt == kU8Interleaved ? launch_tma_u8(ctx->u8_cfg, exact, ent.tmap, tg, ent.grid, stream)
@@ -590,6 +621,7 @@ int harris_init(harris_ctx** out_ctx, int cuda_device) {
     if (e == cudaSuccess) e = quad_configure(&ctx->occ_quad);
     if (e == cudaSuccess) e = sep_ldg_configure(&ctx->occ_sepldg);
     if (e == cudaSuccess) e = u8_ldg_configure(&ctx->occ_u8ldg, &ctx->occ_u8bulk);
+    if (e == cudaSuccess) e = u8_group_configure(&ctx->occ_u8pair, &ctx->occ_u8quad);
     if (e != cudaSuccess) {
         int rc = cuda_fail(ctx, e, "configure u8 ldg kernel");
         delete ctx;

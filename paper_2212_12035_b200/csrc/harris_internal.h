@@ -103,6 +103,12 @@ cudaError_t u8_occupancy(int cfg, int* ctas_per_sm);
 cudaError_t launch_tma_u8(int cfg, bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid,
                           cudaStream_t stream);
 cudaError_t launch_generic_u8(bool exact, const Geom& g, cudaStream_t stream);
+// u8 rows whose pitch is 4, 8 or 12 (mod 16) bytes: TMA over pairs / quads of rows
+extern const TmaConfig kU8PairConfig;
+extern const TmaConfig kU8QuadConfig;
+cudaError_t u8_group_configure(int* occ_pair, int* occ_quad);
+cudaError_t launch_tma_u8_group(int k, bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid,
+                                int32_t pitch_words, cudaStream_t stream);
 
 // separable 3x3 stencil on one f32 plane (stencil_sep.cu)
 constexpr int kNumSepConfigs = 3;

@@ -417,4 +417,74 @@ struct HarrisU8x2Op {
     }
 };
 
+// ------------------------------ interleaved u8 whose row pitch is 4, 8 or 12 (mod 16) bytes
+// (e.g. 1080 or 1366 px wide: 3W % 16 != 0, so TMA cannot step single rows).  K rows (K = 2
+// for pitch = 8 mod 16, 4 for pitch = 4 mod 8) are a 16-byte multiple: the tensor map views
+// each image as H/K group-rows of K*P bytes (32-bit words), image row K*j + r is group-row j
+// at word r*P/4 + x.  A stage of CH rows is, per strip, K boxes (one per row class r) of
+// CH/K group-rows, each starting at its 16-byte aligned-down word and read `skip` words in
+// (a per-tile constant per class and strip).  Packed dual-strip u8 core as the TMA path.
+template <bool EXACT, int K>
+struct HarrisU8RowGroupOp {
+    static_assert(K == 2 || K == 4, "row groups of 2 or 4");
+    static constexpr int CH = K == 2 ? 6 : 12;
+    using L = Strip<124>;
+    static constexpr int kGroups = 2;
+    static constexpr int kStripCols = 124;
+    static constexpr int kRowsPerStage = CH;
+    static constexpr int kHaloRows = 4;
+    static constexpr int kWords = L::kU8BoxWords;
+    static constexpr int kBoxRows = CH / K;  // group-rows per box
+    static constexpr uint32_t kBoxBytes = uint32_t(kBoxRows) * kWords * 4u;
+    static constexpr uint32_t kBoxStride = (kBoxBytes + 127u) / 128u * 128u;
+    static constexpr uint32_t kTxBytes = 2u * K * kBoxBytes;
+    static constexpr uint32_t kStageBytes = 2u * K * kBoxStride;
+    struct Params {
+        float kappa;
+        int32_t pitch_words;  // P / 4
+    };
+    HarrisCore2<EXACT> core;
+    int32_t pw;
+    int skip_a[K], skip_b[K];
+
+    __device__ __forceinline__ explicit HarrisU8RowGroupOp(const Params& p) : core(p.kappa), pw(p.pitch_words) {}
+
+    __device__ __forceinline__ static void load_p(void* smem, const CUtensorMap* tmap, uint64_t* bar,
+                                                  const int (&col0)[2], int row0, const int (&image)[2],
+                                                  uint64_t policy, const Params& p) {
+        const int j0 = row0 / K;  // row0 is a multiple of K (planner)
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int w0 = (col0[k] / 124) * L::kU8Words;
+#pragma unroll
+            for (int r = 0; r < K; ++r)
+                tma_load_3d(static_cast<unsigned char*>(smem) + (k * K + r) * kBoxStride, tmap, bar,
+                            (r * p.pitch_words + w0) & ~3, j0, image[k], policy);
+        }
+    }
+
+    __device__ __forceinline__ void begin_tile(const int (&col0)[2], int, const int (&)[2]) {
+        const int wa = (col0[0] / 124) * L::kU8Words, wb = (col0[1] / 124) * L::kU8Words;
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+            skip_a[r] = (r * pw + wa) & 3;
+            skip_b[r] = (r * pw + wb) & 3;
+        }
+    }
+
+    template <int R>
+    __device__ __forceinline__ void row(const unsigned char* stage, int lane, float (&out)[2][4]) {
+        constexpr int cls = R % K, gr = R / K;
+        const uint32_t* wa =
+            reinterpret_cast<const uint32_t*>(stage + cls * kBoxStride) + gr * kWords + skip_a[cls] + 3 * lane;
+        const uint32_t* wb =
+            reinterpret_cast<const uint32_t*>(stage + (K + cls) * kBoxStride) + gr * kWords + skip_b[cls] + 3 * lane;
+        const uint32_t a[3] = {wa[0], wa[1], wa[2]};
+        const uint32_t b[3] = {wb[0], wb[1], wb[2]};
+        float2 gown[4];
+        gray4_u8x2<EXACT>(a, b, gown[0], gown[1], gown[2], gown[3]);
+        core.template step<R, NoHalo, true>(gown, lane, NoHalo{}, out);
+    }
+};
+
 }  // namespace harris

@@ -171,4 +171,60 @@ cudaError_t launch_tma_u8(int cfg, bool exact, const CUtensorMap& tmap, const Ti
     }
 }
 
+// ---- row-group TMA kernels for u8 rows TMA cannot step singly (HarrisU8RowGroupOp):
+// pairs (pitch = 8 mod 16 bytes, e.g. 1080 px wide) and quads (pitch = 4 mod 8)
+const TmaConfig kU8PairConfig = {8, 4, 6, 2, 124};
+const TmaConfig kU8QuadConfig = {8, 2, 12, 2, 124};
+
+template <int K>
+struct U8GroupCfg {
+    static constexpr int NW = 8, NS = K == 2 ? 4 : 2;
+};
+template <bool EXACT, int K>
+static constexpr auto u8_group_kernel() {
+    return strip_kernel<HarrisU8RowGroupOp<EXACT, K>, U8GroupCfg<K>::NW, U8GroupCfg<K>::NS, 1>;
+}
+template <int K>
+static constexpr size_t u8_group_smem() {
+    return StripShape<U8GroupCfg<K>::NW, U8GroupCfg<K>::NS, HarrisU8RowGroupOp<false, K>>::kSmemBytes;
+}
+static_assert(u8_group_smem<2>() <= 227 * 1024 && u8_group_smem<4>() <= 227 * 1024, "u8 row-group smem");
+
+template <int K>
+static cudaError_t u8_group_configure_one(int* ctas_per_sm) {
+    cudaError_t e = cudaFuncSetAttribute(u8_group_kernel<false, K>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(u8_group_smem<K>()));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(u8_group_kernel<true, K>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(u8_group_smem<K>()));
+    if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, u8_group_kernel<false, K>(),
+                                                          U8GroupCfg<K>::NW * 32, u8_group_smem<K>());
+    return e;
+}
+
+cudaError_t u8_group_configure(int* occ_pair, int* occ_quad) {
+    cudaError_t e = u8_group_configure_one<2>(occ_pair);
+    return e == cudaSuccess ? u8_group_configure_one<4>(occ_quad) : e;
+}
+
+template <bool EXACT, int K>
+static void u8_group_launch_one(const CUtensorMap& tmap, const TileGeom& tg, int64_t grid, int32_t pitch_words,
+                                cudaStream_t stream) {
+    const typename HarrisU8RowGroupOp<EXACT, K>::Params p{tg.kappa, pitch_words};
+    u8_group_kernel<EXACT, K>()<<<unsigned(grid), unsigned(U8GroupCfg<K>::NW * 32), u8_group_smem<K>(), stream>>>(
+        tmap, tg, p);
+}
+
+cudaError_t launch_tma_u8_group(int k, bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid,
+                                int32_t pitch_words, cudaStream_t stream) {
+    if (k == 2)
+        exact ? u8_group_launch_one<true, 2>(tmap, tg, grid, pitch_words, stream)
+              : u8_group_launch_one<false, 2>(tmap, tg, grid, pitch_words, stream);
+    else
+        exact ? u8_group_launch_one<true, 4>(tmap, tg, grid, pitch_words, stream)
+              : u8_group_launch_one<false, 4>(tmap, tg, grid, pitch_words, stream);
+    return cudaGetLastError();
+}
+
 }  // namespace harris

@@ -89,5 +89,8 @@ def test_fuzz_u8_layouts(cuda_ctx, seed):
     torch.cuda.synchronize()
     for b in range(B):
         assert np.array_equal(got[b].cpu().numpy(), cref.harris_f32(f32[b])), (seed, H, W, B, pad, off, path, b)
-    aligned = off % 16 == 0 and pitch % 16 == 0 and (B == 1 or img_stride % 16 == 0)
-    assert path == (_lib.PATH_TMA if aligned else _lib.PATH_LDG)
+    base_ok = off % 16 == 0 and (B == 1 or img_stride % 16 == 0)
+    k = 2 if pitch % 16 == 8 else 4 if pitch % 8 == 4 else 0
+    expect = (_lib.PATH_TMA if base_ok and pitch % 16 == 0 else
+              (_lib.PATH_PAIR if k == 2 else _lib.PATH_QUAD) if base_ok and k and H % k == 0 else _lib.PATH_LDG)
+    assert path == expect, (seed, H, W, B, pad, off, path)

@@ -562,7 +562,7 @@ def test_every_ldg_config_bitexact(cuda_ctx, cfg):
     ctx.close()
 
 
-@pytest.mark.parametrize("H,W", [(5, 5), (13, 17), (40, 130), (64, 200), (300, 1918), (133, 2563)])
+@pytest.mark.parametrize("H,W", [(5, 5), (13, 17), (40, 130), (64, 202), (300, 1918), (133, 2563)])
 def test_u8_ldg_exact_equals_f32_path(cuda_ctx, H, W):
     """3W % 16 != 0 (rows not 16-byte aligned): the u8 cp.async path, bit-identical in
     EXACT order to the planar f32 path / C oracle on byte/255."""
@@ -631,6 +631,34 @@ def test_u8_bulk_every_pitch_residue(cuda_ctx, off):
         assert torch.equal(ex, ex2), (off, pad)
         assert torch.equal(fast, fast2), (off, pad)
     cpa.close()
+
+
+@pytest.mark.parametrize("B,H,W", [(1, 40, 136), (3, 38, 1080), (1, 300, 1080), (2, 44, 132), (1, 140, 1084),
+                                   (1, 64, 44), (2, 30, 2456)])
+def test_u8_row_group_tma(cuda_ctx, B, H, W):
+    """u8 rows of pitch 8 (mod 16) bytes (1080 px: portrait / square video) or 4 (mod 8):
+    TMA over pairs / quads of rows (HarrisU8RowGroupOp), bit-exact in EXACT order against
+    the C oracle and equal to the bulk-copy path on the same bytes at a 1-byte offset."""
+    hwc, f32 = _u8_image(B, H, W, seed=7 * H + W)
+    pitch = 3 * W
+    k = 2 if pitch % 16 == 8 else 4
+    assert pitch % 16 != 0 and H % k == 0
+    x = torch.from_numpy(hwc if B > 1 else hwc[0]).cuda()
+    ex = hb.harris_u8(x, exact=True)
+    assert cuda_ctx.last_path == (_lib.PATH_PAIR if k == 2 else _lib.PATH_QUAD)
+    fast = hb.harris_u8(x)
+    buf = torch.zeros(hwc.size + 1, dtype=torch.uint8, device="cuda")
+    mis = buf[1:].view(x.shape)
+    mis.copy_(x)
+    ex_b = hb.harris_u8(mis, exact=True)
+    assert cuda_ctx.last_path == _lib.PATH_LDG
+    torch.cuda.synchronize()
+    ex, fast = ex.cpu().numpy().reshape(B, H - 4, W - 4), fast.cpu().numpy().reshape(B, H - 4, W - 4)
+    for b in range(B):
+        assert np.array_equal(ex[b], cref.harris_f32(f32[b])), (B, H, W, b)
+        ok, m = synth.within_tolerance(fast[b], cref.harris_f64(f32[b]))
+        assert ok, (B, H, W, b, m)
+    assert np.array_equal(ex_b.cpu().numpy().reshape(B, H - 4, W - 4), ex)
 
 
 def test_concurrent_streams_and_threads(cuda_ctx):
