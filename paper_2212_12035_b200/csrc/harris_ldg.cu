@@ -1,15 +1,22 @@
 // harris_ldg.cu — the fused Harris strip engine for inputs TMA cannot describe.
 //
-// TMA needs 16-byte aligned row starts and strides; a planar image whose width is not a
-// multiple of 4 floats (1918, 8190, 4255 ...) or whose base is only 4-byte aligned has
-// neither.  Such inputs used to fall back to the generic shared-memory tile kernel K0
-// (118 k MP/s, 29 % of HBM).  This op keeps everything of the TMA path — the warp-strip
-// pipeline, the packed FP32x2 dual-strip core, the stage ring and its mbarriers — and
-// only replaces the stage fill: all 32 lanes copy the stage's 2 boxes x 3 channels x CH
-// rows x 132 columns with 4-byte cp.async (LDGSTS) into exactly the shared-memory layout
-// the TMA box has, and each lane's `cp.async.mbarrier.arrive.noinc` completes the stage
-// barrier once its copies have landed.  Rows beyond the image are skipped and columns
-// beyond the row end are zero-filled; neither reaches a stored output.
+// TMA needs 16-byte aligned row starts and strides; a planar image whose rows are not
+// 16-byte multiples (and not served by the pair- / quad-row tensor maps), a column-crop
+// view whose base is only 4-byte aligned, or interleaved u8 rows of arbitrary byte pitch
+// have neither.  Such inputs used to fall back to the generic shared-memory tile kernel
+// K0 (118 k MP/s, 29 % of HBM).  The ops here keep everything of the TMA path — the
+// warp-strip pipeline, the cores, the stage ring and its mbarriers — and only replace the
+// stage fill, in two ways:
+//  * K1b (default): one `cp.async.bulk` per stage row, issued by its own lane, counted as
+//    transaction bytes on the stage mbarrier like a TMA box (F32BulkOp, U8BulkOp,
+//    SepBulkOp; bulk_stage_fill).  The consumer reads each row at its skew from the
+//    16-byte aligned-down copy start.
+//  * K2: all 32 lanes copy the stage with 4-byte (u8: 4/16-byte) cp.async (LDGSTS) into the
+//    TMA box's shared-memory layout, each lane's `cp.async.mbarrier.arrive.noinc`
+//    completing the stage barrier (LdgOp, U8LdgOp; HARRIS_LDG_CONFIG 0-2,
+//    HARRIS_U8LDG_CHUNK 4/16).
+// Rows beyond the image are skipped and columns beyond the row end are stale or
+// zero-filled; neither reaches a stored output.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -442,7 +449,9 @@ struct U8BulkOp : std::conditional_t<G == 2, HarrisU8x2Op<EXACT, CH, 124>, Harri
 };
 
 #ifndef HARRIS_U8BULK_G
-#define HARRIS_U8BULK_G 1  // scalar core, 16 warps/SM: 613 k vs 610 k (dual, 8 warps) on 512 x 1080x1918, 578 k vs 543 k on 8192x8191
+// scalar core, 16 warps/SM: 613 k vs 610 k (dual, 8 warps) on 512 x 1080x1918, 578 k vs 543 k
+// on 8192x8191
+#define HARRIS_U8BULK_G 1
 #endif
 constexpr int kU8BulkG = HARRIS_U8BULK_G;
 constexpr int kU8BulkNW = 8, kU8BulkNS = 4, kU8BulkCH = 6, kU8BulkMinB = kU8BulkG == 2 ? 1 : 2;
