@@ -363,6 +363,7 @@ __device__ __forceinline__ void gray4_u8x2(const uint32_t (&a)[3], const uint32_
 template <bool EXACT, int CH, int SC = 128>
 struct HarrisU8x2Op {
     static_assert(CH % 3 == 0, "row rotation needs CH % 3 == 0");
+    static constexpr bool kTwoStoreVariants = true;  // issue-bound: measured +5.6 %
     using L = Strip<SC>;
     static constexpr int kGroups = 2;
     static constexpr int kStripCols = SC;

@@ -19,6 +19,7 @@ struct Sep3x3Op {
     static constexpr int kStripCols = kWarpCols;
     static constexpr int kRowsPerStage = CH;
     static constexpr int kHaloRows = 2;
+    static constexpr bool kTwoStoreVariants = true;  // measured +5 % on unaligned planes
     static constexpr uint32_t kTxBytes = uint32_t(CH) * kBoxCols * 4u;
     static constexpr uint32_t kStageBytes = (kTxBytes + 127u) / 128u * 128u;
     struct Params {

@@ -118,6 +118,16 @@ struct SplitStoresOf : std::false_type {};
 template <class Op>
 struct SplitStoresOf<Op, std::void_t<decltype(Op::kSplitStores)>> : std::integral_constant<bool, Op::kSplitStores> {};
 
+// Op::kTwoStoreVariants is optional (default false): compile the consumer's stage loop twice,
+// with and without the scalar-store code for ragged / unaligned output lanes.  Measured per
+// op (tools/perf_matrix.sh): issue-bound u8 TMA 840 -> 887 k MP/s, stencil on 1918-wide
+// planes 727 -> 763 k; but the f32 TMA op -1.8 % and the u8 row-group op -4 % (code size)
+template <class Op, class = void>
+struct TwoStoreVariantsOf : std::false_type {};
+template <class Op>
+struct TwoStoreVariantsOf<Op, std::void_t<decltype(Op::kTwoStoreVariants)>>
+    : std::integral_constant<bool, Op::kTwoStoreVariants> {};
+
 // Op::load_p(smem, tmap, bar, cols, row0, imgs, policy, params) is optional: a TMA stage fill
 // that needs the kernel parameters (the pair-row op's odd-row column offset)
 template <class Op, class = void>
@@ -312,43 +322,56 @@ __global__ void __launch_bounds__(NW * 32, MINB)
         }
         ragged = __any_sync(0xffffffffu, ragged);
 
-        for (int c = 0; c < nch; ++c) {
-            mbar_wait(&bars[stage], phase);
-            const unsigned char* sm = ring + stage * Op::kStageBytes;
-            static_for(
-                [&](auto rc) {
-                    constexpr int R = decltype(rc)::value;
-                    const int i = c * CH + R;  // input row within the tile
-                    float out4[G][4];
-                    op.template row<R>(sm, lane, out4);
-                    if (i >= HALO && i - HALO < rows_out) {
-#pragma unroll
-                        for (int gi = 0; gi < G; ++gi) {
-                            float* po = orow[gi] + int64_t(i - HALO) * g.out_pitch;
-                            stg128_cs_if(vec[gi], po, out4[gi][0], out4[gi][1], out4[gi][2], out4[gi][3]);
-                            if (ragged) {  // unaligned output rows, or the ragged right edge
-                                const int cg = colg[gi];
-                                if (!vec[gi] && cg < g.m) {
-                                    if (SplitStoresOf<Op>::value && g.vec_store == 1 && cg + kColsPerLane <= g.m) {
-                                        stg2x2_cs(po, out4[gi][0], out4[gi][1], out4[gi][2], out4[gi][3]);
-                                    } else {
-#pragma unroll
-                                        for (int k = 0; k < kColsPerLane; ++k)
-                                            if (cg + k < g.m) po[k] = out4[gi][k];
-                                    }
-                                }
-                            }
-                        }
-                    }
-                },
-                std::make_integer_sequence<int, CH>{});
-            __syncwarp();  // every lane is done with this stage: refill it
-            issue(stage);
-            if (++stage == NS) {
-                stage = 0;
-                phase ^= 1u;
+        // the stage loop (a macro so that ops with Op::kTwoStoreVariants get it twice — tiles
+        // without ragged / unaligned output lanes then carry no scalar-store code — while every
+        // other op keeps the single runtime-tested copy: a lambda wrapper alone changed their
+        // code generation, -4.5 % on the u8 row-group op)
+#define HARRIS_STAGE_LOOP(RAGGED)                                                                                \
+    for (int c = 0; c < nch; ++c) {                                                                              \
+        mbar_wait(&bars[stage], phase);                                                                          \
+        const unsigned char* sm = ring + stage * Op::kStageBytes;                                                \
+        static_for(                                                                                              \
+            [&](auto rc) {                                                                                       \
+                constexpr int R = decltype(rc)::value;                                                           \
+                const int i = c * CH + R; /* input row within the tile */                                        \
+                float out4[G][4];                                                                                \
+                op.template row<R>(sm, lane, out4);                                                              \
+                if (i >= HALO && i - HALO < rows_out) {                                                          \
+                    _Pragma("unroll") for (int gi = 0; gi < G; ++gi) {                                           \
+                        float* po = orow[gi] + int64_t(i - HALO) * g.out_pitch;                                  \
+                        stg128_cs_if(vec[gi], po, out4[gi][0], out4[gi][1], out4[gi][2], out4[gi][3]);           \
+                        if (RAGGED) { /* unaligned output rows, or the ragged right edge */                      \
+                            const int cg = colg[gi];                                                             \
+                            if (!vec[gi] && cg < g.m) {                                                          \
+                                if (SplitStoresOf<Op>::value && g.vec_store == 1 && cg + kColsPerLane <= g.m) {  \
+                                    stg2x2_cs(po, out4[gi][0], out4[gi][1], out4[gi][2], out4[gi][3]);           \
+                                } else {                                                                         \
+                                    _Pragma("unroll") for (int k = 0; k < kColsPerLane; ++k) if (cg + k < g.m)   \
+                                        po[k] = out4[gi][k];                                                     \
+                                }                                                                                \
+                            }                                                                                    \
+                        }                                                                                        \
+                    }                                                                                            \
+                }                                                                                                \
+            },                                                                                                   \
+            std::make_integer_sequence<int, CH>{});                                                              \
+        __syncwarp(); /* every lane is done with this stage: refill it */                                        \
+        issue(stage);                                                                                            \
+        if (++stage == NS) {                                                                                     \
+            stage = 0;                                                                                           \
+            phase ^= 1u;                                                                                         \
+        }                                                                                                        \
+    }
+        if constexpr (TwoStoreVariantsOf<Op>::value) {
+            if (ragged) {
+                HARRIS_STAGE_LOOP(true)
+            } else {
+                HARRIS_STAGE_LOOP(false)
             }
+        } else {
+            HARRIS_STAGE_LOOP(ragged)
         }
+#undef HARRIS_STAGE_LOOP
     }
     notify_epilogue(g);
 }
