@@ -428,6 +428,7 @@ struct HarrisU8x2Op {
 template <bool EXACT, int K>
 struct HarrisU8RowGroupOp {
     static_assert(K == 2 || K == 4, "row groups of 2 or 4");
+    static constexpr bool kTwoStoreVariants = true;  // measured +1.2 % (the f32 TMA op: -1.5 %)
     static constexpr int CH = K == 2 ? 6 : 12;
     using L = Strip<124>;
     static constexpr int kGroups = 2;
