@@ -661,6 +661,25 @@ def test_u8_row_group_tma(cuda_ctx, B, H, W):
     assert np.array_equal(ex_b.cpu().numpy().reshape(B, H - 4, W - 4), ex)
 
 
+def test_u8_row_group_band_views(cuda_ctx):
+    """Row bands (4-row halo views, the multi-GPU split) of a 1080-wide u8 image: bands at
+    even starts stay on the row-pair TMA kernel, odd starts (base 8 bytes off 16) go to the
+    bulk-copy engine; EXACT results of every band equal the single launch bit-for-bit."""
+    H, W = 300, 1080
+    hwc, _ = _u8_image(1, H, W, seed=4242)
+    x = torch.from_numpy(hwc[0]).cuda()
+    full = hb.harris_u8(x, exact=True)
+    assert cuda_ctx.last_path == _lib.PATH_PAIR
+    n = H - 4
+    paths = set()
+    for r0, r1 in ((0, 100), (100, 151), (151, 222), (222, n)):
+        band = hb.harris_u8(x[r0: r1 + 4], exact=True)
+        paths.add(cuda_ctx.last_path)
+        torch.cuda.synchronize()
+        assert torch.equal(band, full[r0:r1]), (r0, r1)
+    assert paths == {_lib.PATH_PAIR, _lib.PATH_LDG}
+
+
 def test_concurrent_streams_and_threads(cuda_ctx):
     """One ctx driven from 4 host threads on 4 streams (ctypes drops the GIL, so the C
     launch path and its launch cache really run concurrently); every result bit-exact."""
