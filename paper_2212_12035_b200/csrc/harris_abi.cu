@@ -48,7 +48,11 @@ struct harris_ctx {
                       // 404 k MP/s on a column-crop view of 256 x 1080p; the cp.async config 2: 296 k)
     int sync_waves = 1;  // dev knob HARRIS_SYNC_WAVES=0 disables the per-tile CTA barrier
     int sep_bulk = 0;  // HARRIS_SEP_BULK: aligned stencil planes through the bulk-copy kernel too
-    int l2_policy = 1;  // evict_normal: the 4-column halo sectors are re-read by the neighbouring strip
+    // TMA input loads evict_last: the 4-column halo sectors one strip loads are re-read by its
+    // neighbour; +0.6-1.3 % over evict_normal on every shape of tools/perf_matrix.sh (f32 batch
+    // 413 -> 416 k, 8192^2 398 -> 403 k, u8 886 -> 894 k).  Input lines of a finished launch
+    // stay evict_last in L2 until displaced; HARRIS_L2_POLICY=1 restores evict_normal.
+    int l2_policy = 2;
     int64_t force_band_rows = 0;  // dev knob (HARRIS_BAND_ROWS): override the planner
     CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;  // dev knob HARRIS_L2_PROMO
     int occ[kNumTmaConfigs] = {0};
