@@ -131,11 +131,25 @@ struct LdgOp : BaseOp {
     }
 };
 
+// EVICT_LAST: L2 evict_last hint like the TMA input loads (halo sectors are re-read by the
+// neighbouring strip): +2 % on memory-bound f32 planes, -1 % on the issue-bound u8 / stencil
+// ops (the extra createpolicy), so only F32BulkOp asks for it
+template <bool EVICT_LAST = false>
 __device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(smem)),
-                 "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
+    if constexpr (EVICT_LAST) {
+        uint64_t policy;
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(policy));
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+            "%4;" ::"r"(smem_u32(smem)),
+            "l"(gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+            : "memory");
+    } else {
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(smem)),
+                     "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+                     : "memory");
+    }
 }
 
 // The stage fill of the bulk-copy ops: each active lane copies one stage row — the bytes
@@ -168,7 +182,7 @@ __device__ __noinline__ uint32_t bulk_tail_fix(unsigned char* dst, const unsigne
 // rounding can reach past it): the stage that holds an image's last row (warp-uniform test)
 // sends that row's lane through bulk_tail_fix.  A separate instantiation because even the
 // untaken test measured 2-6 % slower on every other stage.
-template <bool STRICT>
+template <bool STRICT, bool EVICT_LAST = false>
 __device__ __forceinline__ void bulk_stage_fill(unsigned char* dst, const void* src, uint32_t need, uint32_t cap,
                                                 const void* limit, uint64_t* bar, bool active,
                                                 bool stage_has_last_row, bool last_row, int lane) {
@@ -187,7 +201,7 @@ __device__ __forceinline__ void bulk_stage_fill(unsigned char* dst, const void* 
     if constexpr (STRICT) __syncwarp();  // the tail's shared stores before lane 0's release
     if (lane == 0) mbar_arrive_expect_tx(bar, total);
     __syncwarp();
-    if (nb) bulk_g2s(dst, al, nb, bar);
+    if (nb) bulk_g2s<EVICT_LAST>(dst, al, nb, bar);
 }
 
 // ---- planar f32 through the bulk-copy engine (K1b): every (channel, row) of a stage is
@@ -243,9 +257,10 @@ struct F32BulkOp : std::conditional_t<G == 2, HarrisF32x2Op<EXACT, CH, 124>, Har
         const int img = k ? image[G - 1] : image[0], c0 = k ? col0[G - 1] : col0[0];  // selects: no local array
         const float* src =
             p.src + int64_t(img) * p.in_image_stride + int64_t(ch) * p.in_plane_stride + int64_t(y) * p.in_pitch + c0;
-        bulk_stage_fill<STRICT>(static_cast<unsigned char*>(smem) + k * kBoxStride + (ch * CH + r) * (kRowFloats * 4), src,
-                        uint32_t(p.W - c0) * 4u, kRowFloats * 4, p.limit, bar, lane < G * 3 * CH && y < p.H,
-                        row0 + CH > p.H - 1 && row0 <= p.H - 1, y == p.H - 1, lane);
+        bulk_stage_fill<STRICT, true>(
+            static_cast<unsigned char*>(smem) + k * kBoxStride + (ch * CH + r) * (kRowFloats * 4), src,
+            uint32_t(p.W - c0) * 4u, kRowFloats * 4, p.limit, bar, lane < G * 3 * CH && y < p.H,
+            row0 + CH > p.H - 1 && row0 <= p.H - 1, y == p.H - 1, lane);
     }
 
     // 4 floats at q + s (q 16-byte aligned, s warp-uniform in 0..3)
