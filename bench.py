@@ -450,7 +450,7 @@ def run_gpu(a, world, rank, local) -> dict | None:
                          "inputs smaller than L2: see extra.l2_flushed",
                    "kernel": "strip_kernel<HarrisF32x2Op> (fused gray/Sobel/products/box/coarsity, per-warp TMA "
                              "ring, packed FP32x2 dual-strip core, FAST order)",
-                   "tma_config": os.environ.get("HARRIS_TMA_CONFIG", "default"), "plan": plan},
+                   "dev_knobs": os.environ.get("HARRIS_DEV") == "1", "plan": plan},
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,

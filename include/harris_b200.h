@@ -83,6 +83,27 @@ typedef struct harris_ctx harris_ctx;
  * configures the kernels.  cuda_device < 0 means the current device. */
 HARRIS_API int harris_init(harris_ctx** ctx, int cuda_device);
 
+/* Options of harris_init_ex (harris_init = harris_init_ex with harris_options_default).
+ * Call harris_options_default first, then set fields; struct_size guards layout growth. */
+#define HARRIS_L2_EVICT_FIRST  0
+#define HARRIS_L2_EVICT_NORMAL 1
+#define HARRIS_L2_EVICT_LAST   2  /* default: a strip's 4-column halo sectors are re-read by its
+                                     neighbouring strip (+0.6-2 % on every shape).  The input lines of
+                                     a finished launch keep evict_last priority in L2 until displaced;
+                                     pick EVICT_NORMAL when the caller's next kernels need the L2. */
+typedef struct harris_options {
+    uint32_t struct_size;  /* sizeof(harris_options) */
+    int32_t l2_policy;     /* HARRIS_L2_* for the input loads of every kernel path */
+    int32_t band_rows;     /* output rows per tile; 0 = the library's planner */
+    int32_t reserved[5];
+} harris_options;
+
+HARRIS_API void harris_options_default(harris_options* opts);
+/* harris_init with options (NULL = defaults).  Developer knobs are read from the
+ * environment only when HARRIS_DEV=1 (kernel configurations, tiling, L2 promotion);
+ * otherwise the environment never changes the library's behaviour. */
+HARRIS_API int harris_init_ex(harris_ctx** ctx, int cuda_device, const harris_options* opts);
+
 /* ~ <name>_destroy. NULL is accepted. */
 HARRIS_API void harris_destroy(harris_ctx* ctx);
 

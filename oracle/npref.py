@@ -50,3 +50,40 @@ def harris_np(rgb: np.ndarray, kappa: float = 0.04, dtype=np.float32) -> np.ndar
     det = Sxx * Syy - Sxy * Sxy
     tr = Sxx + Syy
     return (det - (k * tr) * tr).astype(dtype)
+
+
+def harris_rrot_np(rgb: np.ndarray, kappa: float = 0.04) -> np.ndarray:
+    """f32 restatement of the thesis's cbuf+rrot schedule's ARITHMETIC:
+    separated Sobel — vertical [1,2,1] sum / [-1,0,1] difference of gray columns
+    (PAPER.md:4777-4790), then the horizontal -1/12, 0, 1/12 and 1/12, 1/6, 1/12 taps
+     — and box sums as vertical 3-row sums of the products followed by
+    horizontal 3-sums, every accumulation from 0 in listing order.
+    Independent of oracle/harris_oracle.c's line buffers; pins oracle_harris_f32_rrot."""
+    rgb = np.asarray(rgb, dtype=np.float32)
+    if rgb.ndim != 3 or rgb.shape[0] != 3 or rgb.shape[1] < 5 or rgb.shape[2] < 5:
+        raise ValueError("rgb must be (3, H>=5, W>=5)")
+    f = np.float32
+    z = f(0.0)
+    g = ((z + f(0.299) * rgb[0]) + f(0.587) * rgb[1]) + f(0.114) * rgb[2]
+    H, W = g.shape
+    g0, g1, g2 = g[0:H - 2], g[1:H - 1], g[2:H]
+    vs = ((z + f(1.0) * g0) + f(2.0) * g1) + f(1.0) * g2
+    vd = ((z + f(-1.0) * g0) + f(0.0) * g1) + f(1.0) * g2
+    a, b = f(0.083333336), f(0.16666667)
+    c0, c1, c2 = slice(0, W - 2), slice(1, W - 1), slice(2, W)
+    Ix = ((z + (-a) * vs[:, c0]) + z * vs[:, c1]) + a * vs[:, c2]
+    Iy = ((z + a * vd[:, c0]) + b * vd[:, c1]) + a * vd[:, c2]
+    n, m = H - 4, W - 4
+    r0, r1, r2 = slice(0, n), slice(1, n + 1), slice(2, n + 2)
+
+    def vsum(p, q):
+        return ((z + p[r0] * q[r0]) + p[r1] * q[r1]) + p[r2] * q[r2]
+
+    vxx, vxy, vyy = vsum(Ix, Ix), vsum(Ix, Iy), vsum(Iy, Iy)
+
+    def hsum(v):
+        return ((z + v[:, 0:m]) + v[:, 1:m + 1]) + v[:, 2:m + 2]
+
+    sxx, sxy, syy = hsum(vxx), hsum(vxy), hsum(vyy)
+    k = f(kappa)
+    return ((sxx * syy - sxy * sxy) - (k * (sxx + syy)) * (sxx + syy)).astype(np.float32)

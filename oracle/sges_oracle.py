@@ -1,9 +1,11 @@
 """Drive the reference package's own evaluator on the thesis Harris program.
 
-TEST INFRASTRUCTURE ONLY — needs ``/root/reference`` (present in the build
-container, absent on the GPU box), so it is used solely by
-``tests/golden/make_golden.py`` (which commits its outputs as fixtures) and by
-CPU tests that skip when the reference is missing.
+TEST INFRASTRUCTURE ONLY — needs the reference package ``sges``: the tree under
+``/root/reference`` (build container) or the unmodified package pip-installed into
+``baseline/_ref`` (which travels to the GPU box).  Used by
+``tests/golden/make_golden.py`` (which commits its outputs as fixtures), by tests
+that skip when the reference is missing, and by ``bench.py --impl reference`` to time
+the reference evaluator itself.
 
 The term is the point-free spelling of the thesis Rise ``harris``
 (grayscale 2430-2432, slide2d/stencil2d 2461-2465,
@@ -28,7 +30,23 @@ from typing import Callable, Optional
 
 import numpy as np
 
-REFERENCE_SRC = os.environ.get("HARRIS_REFERENCE_SRC", "/root/reference/pkg/src")
+_ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _default_src() -> str:
+    """HARRIS_REFERENCE_SRC, else the reference tree (build container), else the unmodified
+    reference package pip-installed into baseline/_ref (travels to the GPU box; see
+    __graft_entry__.build)."""
+    env = os.environ.get("HARRIS_REFERENCE_SRC")
+    if env:
+        return env
+    for cand in ("/root/reference/pkg/src", os.path.join(_ROOT, "baseline", "_ref")):
+        if os.path.isdir(os.path.join(cand, "sges")):
+            return cand
+    return "/root/reference/pkg/src"
+
+
+REFERENCE_SRC = _default_src()
 
 
 def available() -> bool:

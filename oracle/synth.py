@@ -96,3 +96,41 @@ def within_tolerance(out: np.ndarray, ref: np.ndarray) -> tuple[bool, dict]:
     pix = bool(np.all(np.abs(out64 - ref64) <= 1e-5 * np.abs(ref64) + 1e-5 * mx))
     ok = bool(np.all(np.isfinite(out64))) and nl <= NORM_LINF_TOL and ps >= PSNR_MIN_DB and pix
     return ok, {"norm_linf": nl, "psnr_db": ps, "per_pixel_ok": pix}
+
+
+class ToleranceAccumulator:
+    """within_tolerance over an image checked in chunks (rows bands of one image too big to
+    hold its f64 reference at once): accumulates max|d|, max|ref|, sum d^2, the pixel count
+    and the worst per-pixel slack max(|d| - 1e-5|ref|), so ``result()`` equals
+    ``within_tolerance`` on the concatenated image exactly (the per-pixel bound's
+    1e-5*max|ref| term uses the WHOLE image's max)."""
+
+    def __init__(self) -> None:
+        self.max_d = 0.0
+        self.max_ref = 0.0
+        self.sum_d2 = 0.0
+        self.count = 0
+        self.slack = -np.inf
+        self.finite = True
+
+    def add(self, out: np.ndarray, ref: np.ndarray) -> None:
+        o = np.asarray(out, dtype=np.float64)
+        r = np.asarray(ref, dtype=np.float64)
+        if o.size == 0:
+            return
+        self.finite &= bool(np.all(np.isfinite(o)))
+        d = np.abs(o - r)
+        ar = np.abs(r)
+        self.max_d = max(self.max_d, float(d.max()))
+        self.max_ref = max(self.max_ref, float(ar.max()))
+        self.sum_d2 += float(np.dot(d.ravel(), d.ravel()))
+        self.count += d.size
+        self.slack = max(self.slack, float(np.max(d - 1e-5 * ar)))
+
+    def result(self) -> tuple[bool, dict]:
+        nl = self.max_d / self.max_ref if self.max_ref else self.max_d
+        mse = self.sum_d2 / self.count if self.count else 0.0
+        ps = float("inf") if mse == 0.0 else 10.0 * np.log10(1.0 / mse)
+        pix = bool(self.slack <= 1e-5 * self.max_ref)
+        ok = self.finite and nl <= NORM_LINF_TOL and ps >= PSNR_MIN_DB and pix
+        return ok, {"norm_linf": nl, "psnr_db": ps, "per_pixel_ok": pix, "pixels": self.count}

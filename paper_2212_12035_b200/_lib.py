@@ -33,7 +33,7 @@ PATH_NONE, PATH_TMA, PATH_GENERIC, PATH_LDG, PATH_PAIR, PATH_QUAD = 0, 1, 2, 3, 
 
 # every symbol include/harris_b200.h declares (checked by tests/test_abi.py)
 EXPORTED_SYMBOLS = (
-    "harris_init", "harris_destroy", "harris_run", "harris_run_batched", "harris_run_strided",
+    "harris_init", "harris_init_ex", "harris_options_default", "harris_destroy", "harris_run", "harris_run_batched", "harris_run_strided",
     "harris_run_host", "harris_synth_fill", "harris_plan", "harris_last_path", "harris_device",
     "harris_num_sms", "harris_strerror", "harris_last_cuda_error", "harris_abi_version",
     "harris_grouping_scratch_bytes", "harris_grouping_launches", "harris_run_grouping",
@@ -41,6 +41,8 @@ EXPORTED_SYMBOLS = (
     "harris_peer_export", "harris_peer_open", "harris_peer_close", "harris_run_notify",
     "harris_peer_signal", "harris_peer_wait",
 )
+
+L2_EVICT_FIRST, L2_EVICT_NORMAL, L2_EVICT_LAST = 0, 1, 2
 
 GROUPING_UNFUSED, GROUPING_SOBEL_PROD, GROUPING_SOBEL, GROUPING_FUSED = 1, 2, 3, 4
 
@@ -65,6 +67,12 @@ class PlanInfo(ctypes.Structure):
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+
+
+class Options(ctypes.Structure):
+    """harris_options (include/harris_b200.h): fill with harris_options_default first."""
+    _fields_ = [("struct_size", ctypes.c_uint32), ("l2_policy", ctypes.c_int32), ("band_rows", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 5)]
 
 
 class PeerHandle(ctypes.Structure):
@@ -106,6 +114,8 @@ def lib() -> ctypes.CDLL:
                                    ctypes.c_uint64, ctypes.c_float)
     sig = {
         "harris_init": ([ctypes.POINTER(vp), i32], i32),
+        "harris_init_ex": ([ctypes.POINTER(vp), i32, ctypes.POINTER(Options)], i32),
+        "harris_options_default": ([ctypes.POINTER(Options)], None),
         "harris_destroy": ([vp], None),
         "harris_run": ([vp, vp, i64, i64, i64, vp, f32, vp], i32),
         "harris_run_batched": ([vp, vp, i64, i64, vp, i64, f32, vp], i32),

@@ -533,9 +533,28 @@ const char* harris_strerror(int code) {
     }
 }
 
-int harris_init(harris_ctx** out_ctx, int cuda_device) {
+void harris_options_default(harris_options* o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof(*o));
+    o->struct_size = uint32_t(sizeof(harris_options));
+    o->l2_policy = HARRIS_L2_EVICT_LAST;
+    o->band_rows = 0;
+}
+
+int harris_init(harris_ctx** out_ctx, int cuda_device) { return harris_init_ex(out_ctx, cuda_device, nullptr); }
+
+int harris_init_ex(harris_ctx** out_ctx, int cuda_device, const harris_options* opts) {
     if (!out_ctx) return HARRIS_ERR_INVALID_ARGUMENT;
     *out_ctx = nullptr;
+    harris_options o;
+    harris_options_default(&o);
+    if (opts) {
+        if (opts->struct_size < uint32_t(offsetof(harris_options, reserved))) return HARRIS_ERR_INVALID_ARGUMENT;
+        if (opts->l2_policy < HARRIS_L2_EVICT_FIRST || opts->l2_policy > HARRIS_L2_EVICT_LAST) return HARRIS_ERR_INVALID_ARGUMENT;
+        if (opts->band_rows < 0) return HARRIS_ERR_INVALID_ARGUMENT;
+        o.l2_policy = opts->l2_policy;
+        o.band_rows = opts->band_rows;
+    }
     int count = 0;
     if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
         cudaGetLastError();
@@ -560,48 +579,55 @@ int harris_init(harris_ctx** out_ctx, int cuda_device) {
         delete ctx;
         return HARRIS_ERR_UNSUPPORTED_DEVICE;
     }
-    const char* env = std::getenv("HARRIS_TMA_CONFIG");
-    if (env) {
-        int v = std::atoi(env);
-        if (v >= 0 && v < kNumTmaConfigs) {
-            ctx->tma_cfg = v;
-            ctx->tma_cfg_forced = true;
+    ctx->l2_policy = o.l2_policy;
+    ctx->force_band_rows = o.band_rows;
+    // Developer knobs (kernel configuration, tiling, L2 promotion / policy): read only with
+    // HARRIS_DEV=1 so a drop-in library never changes behaviour from the environment.
+    const char* dev_env = std::getenv("HARRIS_DEV");
+    if (dev_env && std::atoi(dev_env) == 1) {
+        const char* env = std::getenv("HARRIS_TMA_CONFIG");
+        if (env) {
+            int v = std::atoi(env);
+            if (v >= 0 && v < kNumTmaConfigs) {
+                ctx->tma_cfg = v;
+                ctx->tma_cfg_forced = true;
+            }
         }
-    }
-    env = std::getenv("HARRIS_U8_CONFIG");
-    if (env) {
-        int v = std::atoi(env);
-        if (v >= 0 && v < kNumU8Configs) ctx->u8_cfg = v;
-    }
-    env = std::getenv("HARRIS_SEP_BULK");
-    if (env) ctx->sep_bulk = std::atoi(env) != 0;
-    env = std::getenv("HARRIS_SEP_CONFIG");
-    if (env) {
-        int v = std::atoi(env);
-        if (v >= 0 && v < kNumSepConfigs) ctx->sep_cfg = v;
-    }
-    env = std::getenv("HARRIS_U8LDG_CHUNK");
-    if (env) ctx->u8ldg_chunk = std::atoi(env) == 4 ? 4 : std::atoi(env) == 16 ? 16 : 0;
-    env = std::getenv("HARRIS_LDG_CONFIG");
-    if (env) {
-        int v = std::atoi(env);
-        if (v >= 0 && v < kNumLdgConfigs) ctx->ldg_cfg = v;
-    }
-    env = std::getenv("HARRIS_SYNC_WAVES");
-    if (env) ctx->sync_waves = std::atoi(env) != 0;
-    env = std::getenv("HARRIS_L2_PROMO");
-    if (env) {
-        const int v = std::atoi(env);
-        const CUtensorMapL2promotion tab[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
-                                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
-        if (v >= 0 && v < 4) ctx->promo = tab[v];
-    }
-    env = std::getenv("HARRIS_BAND_ROWS");
-    if (env) ctx->force_band_rows = std::atoll(env);
-    env = std::getenv("HARRIS_L2_POLICY");
-    if (env) {
-        int v = std::atoi(env);
-        if (v >= 0 && v <= 2) ctx->l2_policy = v;
+        env = std::getenv("HARRIS_U8_CONFIG");
+        if (env) {
+            int v = std::atoi(env);
+            if (v >= 0 && v < kNumU8Configs) ctx->u8_cfg = v;
+        }
+        env = std::getenv("HARRIS_SEP_BULK");
+        if (env) ctx->sep_bulk = std::atoi(env) != 0;
+        env = std::getenv("HARRIS_SEP_CONFIG");
+        if (env) {
+            int v = std::atoi(env);
+            if (v >= 0 && v < kNumSepConfigs) ctx->sep_cfg = v;
+        }
+        env = std::getenv("HARRIS_U8LDG_CHUNK");
+        if (env) ctx->u8ldg_chunk = std::atoi(env) == 4 ? 4 : std::atoi(env) == 16 ? 16 : 0;
+        env = std::getenv("HARRIS_LDG_CONFIG");
+        if (env) {
+            int v = std::atoi(env);
+            if (v >= 0 && v < kNumLdgConfigs) ctx->ldg_cfg = v;
+        }
+        env = std::getenv("HARRIS_SYNC_WAVES");
+        if (env) ctx->sync_waves = std::atoi(env) != 0;
+        env = std::getenv("HARRIS_L2_PROMO");
+        if (env) {
+            const int v = std::atoi(env);
+            const CUtensorMapL2promotion tab[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
+                                                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
+            if (v >= 0 && v < 4) ctx->promo = tab[v];
+        }
+        env = std::getenv("HARRIS_BAND_ROWS");
+        if (env) ctx->force_band_rows = std::atoll(env);
+        env = std::getenv("HARRIS_L2_POLICY");
+        if (env) {
+            int v = std::atoi(env);
+            if (v >= 0 && v <= 2) ctx->l2_policy = v;
+        }
     }
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -971,13 +997,19 @@ static int run_host_impl(harris_ctx* ctx, int fmt, float* out_host, int64_t out_
                 c = make_call(dout, m, rows * m, rows, m, reinterpret_cast<const float*>(din), W, rin * W,
                               3 * rin * W, 1, kappa, flags);
             }
-            if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D band");
+            if (e != cudaSuccess) {  // stop issuing; the final sync below still drains every slot
+                rc = cuda_fail(ctx, e, "H2D band");
+                break;
+            }
         } else {
             b0 = k * imgs_per_chunk;
             nb = std::min(imgs_per_chunk, batch - b0);
             e = cudaMemcpyAsync(din, src + size_t(b0 * img_bytes), size_t(nb * img_bytes), cudaMemcpyHostToDevice,
                                 s);
-            if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D images");
+            if (e != cudaSuccess) {  // stop issuing; the final sync below still drains every slot
+                rc = cuda_fail(ctx, e, "H2D images");
+                break;
+            }
             c = u8 ? make_call(dout, m, n * m, n, m, reinterpret_cast<const float*>(din), 3 * W, 0, img_bytes, nb,
                                kappa, flags)
                    : make_call(dout, m, n * m, n, m, reinterpret_cast<const float*>(din), W, H * W, 3 * H * W, nb,
@@ -989,7 +1021,10 @@ static int run_host_impl(harris_ctx* ctx, int fmt, float* out_host, int64_t out_
         e = cudaMemcpy2DAsync(out_host + (banded ? r0 : b0 * n) * out_pitch, size_t(out_pitch) * 4, dout,
                               size_t(m) * 4, size_t(m) * 4, size_t(banded ? rows : nb * n), cudaMemcpyDeviceToHost,
                               s);
-        if (e != cudaSuccess) return cuda_fail(ctx, e, "D2H");
+        if (e != cudaSuccess) {  // stop issuing; the final sync below still drains every slot
+                rc = cuda_fail(ctx, e, "D2H");
+                break;
+            }
     }
     for (int k = 0; k < harris_ctx::kSlots; ++k) {
         cudaError_t se = cudaStreamSynchronize(ctx->streams[k]);

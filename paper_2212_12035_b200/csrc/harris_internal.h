@@ -23,7 +23,7 @@ struct TileGeom {
     int32_t n, m;
     int32_t band_rows, bands, colsegs;  // colsegs: 128-column strips per image
     int32_t batch;
-    int32_t l2_policy;  // 0 evict_first, 1 evict_normal (default), 2 evict_last
+    int32_t l2_policy;  // 0 evict_first, 1 evict_normal, 2 evict_last (default, harris_options)
     int32_t vec_store;  // 2: output rows 16-byte aligned (float4 stores); 1: 8-byte aligned (2 x float2); 0: scalar
     int32_t sync_waves; // 1: CTA barrier at every tile boundary (keeps neighbour strips in step)
     int64_t tiles;

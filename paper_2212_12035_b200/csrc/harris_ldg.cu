@@ -103,6 +103,7 @@ struct LdgOp : BaseOp {
         int64_t in_pitch, in_plane_stride, in_image_stride;  // elements
         int32_t W, H;                                        // input columns / rows per image
         const void* limit;  // one past the view's last element (used by the bulk-copy ops)
+        int32_t l2_policy;  // unused here (F32BulkOp's Params shares this initializer)
     };
 
     __device__ __forceinline__ explicit LdgOp(const Params& p) : BaseOp(p.base) {}
@@ -131,14 +132,14 @@ struct LdgOp : BaseOp {
     }
 };
 
-// EVICT_LAST: L2 evict_last hint like the TMA input loads (halo sectors are re-read by the
-// neighbouring strip): +2 % on memory-bound f32 planes, -1 % on the issue-bound u8 / stencil
-// ops (the extra createpolicy), so only F32BulkOp asks for it
-template <bool EVICT_LAST = false>
-__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
-    if constexpr (EVICT_LAST) {
-        uint64_t policy;
-        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(policy));
+// HINT: an L2 cache-policy hint like the TMA input loads (`which`: the ctx's l2_policy, 2 =
+// evict_last, whose halo sectors are re-read by the neighbouring strip): +2 % on memory-bound
+// f32 planes, -1 % on the issue-bound u8 / stencil ops (the extra createpolicy), so only
+// F32BulkOp asks for it
+template <bool HINT = false>
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar, int which = 2) {
+    if constexpr (HINT) {
+        const uint64_t policy = l2_policy(which);
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
             "%4;" ::"r"(smem_u32(smem)),
@@ -182,10 +183,11 @@ __device__ __noinline__ uint32_t bulk_tail_fix(unsigned char* dst, const unsigne
 // rounding can reach past it): the stage that holds an image's last row (warp-uniform test)
 // sends that row's lane through bulk_tail_fix.  A separate instantiation because even the
 // untaken test measured 2-6 % slower on every other stage.
-template <bool STRICT, bool EVICT_LAST = false>
+template <bool STRICT, bool HINT = false>
 __device__ __forceinline__ void bulk_stage_fill(unsigned char* dst, const void* src, uint32_t need, uint32_t cap,
                                                 const void* limit, uint64_t* bar, bool active,
-                                                bool stage_has_last_row, bool last_row, int lane) {
+                                                bool stage_has_last_row, bool last_row, int lane,
+                                                int l2_which = 2) {
     uint32_t nb = 0;
     const unsigned char* al = nullptr;
     if (active) {
@@ -201,7 +203,7 @@ __device__ __forceinline__ void bulk_stage_fill(unsigned char* dst, const void* 
     if constexpr (STRICT) __syncwarp();  // the tail's shared stores before lane 0's release
     if (lane == 0) mbar_arrive_expect_tx(bar, total);
     __syncwarp();
-    if (nb) bulk_g2s<EVICT_LAST>(dst, al, nb, bar);
+    if (nb) bulk_g2s<HINT>(dst, al, nb, bar, l2_which);
 }
 
 // ---- planar f32 through the bulk-copy engine (K1b): every (channel, row) of a stage is
@@ -228,6 +230,7 @@ struct F32BulkOp : std::conditional_t<G == 2, HarrisF32x2Op<EXACT, CH, 124>, Har
         int64_t in_pitch, in_plane_stride, in_image_stride;  // elements
         int32_t W, H;                                        // input columns / rows per image
         const void* limit;                                   // one past the view's last element
+        int32_t l2_policy;                                   // TileGeom::l2_policy of the ctx
     };
     uint32_t base_r, pitch_r, plane_r, image_r;  // float-index residues mod 4
     uint32_t sk[G][3];                           // current row's skew per strip and channel
@@ -260,7 +263,7 @@ struct F32BulkOp : std::conditional_t<G == 2, HarrisF32x2Op<EXACT, CH, 124>, Har
         bulk_stage_fill<STRICT, true>(
             static_cast<unsigned char*>(smem) + k * kBoxStride + (ch * CH + r) * (kRowFloats * 4), src,
             uint32_t(p.W - c0) * 4u, kRowFloats * 4, p.limit, bar, lane < G * 3 * CH && y < p.H,
-            row0 + CH > p.H - 1 && row0 <= p.H - 1, y == p.H - 1, lane);
+            row0 + CH > p.H - 1 && row0 <= p.H - 1, y == p.H - 1, lane, p.l2_policy);
     }
 
     // 4 floats at q + s (q 16-byte aligned, s warp-uniform in 0..3)
@@ -646,7 +649,7 @@ static void launch_ldg_one(const Geom& geom, const TileGeom& tg, int64_t grid, c
         constexpr bool S = decltype(strict)::value;
         using Op = typename LdgCfg<CFG>::template Op<EXACT, S>;
         const typename Op::Params p{{geom.kappa}, geom.rgb, geom.in_pitch, geom.in_chan_stride, img_stride,
-                                    int32_t(geom.m + 4), int32_t(geom.n + 4), limit};
+                                    int32_t(geom.m + 4), int32_t(geom.n + 4), limit, tg.l2_policy};
         ldg_kernel<CFG, EXACT, S>()<<<unsigned(grid), unsigned(LdgCfg<CFG>::NW * 32), ldg_smem<CFG>(), stream>>>(
             unused, tg, p);
     };

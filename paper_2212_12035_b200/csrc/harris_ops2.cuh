@@ -102,8 +102,8 @@ struct HarrisCore2 {
 
     __device__ __forceinline__ explicit HarrisCore2(float k) : kappa(k) {
 #pragma unroll
-#pragma unroll
         for (int q = 0; q < 12; ++q) PV[q] = f2(0.f);
+#pragma unroll
         for (int a = 0; a < 3; ++a) {
 #pragma unroll
             for (int j = 0; j < 6; ++j) D[a][j] = Hs[a][j] = f2(0.f);

@@ -26,12 +26,22 @@ KAPPA = 0.04
 
 
 class HarrisContext:
-    """One ``harris_ctx`` bound to a CUDA device (``harris_init`` / ``harris_destroy``)."""
+    """One ``harris_ctx`` bound to a CUDA device (``harris_init_ex`` / ``harris_destroy``).
 
-    def __init__(self, device: int):
+    ``l2_policy`` (``_lib.L2_EVICT_*``) and ``band_rows`` map to ``harris_options``; None keeps
+    the library default (evict_last input loads, planner-chosen tiles)."""
+
+    def __init__(self, device: int, l2_policy: Optional[int] = None, band_rows: Optional[int] = None):
         self.device = int(device)
         h = ctypes.c_void_p()
-        check(lib().harris_init(ctypes.byref(h), self.device), f"harris_init(cuda:{self.device})")
+        opts = _lib.Options()
+        lib().harris_options_default(ctypes.byref(opts))
+        if l2_policy is not None:
+            opts.l2_policy = int(l2_policy)
+        if band_rows is not None:
+            opts.band_rows = int(band_rows)
+        check(lib().harris_init_ex(ctypes.byref(h), self.device, ctypes.byref(opts)),
+              f"harris_init_ex(cuda:{self.device})")
         self._h = h
 
     @property
@@ -230,10 +240,18 @@ def harris_u8(rgb8, kappa: float = KAPPA, *, out: Optional[torch.Tensor] = None,
     batched = len(shape) == 4
     if isinstance(rgb8, np.ndarray) or not rgb8.is_cuda:
         arr = np.ascontiguousarray(rgb8 if isinstance(rgb8, np.ndarray) else rgb8.numpy())
-        res = np.empty((B, n, m) if batched else (n, m), dtype=np.float32)
-        ctx = context(torch.cuda.current_device())
+        oshape = (B, n, m) if batched else (n, m)
+        if out is not None:  # a host array / CPU tensor of the output shape (pinned for full speed)
+            res = out if isinstance(out, np.ndarray) else out.numpy()
+            if res.dtype != np.float32 or res.shape != oshape or not res.flags["C_CONTIGUOUS"]:
+                raise ValueError("out must be a C-contiguous float32 host array of the output shape")
+        else:
+            res = np.empty(oshape, dtype=np.float32)
+        ctx = ctx or context(torch.cuda.current_device())
         rc = lib().harris_run_host_u8(ctx.handle, res.ctypes.data, m, n, m, arr.ctypes.data, B, kappa, flags)
         check(rc, "harris_run_host_u8", ctx.handle)
+        if out is not None:
+            return out
         return res if isinstance(rgb8, np.ndarray) else torch.from_numpy(res)
     if rgb8.stride(-1) != 1 or rgb8.stride(-2) != 3:
         rgb8 = rgb8.contiguous()
@@ -276,8 +294,9 @@ def stencil3x3_sep(img: torch.Tensor, wv=BINOMIAL, wh=BINOMIAL, *, out: Optional
     n, m = H - 2, W - 2
     if out is None:
         out = torch.empty((B, n, m) if batched else (n, m), dtype=torch.float32, device=img.device)
-    elif tuple(out.shape) != ((B, n, m) if batched else (n, m)) or out.stride(-1) != 1:
-        raise ValueError("out has the wrong shape or column stride")
+    elif tuple(out.shape) != ((B, n, m) if batched else (n, m)) or out.stride(-1) != 1 or \
+            out.dtype != torch.float32 or out.device != img.device:
+        raise ValueError("out must be float32 on the input's device, of shape (B,) H-2, W-2 with unit column stride")
     fwv = (ctypes.c_float * 3)(*[float(v) for v in wv])
     fwh = (ctypes.c_float * 3)(*[float(v) for v in wh])
     dev = img.device.index if img.device.index is not None else torch.cuda.current_device()
@@ -326,14 +345,19 @@ def harris_grouping(rgb: torch.Tensor, grouping: int, kappa: float = KAPPA, *, o
         raise ValueError(f"unknown grouping {grouping}")
     if scratch is None and need > 0:
         scratch = torch.empty(need // 4, dtype=torch.float32, device=rgb.device)
+    elif scratch is not None and (not scratch.is_contiguous() or scratch.device != rgb.device):
+        raise ValueError("scratch must be a contiguous tensor on the input's device")
     if out is None:
         out = torch.empty((n, m), dtype=torch.float32, device=rgb.device)
+    elif out.dtype != torch.float32 or out.device != rgb.device or tuple(out.shape) != (n, m) or \
+            not out.is_contiguous():
+        raise ValueError("out must be a contiguous float32 (H-4, W-4) tensor on the input's device")
     dev = rgb.device.index
     ctx = context(dev)
     st = torch.cuda.current_stream(dev).cuda_stream
     rc = L.harris_run_grouping(ctx.handle, grouping, out.data_ptr(), n, m, rgb.data_ptr(),
                                scratch.data_ptr() if scratch is not None else None,
-                               scratch.numel() * 4 if scratch is not None else 0, kappa,
+                               scratch.numel() * scratch.element_size() if scratch is not None else 0, kappa,
                                FLAG_EXACT_ORDER if exact else 0, st)
     check(rc, "harris_run_grouping", ctx.handle)
     return out

@@ -27,8 +27,13 @@ import numpy as np
 HARRIS_SCHEME = "3.(?n+4).(?m+4).f32 -> ?n.?m.f32"
 
 
+_ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
 def _sges(reference_src: Optional[str] = None):
     src = reference_src or os.environ.get("HARRIS_REFERENCE_SRC")
+    if not src and os.path.isdir(os.path.join(_ROOT, "baseline", "_ref", "sges")):
+        src = os.path.join(_ROOT, "baseline", "_ref")  # the pip-installed reference (__graft_entry__.build)
     if src and src not in sys.path:
         sys.path.insert(0, src)
     try:

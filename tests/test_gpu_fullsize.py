@@ -5,8 +5,9 @@ pixel of every config: the EXACT-order kernel must equal the C f32 restatement
 bit-for-bit over the whole 8192^2 image, the whole 32768^2 image and all 1024 images
 of the batch, each computed in ONE launch exactly as the bench runs it.  The shipped
 FAST order is checked against the f64 oracle (pinned to the reference evaluator) on
-every pixel of configs[1]/[2] and on sampled images / row bands of configs[3]/[4]
-(SURVEY.md §8(d) tolerance).  Size-independent properties at full size: the 8 row
+every pixel of every config too — every image of the 1024-image batch and every row of
+32768^2 (SURVEY.md §8(d) tolerance, per image; row bands of one image accumulate into one
+verdict through synth.ToleranceAccumulator, exactly equal to the whole-image check).  Size-independent properties at full size: the 8 row
 bands of 32768^2 (the multi-GPU decomposition, 4-row halo views) reproduce the
 single-launch output bit-for-bit.
 
@@ -72,10 +73,17 @@ def test_fullsize_batch_1024(cuda_ctx):
     del ex
     fast = hb.harris(x)
     torch.cuda.synchronize()
-    # sampled images incl. the first / last and strip pairs straddling image boundaries
-    for b in (0, 1, 2, 511, 512, 513, 1021, 1022, 1023):
-        ok, m = synth.within_tolerance(fast[b].cpu().numpy(), cref.harris_f64(x[b].cpu().numpy()))
-        assert ok, (b, m)
+    # every image of the shipped order vs the f64 oracle, per-image tolerance
+    worst = {"norm_linf": 0.0, "psnr_db": float("inf")}
+    for b0 in range(0, B, 64):
+        host = x[b0: b0 + 64].cpu().numpy()
+        got = fast[b0: b0 + 64].cpu().numpy()
+        for i in range(host.shape[0]):
+            ok, m = synth.within_tolerance(got[i], cref.harris_f64(host[i]))
+            assert ok, (b0 + i, m)
+            worst["norm_linf"] = max(worst["norm_linf"], m["norm_linf"])
+            worst["psnr_db"] = min(worst["psnr_db"], m["psnr_db"])
+    print(f"\nconfigs[4] FAST vs f64, all {B} images: worst {worst}")
 
 
 def test_fullsize_image32768_and_row_bands(cuda_ctx):
@@ -99,7 +107,11 @@ def test_fullsize_image32768_and_row_bands(cuda_ctx):
     torch.cuda.synchronize()
     assert torch.equal(torch.cat(parts, 0), fast), "row bands differ from the single launch"
     del parts
-    for r0 in (0, n // 2 - 128, n - 256):    # sampled bands vs the f64 oracle
-        host = x[:, r0: r0 + 256 + 4].cpu().numpy()
-        ok, mt = synth.within_tolerance(fast[r0: r0 + 256].cpu().numpy(), cref.harris_f64(host))
-        assert ok, (r0, mt)
+    acc = synth.ToleranceAccumulator()       # every output row vs the f64 oracle, one verdict
+    for r0 in range(0, n, step):
+        rows = min(step, n - r0)
+        host = x[:, r0: r0 + rows + 4].cpu().numpy()
+        acc.add(fast[r0: r0 + rows].cpu().numpy(), cref.harris_f64(host))
+    ok, mt = acc.result()
+    assert ok and mt["pixels"] == n * m, mt
+    print(f"\nconfigs[3] FAST vs f64, all {n} rows: {mt}")

@@ -48,6 +48,33 @@ def test_golden_f32_within_tolerance(oracle_lib, golden):
         assert ok, (case["name"], m)
 
 
+def test_rrot_within_tolerance_on_goldens(oracle_lib, golden):
+    """The thesis cbuf+rrot CPU schedule (a timed CPU baseline variant)
+    against the f64 oracle that is pinned bit-for-bit to the reference evaluator, on every
+    golden case incl. the 512^2 config-1 image."""
+    meta, arrays = golden
+    for case in meta["cases"]:
+        rgb = _input(case, arrays)
+        ok, m = synth.within_tolerance(cref.harris_f32_rrot(rgb), cref.harris_f64(rgb))
+        assert ok, (case["name"], m)
+
+
+@pytest.mark.parametrize("H,W,dist", [(5, 5, 0), (6, 11, 1), (31, 45, 2), (64, 130, 1), (203, 77, 0), (100, 517, 2)])
+def test_rrot_c_equals_numpy_restatement(oracle_lib, H, W, dist):
+    """oracle_harris_f32_rrot (line buffers, 32-row strips, register rotation) equals an
+    independent whole-plane numpy restatement of the same arithmetic bit-for-bit, and is
+    invariant to the thread count and to batching."""
+    rgb = synth.synth_numpy(3, H, W, seed=3 * H + W, dist=dist)
+    one = cref.harris_f32_rrot(rgb, nthreads=1)
+    assert np.array_equal(one, npref.harris_rrot_np(rgb))
+    assert np.array_equal(one, cref.harris_f32_rrot(rgb, nthreads=4))
+    ok, m = synth.within_tolerance(one, cref.harris_f64(rgb))
+    assert ok, m
+    batch = np.stack([rgb, rgb[::-1].copy()])
+    both = cref.harris_batched(batch, variant="rrot")
+    assert np.array_equal(both[0], one) and np.array_equal(both[1], cref.harris_f32_rrot(batch[1]))
+
+
 def test_ambient_primitive_recorded(golden):
     meta, _ = golden
     assert meta["ambient_primitive_roundtrip_equal"] is True

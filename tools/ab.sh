@@ -1,4 +1,5 @@
 #!/bin/bash
+export HARRIS_DEV=1  # developer knobs (HARRIS_*_CONFIG, HARRIS_BAND_ROWS, ...) are read only with this
 # dev A/B: alternate the in-tree library and ab/libharris_old.so within one box session
 for i in 1 2 3; do
   for v in new old; do

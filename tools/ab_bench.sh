@@ -1,4 +1,5 @@
 #!/bin/bash
+export HARRIS_DEV=1  # developer knobs (HARRIS_*_CONFIG, HARRIS_BAND_ROWS, ...) are read only with this
 # dev: the real bench line (headline only) for the in-tree library vs ab/libold.so, alternating
 for i in 1 2 3; do
   for v in new old; do

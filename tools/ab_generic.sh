@@ -1,4 +1,5 @@
 #!/bin/bash
+export HARRIS_DEV=1  # developer knobs (HARRIS_*_CONFIG, HARRIS_BAND_ROWS, ...) are read only with this
 # dev: unaligned-input (K2) timing for several library variants
 for i in 1 2; do
   for v in ${VARIANTS}; do

@@ -1,4 +1,5 @@
 #!/bin/bash
+export HARRIS_DEV=1  # developer knobs (HARRIS_*_CONFIG, HARRIS_BAND_ROWS, ...) are read only with this
 # dev: f32 default config device time for several library variants (HARRIS_LIB), alternating
 for i in 1 2; do
   for v in ${VARIANTS:-new old}; do

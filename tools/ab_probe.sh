@@ -1,4 +1,5 @@
 #!/bin/bash
+export HARRIS_DEV=1  # developer knobs (HARRIS_*_CONFIG, HARRIS_BAND_ROWS, ...) are read only with this
 # dev A/B: in-tree library vs ab/libharris_old.so, alternating, f32 and u8 default configs
 for i in 1 2; do
   for v in new old; do

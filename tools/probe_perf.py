@@ -26,7 +26,7 @@ def peak():
 
 
 def time_cfg(cfg, workloads, iters, exact=False, generic=False):
-    env = dict(os.environ, HARRIS_TMA_CONFIG=str(cfg))
+    env = dict(os.environ, HARRIS_DEV="1", HARRIS_TMA_CONFIG=str(cfg))
     code = f"""
 import sys, torch, json
 sys.path.insert(0, {ROOT!r})
@@ -61,7 +61,7 @@ print(json.dumps(res))
 
 
 def time_u8(cfg, workloads, iters):
-    env = dict(os.environ, HARRIS_U8_CONFIG=str(cfg))
+    env = dict(os.environ, HARRIS_DEV="1", HARRIS_U8_CONFIG=str(cfg))
     code = f"""
 import sys, torch, json
 sys.path.insert(0, {ROOT!r})

@@ -32,7 +32,7 @@ print(json.dumps(dict(ms=ts[len(ts)//2], min=ts[0], plan=hb.context().plan(H - 4
 
 def main():
     for cfg in [int(c) for c in (sys.argv[1] if len(sys.argv) > 1 else "0,3,6").split(",")]:
-        env = dict(os.environ, HARRIS_TMA_CONFIG=str(cfg))
+        env = dict(os.environ, HARRIS_DEV="1", HARRIS_TMA_CONFIG=str(cfg))
         r = subprocess.run([sys.executable, "-c", CODE.replace("ROOT", repr(ROOT))], env=env, capture_output=True,
                            text=True)
         print("cfg", cfg, r.stdout.strip()[-400:] or r.stderr[-400:], flush=True)

@@ -51,7 +51,7 @@ def main():
     rows = [int(c) for c in (sys.argv[2] if len(sys.argv) > 2 else "0").split(",")]
     for cfg in cfgs:
         for br in rows:
-            env = dict(os.environ, HARRIS_TMA_CONFIG=str(cfg))
+            env = dict(os.environ, HARRIS_DEV="1", HARRIS_TMA_CONFIG=str(cfg))
             if br:
                 env["HARRIS_BAND_ROWS"] = str(br)
             r = subprocess.run([sys.executable, "-c", CODE.replace("ROOT", repr(ROOT))], env=env,

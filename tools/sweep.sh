@@ -1,4 +1,5 @@
 #!/bin/bash
+export HARRIS_DEV=1  # developer knobs (HARRIS_*_CONFIG, HARRIS_BAND_ROWS, ...) are read only with this
 # dev sweep: L2 policy x TMA config x band rows on the probe workloads
 set -u
 for pol in 0 1 2; do
