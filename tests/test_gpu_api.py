@@ -64,10 +64,11 @@ def test_dev_knobs_ignored_without_harris_dev(cuda_ctx, monkeypatch):
     plain = hb.HarrisContext(0)
     monkeypatch.setenv("HARRIS_DEV", "1")
     dev = hb.HarrisContext(0)
-    assert plain.plan(1076, 1916, batch=4)["band_rows"] != 30
-    assert plain.plan(1076, 1916, batch=4)["tma_config"] == 6
-    assert dev.plan(1076, 1916, batch=4)["band_rows"] == 30
-    assert dev.plan(1076, 1916, batch=4)["tma_config"] == 1
+    default = cuda_ctx.plan(1076, 1916, batch=1024)
+    assert plain.plan(1076, 1916, batch=1024) == default
+    assert default["band_rows"] != 30 and default["tma_config"] != 1
+    assert dev.plan(1076, 1916, batch=1024)["band_rows"] == 30
+    assert dev.plan(1076, 1916, batch=1024)["tma_config"] == 1
 
 
 def test_stencil_out_validation(cuda_ctx):
