@@ -131,6 +131,52 @@ static inline float sum9_f32(const float* a, const float* b, const float* c, int
     return s;
 }
 
+/* one 32-row strip of the cbuf schedule; buf: 3W + 15Ws floats of per-thread line buffers */
+static void cbuf_strip_f32(float* buf, float* out, int64_t out_pitch, int64_t n, int64_t m, const float* rgb,
+                           int64_t in_pitch, int64_t chan_stride, float kappa, int64_t s) {
+    const int64_t W = m + 4, Ws = m + 2;
+    float* gl[3] = {buf, buf + W, buf + 2 * W};
+    float* sb = buf + 3 * W;
+    float *ix[3], *iy[3], *pxx[3], *pxy[3], *pyy[3];
+    for (int k = 0; k < 3; ++k) {
+        ix[k] = sb + (0 + k) * Ws;  iy[k] = sb + (3 + k) * Ws;
+        pxx[k] = sb + (6 + k) * Ws; pxy[k] = sb + (9 + k) * Ws;
+        pyy[k] = sb + (12 + k) * Ws;
+    }
+    const int64_t y0 = s * STRIP;
+    const int64_t y1 = (y0 + STRIP < n) ? y0 + STRIP : n;
+    /* input rows y0 .. y1+3; gray row r lives in gl[r % 3]; Sobel row
+     * q (= gray rows q..q+2) lives in slot q % 3 */
+    for (int64_t r = y0; r < y1 + 4; ++r) {
+        const float* R = rgb + 0 * chan_stride + r * in_pitch;
+        const float* G = rgb + 1 * chan_stride + r * in_pitch;
+        const float* B = rgb + 2 * chan_stride + r * in_pitch;
+        gray_line_f32(gl[r % 3], R, G, B, W);
+        if (r >= y0 + 2) {
+            int64_t q = r - 2;
+            int k = (int)(q % 3);
+            sobel_line_f32(ix[k], iy[k], gl[q % 3], gl[(q + 1) % 3],
+                           gl[(q + 2) % 3], Ws);
+            products_line_f32(pxx[k], pxy[k], pyy[k], ix[k], iy[k], Ws);
+        }
+        if (r >= y0 + 4) {
+            int64_t y = r - 4;
+            int a = (int)(y % 3), b = (int)((y + 1) % 3), c = (int)((y + 2) % 3);
+            float* o = out + y * out_pitch;
+            for (int64_t x = 0; x < m; ++x) {
+                float sxx = sum9_f32(pxx[a], pxx[b], pxx[c], x);
+                float sxy = sum9_f32(pxy[a], pxy[b], pxy[c], x);
+                float syy = sum9_f32(pyy[a], pyy[b], pyy[c], x);
+                float det = sxx * syy - sxy * sxy;
+                float tr = sxx + syy;
+                o[x] = det - kappa * tr * tr;
+            }
+        }
+    }
+}
+
+#define CBUF_BUF_FLOATS(W, Ws) ((size_t)(3 * (W) + 15 * (Ws)))
+
 int oracle_harris_f32(float* out, int64_t out_pitch, int64_t n, int64_t m,
                       const float* rgb, int64_t in_pitch, int64_t chan_stride,
                       float kappa, int nthreads) {
@@ -146,53 +192,14 @@ int oracle_harris_f32(float* out, int64_t out_pitch, int64_t n, int64_t m,
 #pragma omp parallel
     {
         /* per-thread circular line buffers: 3 gray, 3 Ix, 3 Iy, 3x3 products */
-        float* buf = (float*)malloc(sizeof(float) * (size_t)(3 * W + 15 * Ws));
+        float* buf = (float*)malloc(sizeof(float) * CBUF_BUF_FLOATS(W, Ws));
         if (!buf) {
 #pragma omp atomic write
             err = -2;
         }
 #pragma omp for schedule(dynamic, 1)
-        for (int64_t s = 0; s < nstrips; ++s) {
-            if (!buf) continue;
-            float* gl[3] = {buf, buf + W, buf + 2 * W};
-            float* sb = buf + 3 * W;
-            float *ix[3], *iy[3], *pxx[3], *pxy[3], *pyy[3];
-            for (int k = 0; k < 3; ++k) {
-                ix[k] = sb + (0 + k) * Ws;  iy[k] = sb + (3 + k) * Ws;
-                pxx[k] = sb + (6 + k) * Ws; pxy[k] = sb + (9 + k) * Ws;
-                pyy[k] = sb + (12 + k) * Ws;
-            }
-            const int64_t y0 = s * STRIP;
-            const int64_t y1 = (y0 + STRIP < n) ? y0 + STRIP : n;
-            /* input rows y0 .. y1+3; gray row r lives in gl[r % 3]; Sobel row
-             * q (= gray rows q..q+2) lives in slot q % 3 */
-            for (int64_t r = y0; r < y1 + 4; ++r) {
-                const float* R = rgb + 0 * chan_stride + r * in_pitch;
-                const float* G = rgb + 1 * chan_stride + r * in_pitch;
-                const float* B = rgb + 2 * chan_stride + r * in_pitch;
-                gray_line_f32(gl[r % 3], R, G, B, W);
-                if (r >= y0 + 2) {
-                    int64_t q = r - 2;
-                    int k = (int)(q % 3);
-                    sobel_line_f32(ix[k], iy[k], gl[q % 3], gl[(q + 1) % 3],
-                                   gl[(q + 2) % 3], Ws);
-                    products_line_f32(pxx[k], pxy[k], pyy[k], ix[k], iy[k], Ws);
-                }
-                if (r >= y0 + 4) {
-                    int64_t y = r - 4;
-                    int a = (int)(y % 3), b = (int)((y + 1) % 3), c = (int)((y + 2) % 3);
-                    float* o = out + y * out_pitch;
-                    for (int64_t x = 0; x < m; ++x) {
-                        float sxx = sum9_f32(pxx[a], pxx[b], pxx[c], x);
-                        float sxy = sum9_f32(pxy[a], pxy[b], pxy[c], x);
-                        float syy = sum9_f32(pyy[a], pyy[b], pyy[c], x);
-                        float det = sxx * syy - sxy * sxy;
-                        float tr = sxx + syy;
-                        o[x] = det - kappa * tr * tr;
-                    }
-                }
-            }
-        }
+        for (int64_t s = 0; s < nstrips; ++s)
+            if (buf) cbuf_strip_f32(buf, out, out_pitch, n, m, rgb, in_pitch, chan_stride, kappa, s);
         free(buf);
     }
     return err;
@@ -325,6 +332,86 @@ int oracle_harris_f64(double* out, int64_t out_pitch, int64_t n, int64_t m,
  * every accumulation from 0 in listing order (-ffp-contract=off).  A different
  * op order from Appendix B (results agree within the SURVEY.md §8(d) tolerance,
  * not bit-for-bit); used as the strongest CPU baseline. */
+/* vertical 3-row sums of the products; a separate function with
+ * restrict line pointers so gcc vectorises it like the cbuf line functions */
+static void rrot_vbox_line_f32(float* restrict vxx, float* restrict vxy, float* restrict vyy,
+                               const float* restrict a0, const float* restrict a1, const float* restrict a2,
+                               const float* restrict b0, const float* restrict b1, const float* restrict b2,
+                               int64_t Ws) {
+    for (int64_t x = 0; x < Ws; ++x) {
+        float t = 0.0f;
+        t = t + a0[x] * a0[x]; t = t + a1[x] * a1[x]; t = t + a2[x] * a2[x];
+        vxx[x] = t;
+        float u = 0.0f;
+        u = u + a0[x] * b0[x]; u = u + a1[x] * b1[x]; u = u + a2[x] * b2[x];
+        vxy[x] = u;
+        float v = 0.0f;
+        v = v + b0[x] * b0[x]; v = v + b1[x] * b1[x]; v = v + b2[x] * b2[x];
+        vyy[x] = v;
+    }
+}
+
+/* one 32-row strip of the cbuf+rrot schedule; buf: 5W + 9Ws floats */
+static void rrot_strip_f32(float* buf, float* out, int64_t out_pitch, int64_t n, int64_t m, const float* rgb,
+                           int64_t in_pitch, int64_t chan_stride, float kappa, int64_t s) {
+    const int64_t W = m + 4, Ws = m + 2;
+    float* gl[3] = {buf, buf + W, buf + 2 * W};
+    float* vs = buf + 3 * W;          /* vertical [1,2,1] sum, width W */
+    float* vd = buf + 4 * W;          /* vertical [-1,0,1] diff, width W */
+    float* sb = buf + 5 * W;
+    float *ix[3], *iy[3];
+    for (int k = 0; k < 3; ++k) { ix[k] = sb + k * Ws; iy[k] = sb + (3 + k) * Ws; }
+    float* vxx = sb + 6 * Ws;
+    float* vxy = sb + 7 * Ws;
+    float* vyy = sb + 8 * Ws;
+    const int64_t y0 = s * STRIP;
+    const int64_t y1 = (y0 + STRIP < n) ? y0 + STRIP : n;
+    for (int64_t r = y0; r < y1 + 4; ++r) {
+        const float* R = rgb + 0 * chan_stride + r * in_pitch;
+        const float* G = rgb + 1 * chan_stride + r * in_pitch;
+        const float* B = rgb + 2 * chan_stride + r * in_pitch;
+        gray_line_f32(gl[r % 3], R, G, B, W);
+        if (r >= y0 + 2) {
+            const int64_t q = r - 2;
+            const float* g0 = gl[q % 3];
+            const float* g1 = gl[(q + 1) % 3];
+            const float* g2 = gl[(q + 2) % 3];
+            for (int64_t x = 0; x < W; ++x) {
+                float t = 0.0f;
+                t += 1.0f * g0[x]; t += 2.0f * g1[x]; t += 1.0f * g2[x];
+                vs[x] = t;
+                float u = 0.0f;
+                u += -1.0f * g0[x]; u += 0.0f * g1[x]; u += 1.0f * g2[x];
+                vd[x] = u;
+            }
+            float* px = ix[q % 3];
+            float* py = iy[q % 3];
+            for (int64_t x = 0; x < Ws; ++x) {
+                float t = 0.0f;
+                t = t + (-SA) * vs[x]; t = t + 0.0f * vs[x + 1]; t = t + SA * vs[x + 2];
+                px[x] = t;
+                float u = 0.0f;
+                u = u + SA * vd[x]; u = u + SB * vd[x + 1]; u = u + SA * vd[x + 2];
+                py[x] = u;
+            }
+        }
+        if (r >= y0 + 4) {
+            const int64_t y = r - 4;
+            rrot_vbox_line_f32(vxx, vxy, vyy, ix[y % 3], ix[(y + 1) % 3], ix[(y + 2) % 3],
+                               iy[y % 3], iy[(y + 1) % 3], iy[(y + 2) % 3], Ws);
+            float* o = out + y * out_pitch;
+            for (int64_t x = 0; x < m; ++x) {
+                float sxy = 0.0f; sxy = sxy + vxy[x]; sxy = sxy + vxy[x + 1]; sxy = sxy + vxy[x + 2];
+                float syy = 0.0f; syy = syy + vyy[x]; syy = syy + vyy[x + 1]; syy = syy + vyy[x + 2];
+                float sxx = 0.0f; sxx = sxx + vxx[x]; sxx = sxx + vxx[x + 1]; sxx = sxx + vxx[x + 2];
+                o[x] = sxx * syy - sxy * sxy - kappa * (sxx + syy) * (sxx + syy);
+            }
+        }
+    }
+}
+
+#define RROT_BUF_FLOATS(W, Ws) ((size_t)(5 * (W) + 9 * (Ws)))
+
 int oracle_harris_f32_rrot(float* out, int64_t out_pitch, int64_t n, int64_t m,
                            const float* rgb, int64_t in_pitch, int64_t chan_stride,
                            float kappa, int nthreads) {
@@ -340,78 +427,46 @@ int oracle_harris_f32_rrot(float* out, int64_t out_pitch, int64_t n, int64_t m,
 #pragma omp parallel
     {
         /* 3 gray lines, 2 vertical-sum lines, 3 Ix + 3 Iy lines, 3 vertical box lines */
-        float* buf = (float*)malloc(sizeof(float) * (size_t)(5 * W + 6 * Ws + 3 * Ws));
+        float* buf = (float*)malloc(sizeof(float) * RROT_BUF_FLOATS(W, Ws));
         if (!buf) {
 #pragma omp atomic write
             err = -2;
         }
 #pragma omp for schedule(dynamic, 1)
-        for (int64_t s = 0; s < nstrips; ++s) {
-            if (!buf) continue;
-            float* gl[3] = {buf, buf + W, buf + 2 * W};
-            float* vs = buf + 3 * W;          /* vertical [1,2,1] sum, width W */
-            float* vd = buf + 4 * W;          /* vertical [-1,0,1] diff, width W */
-            float* sb = buf + 5 * W;
-            float *ix[3], *iy[3];
-            for (int k = 0; k < 3; ++k) { ix[k] = sb + k * Ws; iy[k] = sb + (3 + k) * Ws; }
-            float* vxx = sb + 6 * Ws;
-            float* vxy = sb + 7 * Ws;
-            float* vyy = sb + 8 * Ws;
-            const int64_t y0 = s * STRIP;
-            const int64_t y1 = (y0 + STRIP < n) ? y0 + STRIP : n;
-            for (int64_t r = y0; r < y1 + 4; ++r) {
-                const float* R = rgb + 0 * chan_stride + r * in_pitch;
-                const float* G = rgb + 1 * chan_stride + r * in_pitch;
-                const float* B = rgb + 2 * chan_stride + r * in_pitch;
-                gray_line_f32(gl[r % 3], R, G, B, W);
-                if (r >= y0 + 2) {
-                    const int64_t q = r - 2;
-                    const float* g0 = gl[q % 3];
-                    const float* g1 = gl[(q + 1) % 3];
-                    const float* g2 = gl[(q + 2) % 3];
-                    for (int64_t x = 0; x < W; ++x) {
-                        float t = 0.0f;
-                        t += 1.0f * g0[x]; t += 2.0f * g1[x]; t += 1.0f * g2[x];
-                        vs[x] = t;
-                        float u = 0.0f;
-                        u += -1.0f * g0[x]; u += 0.0f * g1[x]; u += 1.0f * g2[x];
-                        vd[x] = u;
-                    }
-                    float* px = ix[q % 3];
-                    float* py = iy[q % 3];
-                    for (int64_t x = 0; x < Ws; ++x) {
-                        float t = 0.0f;
-                        t = t + (-SA) * vs[x]; t = t + 0.0f * vs[x + 1]; t = t + SA * vs[x + 2];
-                        px[x] = t;
-                        float u = 0.0f;
-                        u = u + SA * vd[x]; u = u + SB * vd[x + 1]; u = u + SA * vd[x + 2];
-                        py[x] = u;
-                    }
-                }
-                if (r >= y0 + 4) {
-                    const int64_t y = r - 4;
-                    const float* a0 = ix[y % 3]; const float* a1 = ix[(y + 1) % 3]; const float* a2 = ix[(y + 2) % 3];
-                    const float* b0 = iy[y % 3]; const float* b1 = iy[(y + 1) % 3]; const float* b2 = iy[(y + 2) % 3];
-                    for (int64_t x = 0; x < Ws; ++x) {
-                        float t = 0.0f;
-                        t = t + a0[x] * a0[x]; t = t + a1[x] * a1[x]; t = t + a2[x] * a2[x];
-                        vxx[x] = t;
-                        float u = 0.0f;
-                        u = u + a0[x] * b0[x]; u = u + a1[x] * b1[x]; u = u + a2[x] * b2[x];
-                        vxy[x] = u;
-                        float v = 0.0f;
-                        v = v + b0[x] * b0[x]; v = v + b1[x] * b1[x]; v = v + b2[x] * b2[x];
-                        vyy[x] = v;
-                    }
-                    float* o = out + y * out_pitch;
-                    for (int64_t x = 0; x < m; ++x) {
-                        float sxy = 0.0f; sxy = sxy + vxy[x]; sxy = sxy + vxy[x + 1]; sxy = sxy + vxy[x + 2];
-                        float syy = 0.0f; syy = syy + vyy[x]; syy = syy + vyy[x + 1]; syy = syy + vyy[x + 2];
-                        float sxx = 0.0f; sxx = sxx + vxx[x]; sxx = sxx + vxx[x + 1]; sxx = sxx + vxx[x + 2];
-                        o[x] = sxx * syy - sxy * sxy - kappa * (sxx + syy) * (sxx + syy);
-                    }
-                }
-            }
+        for (int64_t s = 0; s < nstrips; ++s)
+            if (buf) rrot_strip_f32(buf, out, out_pitch, n, m, rgb, in_pitch, chan_stride, kappa, s);
+        free(buf);
+    }
+    return err;
+}
+
+/* batched forms: contiguous 3 x H x W images, contiguous n x m outputs.  One OpenMP
+ * loop over every (image, strip) pair, so a batch of small images keeps every core busy
+ * (per-image loops leave cores idle when strips per image is not a multiple of threads). */
+typedef void (*strip_fn)(float*, float*, int64_t, int64_t, int64_t, const float*, int64_t, int64_t, float, int64_t);
+
+static int batched_strips(strip_fn fn, size_t buf_floats, float* out, int64_t n, int64_t m, const float* rgb,
+                          int64_t batch, float kappa, int nthreads) {
+    if (n < 1 || m < 1 || batch < 1 || !out || !rgb) return -1;
+    const int64_t H = n + 4, W = m + 4;
+    const int64_t nstrips = (n + STRIP - 1) / STRIP;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+    int err = 0;
+#pragma omp parallel
+    {
+        float* buf = (float*)malloc(sizeof(float) * buf_floats);
+        if (!buf) {
+#pragma omp atomic write
+            err = -2;
+        }
+#pragma omp for schedule(dynamic, 1)
+        for (int64_t t = 0; t < batch * nstrips; ++t) {
+            const int64_t b = t / nstrips, s = t - b * nstrips;
+            if (buf) fn(buf, out + b * n * m, m, n, m, rgb + b * 3 * H * W, W, H * W, kappa, s);
         }
         free(buf);
     }
@@ -420,26 +475,12 @@ int oracle_harris_f32_rrot(float* out, int64_t out_pitch, int64_t n, int64_t m,
 
 int oracle_harris_f32_rrot_batched(float* out, int64_t n, int64_t m, const float* rgb,
                                    int64_t batch, float kappa, int nthreads) {
-    const int64_t H = n + 4, W = m + 4;
-    for (int64_t b = 0; b < batch; ++b) {
-        int rc = oracle_harris_f32_rrot(out + b * n * m, m, n, m, rgb + b * 3 * H * W, W, H * W,
-                                        kappa, nthreads);
-        if (rc) return rc;
-    }
-    return 0;
+    return batched_strips(rrot_strip_f32, RROT_BUF_FLOATS(m + 4, m + 2), out, n, m, rgb, batch, kappa, nthreads);
 }
 
-/* batched f32 convenience for the CPU baseline: images are contiguous
- * 3 x H x W planes, outputs contiguous n x m. */
 int oracle_harris_f32_batched(float* out, int64_t n, int64_t m, const float* rgb,
                               int64_t batch, float kappa, int nthreads) {
-    const int64_t H = n + 4, W = m + 4;
-    for (int64_t b = 0; b < batch; ++b) {
-        int rc = oracle_harris_f32(out + b * n * m, m, n, m, rgb + b * 3 * H * W, W, H * W,
-                                   kappa, nthreads);
-        if (rc) return rc;
-    }
-    return 0;
+    return batched_strips(cbuf_strip_f32, CBUF_BUF_FLOATS(m + 4, m + 2), out, n, m, rgb, batch, kappa, nthreads);
 }
 
 int oracle_max_threads(void) {

@@ -12,6 +12,7 @@ import socket
 import subprocess
 import sys
 
+import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -42,6 +43,25 @@ def test_reference_arm_line():
     assert cb["kind"] in ("port", "reference") and cb["cores"] >= 1 and cb["sample"] and cb["value"] == d["value"]
     assert d["e2e"] == {"value": d["value"], "unit": "MP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     assert "configs[4]" in d["config"]["workload"]
+    # both thesis CPU schedules are timed; the arm runs the faster one
+    v = cb["variants"]
+    assert v["cbuf"]["value"] > 0 and v["rrot"]["value"] > 0 and cb["variant"] in ("cbuf", "rrot")
+    assert v["rrot_over_cbuf"] == pytest.approx(v["rrot"]["value"] / v["cbuf"]["value"])
+    assert d["config"]["same_as_gpu_arm"] is False  # --ref-images 1: a prefix of the batch
+
+
+def test_reference_workload_is_the_whole_batch_by_default(monkeypatch):
+    """Without --ref-images the reference arm's per-step input is every image of the
+    workload (same config as the GPU arm), regenerated bit-exactly on the host."""
+    import bench
+    from oracle import synth
+    wl = dict(bench.WORKLOADS["batch"], B=5, H=40, W=70)
+    x, px, desc, same = bench.reference_workload(wl, None)
+    assert same and x.shape == (5, 3, 40, 70) and px == 5 * 36 * 66 and "all 5" in desc
+    assert np.array_equal(x.reshape(15, 40, 70), synth.synth_numpy(15, 40, 70, seed=bench.SEED))
+    monkeypatch.setattr(bench, "host_mem_available", lambda: 2 * 3 * (12 * 40 * 70 + 4 * 36 * 66))
+    x, _, desc, same = bench.reference_workload(wl, None)
+    assert not same and x.shape[0] == 3 and "first 3 of 5" in desc
 
 
 def test_reference_arm_under_torchrun_prints_once():
@@ -72,7 +92,7 @@ def test_workload_accounting():
     assert sh.total_px == 1024 * 1076 * 1916 == sh.local_px
     assert sh.algorithmic_bytes() == 1024 * (12 * 1080 * 1920 + 4 * 1076 * 1916)
     # weak scaling: every rank owns a full 1024-image batch, global images disjoint
-    shards = [bench.Shard(wl, world=8, rank=r) for r in range(8)]
+    shards = [bench.Shard(wl, world=8, rank=r, scaling="weak") for r in range(8)]
     assert [s.b0 for s in shards] == [r * 1024 for r in range(8)]
     assert all(s.nb == 1024 for s in shards) and shards[0].total_px == 8 * 1024 * 1076 * 1916
     # strong scaling: one batch split, row bands: one image split with a 4-row halo each

@@ -2,8 +2,9 @@
 
 Two torchrun ranks share cuda:0 (HARRIS_BENCH_SHARE_GPU=1, gloo for the host-side
 collectives — NCCL refuses two ranks on one device): the row-band workload with the fused
-peer gather and the image-sharded batch workload (weak scaling) must each print exactly
-one JSON line with n_gpus = 2.  The numbers themselves are meaningless here (two
+peer gather and the image-sharded batch workload (strong scaling by default: the literal
+configs[4] batch split over the ranks; weak as a flag) must each print exactly one JSON
+line with n_gpus = N.  The numbers themselves are meaningless here (two
 processes time-slice one GPU); this checks the plumbing the 8-GPU scaling run uses.
 """
 import json
@@ -42,10 +43,26 @@ def test_two_rank_row_bands_with_fused_gather():
 
 
 def test_two_rank_weak_scaling_batch():
-    d = _torchrun(["--steps", "3", "--warmup", "3", "--e2e-images", "8", "--e2e-steps", "1"])
+    d = _torchrun(["--scaling", "weak", "--steps", "3", "--warmup", "3", "--e2e-images", "8", "--e2e-steps", "1"])
     assert d["n_gpus"] == 2 and d["scaling"] == "weak"
     assert d["config"]["images"] == 2048 and d["config"]["images_per_gpu"] == 1024
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
+
+
+@pytest.mark.parametrize("nproc", [2, 4, 8])
+def test_default_batch_line_is_the_literal_config(nproc):
+    """The default N>1 batch line (what the driver's scaling run prints) is BASELINE
+    configs[4] itself: ONE 1024-image batch of 1920x1080 split over the ranks (strong
+    scaling), value = all 1024 images' output pixels / max-over-ranks time."""
+    d = _torchrun(["--steps", "2", "--warmup", "3", "--e2e-images", "4", "--e2e-steps", "1"], nproc=nproc,
+                  timeout=900)
+    c = d["config"]
+    assert d["n_gpus"] == nproc and d["scaling"] == "strong"
+    assert "configs[4]" in c["workload"] and c["images"] == 1024 and c["images_per_gpu"] == 1024 // nproc
+    assert c["output"] == [1024, 1076, 1916] and c["height"] == 1080 and c["width"] == 1920
+    px = 1024 * 1076 * 1916
+    assert d["value"] == pytest.approx(px * d["steps"] / (d["ms_per_step"] * d["steps"] * 1e-3) / 1e6, rel=1e-9)
+    assert d["roofline"]["algorithmic_bytes_per_launch"] == (1024 // nproc) * (12 * 1080 * 1920 + 4 * 1076 * 1916)
 
 
 def test_four_rank_row_bands_fused_gather():
