@@ -33,6 +33,8 @@ struct harris_ctx {
     int tma_cfg = kDefaultTmaConfig;
     bool tma_cfg_forced = false;  // HARRIS_TMA_CONFIG given: no per-call choice
     int u8_cfg = kDefaultU8Config;
+    // register-store config 0: the TMA-store epilogue (config 3) fits only 6 input stages next
+    // to its output staging and measured 4 % slower (profiles/sep_store_r02.txt)
     int sep_cfg = 0;
     int occ_sep[kNumSepConfigs] = {0};
     int occ_u8[kNumU8Configs] = {0};
@@ -188,7 +190,7 @@ bool tma_eligible(const Call& c) {
 // of one band row of all images are paired consecutively (strip_pipeline.cuh).
 void plan_tiles(int64_t n, int64_t m, int64_t batch, int64_t gw, int rows_per_stage, int64_t force_rows,
                 TileGeom& tg, int halo = 4, int groups = 1, int strip_cols = kWarpCols, bool cap_rows = true,
-                int row_align = 1) {
+                int row_align = 1, int64_t max_rows = 288) {
     const int64_t colsegs = (m + strip_cols - 1) / strip_cols;
     const int64_t units_per_band = groups == 2 ? (batch * colsegs + 1) / 2 : batch * colsegs;
     tg.n = int32_t(n);
@@ -209,7 +211,7 @@ void plan_tiles(int64_t n, int64_t m, int64_t batch, int64_t gw, int rows_per_st
     // 269-row 5.05-5.07 ms; binomial 1076-row 3.48 ms, 269-row 2.97 ms; 32768^2: 886-row
     // 2.526 ms, 254-row 2.517 ms.  The issue-bound u8 op prefers long tiles (1076 rows
     // 2.93-2.95 ms vs 3.03 ms capped) and plans without the cap (profiles/band_rows_r01.txt).
-    const int64_t kMaxBandRows = cap_rows ? 288 : INT64_MAX;
+    const int64_t kMaxBandRows = cap_rows ? max_rows : INT64_MAX;
     const int64_t max_bands = std::max<int64_t>(1, std::min<int64_t>(n, 1 + n / 8));
     int64_t best_cost = INT64_MAX, best_rows = n, best_bands = 1;
     for (int64_t nb = 1; nb <= max_bands; ++nb) {
@@ -800,7 +802,12 @@ int harris_stencil3x3_sep(harris_ctx* ctx, float* out, int64_t out_pitch, int64_
         CUtensorMap tmap;
         cuuint64_t dims[3] = {cuuint64_t(m + 2), cuuint64_t(n + 2), cuuint64_t(batch)};
         cuuint64_t strides[2] = {cuuint64_t(in_pitch) * 4, cuuint64_t((img_stride + 3) / 4 * 4) * 4};
-        const TmaConfig& scfg = kSepConfigs[ctx->sep_cfg];
+        const int out_vec = store_mode(out, out_pitch, batch, out_image_stride);
+        // TMA-store epilogue: needs 16-byte aligned output rows / images (tensor-map strides) and
+        // m % 4 == 0 — a TMA store writes the out-of-bounds tail of a box's last 16-byte chunk
+        // (measured: m = 6 wrote columns 6 and 7), which would touch the caller's padding
+        const int cfg = sep_config_tma_store(ctx->sep_cfg) && (out_vec != 2 || (m & 3)) ? 0 : ctx->sep_cfg;
+        const TmaConfig& scfg = kSepConfigs[cfg];
         cuuint32_t box[3] = {cuuint32_t(kBoxCols), cuuint32_t(scfg.rows), 1};
         cuuint32_t estr[3] = {1, 1, 1};
         CUresult r = ctx->encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(in), dims, strides,
@@ -811,18 +818,38 @@ int harris_stencil3x3_sep(harris_ctx* ctx, float* out, int64_t out_pitch, int64_
             return HARRIS_ERR_TMA;
         }
         TileGeom tg;
-        const int64_t resident = int64_t(ctx->num_sms) * std::max(1, ctx->occ_sep[ctx->sep_cfg]);
-        plan_tiles(n, m, batch, resident * scfg.warps, scfg.rows, ctx->force_band_rows, tg, 2);
+        const int64_t resident = int64_t(ctx->num_sms) * std::max(1, ctx->occ_sep[cfg]);
+        // TMA stores: row pairs never straddle tiles.  Tiles of at most 136 rows: the 8 warps of a
+        // CTA re-align at every tile boundary, which this 1:1 read/write op needs more than the
+        // Harris ops (1024 x 1080x1920: 269-row tiles 710 k MP/s, 136-row 796 k; 16 x 8192^2
+        // 680 -> 695 k; 256 x 1536x2560 771 -> 788 k; profiles/band_rows_r02.txt)
+        plan_tiles(n, m, batch, resident * scfg.warps, scfg.rows, ctx->force_band_rows, tg, 2, 1, kWarpCols, true,
+                   sep_config_tma_store(cfg) ? 2 : 1, kSepMaxBandRows);
         const int64_t grid = std::min<int64_t>((tg.tiles + scfg.warps - 1) / scfg.warps, resident);
         tg.out = out;
         tg.out_pitch = out_pitch;
         tg.out_image_stride = batch > 1 ? out_image_stride : n * out_pitch;
         tg.kappa = 0.f;
         tg.l2_policy = ctx->l2_policy;
-        tg.vec_store = store_mode(out, out_pitch, batch, out_image_stride);
+        tg.vec_store = out_vec;
         tg.sync_waves = ctx->sync_waves;
         if (tg.tiles > INT32_MAX) return HARRIS_ERR_SIZE;  // beyond the engine's 32-bit tile index
-        e = launch_tma_sep(ctx->sep_cfg, exact, tmap, tg, grid, wv, wh, stream);
+        CUtensorMap out_tmap;
+        const bool ts = sep_config_tma_store(cfg);
+        if (ts) {
+            cuuint64_t odims[3] = {cuuint64_t(m), cuuint64_t(n), cuuint64_t(batch)};
+            cuuint64_t ostr[2] = {cuuint64_t(out_pitch) * 4, cuuint64_t(batch > 1 ? out_image_stride : n * out_pitch) * 4};
+            cuuint32_t obox[3] = {cuuint32_t(kWarpCols), 2, 1};
+            r = ctx->encode(&out_tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, out, odims, ostr, obox, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) {
+                std::snprintf(ctx->last_err, sizeof(ctx->last_err), "cuTensorMapEncodeTiled (stencil out) failed (%d)",
+                              int(r));
+                return HARRIS_ERR_TMA;
+            }
+        }
+        e = launch_tma_sep(cfg, exact, tmap, ts ? &out_tmap : nullptr, tg, grid, wv, wh, stream);
     } else {
         e = launch_generic_sep(exact, in, in_pitch, img_stride, out, out_pitch,
                                batch > 1 ? out_image_stride : n * out_pitch, n, m, batch, wv, wh, ctx->num_sms,

@@ -111,11 +111,15 @@ cudaError_t launch_tma_u8_group(int k, bool exact, const CUtensorMap& tmap, cons
                                 int32_t pitch_words, cudaStream_t stream);
 
 // separable 3x3 stencil on one f32 plane (stencil_sep.cu)
-constexpr int kNumSepConfigs = 3;
+constexpr int kNumSepConfigs = 9;
+constexpr int kSepTmaStoreConfig = 3;  // TMA-store epilogue (16-byte aligned outputs with m % 4 == 0)
+constexpr int64_t kSepMaxBandRows = 136;  // tile-height cap of the TMA-loaded stencil
 extern const TmaConfig kSepConfigs[kNumSepConfigs];
 cudaError_t sep_configure(int cfg, int* ctas_per_sm);
-cudaError_t launch_tma_sep(int cfg, bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid,
-                           const float* wv, const float* wh, cudaStream_t stream);
+bool sep_config_tma_store(int cfg);
+// out_tmap: the output tensor map {m, n, batch}, box {128, 2, 1} (TMA-store configs only)
+cudaError_t launch_tma_sep(int cfg, bool exact, const CUtensorMap& tmap, const CUtensorMap* out_tmap,
+                           const TileGeom& tg, int64_t grid, const float* wv, const float* wh, cudaStream_t stream);
 cudaError_t launch_generic_sep(bool exact, const float* in, int64_t in_pitch, int64_t in_image_stride, float* out,
                                int64_t out_pitch, int64_t out_image_stride, int64_t n, int64_t m, int64_t batch,
                                const float* wv, const float* wh, int num_sms, cudaStream_t stream);

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "harris_common.cuh"
 #include "harris_internal.h"
@@ -38,20 +39,60 @@ template <>
 struct SepCfg<2> {
     static constexpr int NW = 8, NS = 4, CH = 6, MINB = 1;
 };
+// 3 (default for 16-byte aligned outputs): TMA-store outputs, 8 warps x 6 stages + 2 output
+// staging buffers per warp (202 KB)
+template <>
+struct SepCfg<3> {
+    static constexpr int NW = 8, NS = 6, CH = 6, MINB = 1;
+    static constexpr bool TS = true;
+};
+// 4-8: pipeline-shape sweep (warps x stages x rows per stage), register stores
+template <>
+struct SepCfg<4> {
+    static constexpr int NW = 6, NS = 10, CH = 6, MINB = 1;
+};
+template <>
+struct SepCfg<5> {
+    static constexpr int NW = 4, NS = 16, CH = 6, MINB = 1;
+};
+template <>
+struct SepCfg<6> {
+    static constexpr int NW = 16, NS = 4, CH = 6, MINB = 1;
+};
+template <>
+struct SepCfg<7> {
+    static constexpr int NW = 8, NS = 4, CH = 12, MINB = 1;
+};
+template <>
+struct SepCfg<8> {
+    static constexpr int NW = 12, NS = 5, CH = 6, MINB = 1;
+};
+template <int CFG, class = void>
+struct SepTs : std::false_type {};
+template <int CFG>
+struct SepTs<CFG, std::void_t<decltype(SepCfg<CFG>::TS)>> : std::integral_constant<bool, SepCfg<CFG>::TS> {};
 
-const TmaConfig kSepConfigs[kNumSepConfigs] = {{8, 8, 6}, {8, 4, 6}, {8, 4, 6}};
+const TmaConfig kSepConfigs[kNumSepConfigs] = {{8, 8, 6}, {8, 4, 6}, {8, 4, 6}, {8, 6, 6}, {6, 10, 6},
+                                               {4, 16, 6}, {16, 4, 6}, {8, 4, 12}, {12, 5, 6}};
+
+template <int CFG, bool EXACT>
+using SepOpOf = std::conditional_t<SepTs<CFG>::value, Sep3x3TsOp<EXACT, SepCfg<CFG>::CH>,
+                                   Sep3x3Op<EXACT, SepCfg<CFG>::CH>>;
 
 template <int CFG, bool EXACT>
 static constexpr auto sep_kernel() {
     using C = SepCfg<CFG>;
-    return strip_kernel<Sep3x3Op<EXACT, C::CH>, C::NW, C::NS, C::MINB>;
+    return strip_kernel<SepOpOf<CFG, EXACT>, C::NW, C::NS, C::MINB>;
 }
 
 template <int CFG>
 static constexpr size_t sep_smem() {
     using C = SepCfg<CFG>;
-    return StripShape<C::NW, C::NS, Sep3x3Op<false, C::CH>>::kSmemBytes;
+    return StripShape<C::NW, C::NS, SepOpOf<CFG, false>>::kSmemBytes;
 }
+static_assert(sep_smem<3>() <= 227 * 1024 && sep_smem<4>() <= 227 * 1024 && sep_smem<5>() <= 227 * 1024 &&
+                  sep_smem<6>() <= 227 * 1024 && sep_smem<7>() <= 227 * 1024 && sep_smem<8>() <= 227 * 1024,
+              "stencil smem");
 
 template <int CFG>
 static cudaError_t sep_configure_one(int* ctas_per_sm) {
@@ -72,31 +113,60 @@ cudaError_t sep_configure(int cfg, int* ctas_per_sm) {
         case 0: return sep_configure_one<0>(ctas_per_sm);
         case 1: return sep_configure_one<1>(ctas_per_sm);
         case 2: return sep_configure_one<2>(ctas_per_sm);
+        case 3: return sep_configure_one<3>(ctas_per_sm);
+        case 4: return sep_configure_one<4>(ctas_per_sm);
+        case 5: return sep_configure_one<5>(ctas_per_sm);
+        case 6: return sep_configure_one<6>(ctas_per_sm);
+        case 7: return sep_configure_one<7>(ctas_per_sm);
+        case 8: return sep_configure_one<8>(ctas_per_sm);
         default: return cudaErrorInvalidValue;
     }
 }
 
-template <int CFG>
-static cudaError_t sep_launch_one(bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid,
-                                  const float* wv, const float* wh, cudaStream_t stream) {
+template <int CFG, bool EXACT>
+static void sep_launch_order(const CUtensorMap& tmap, const CUtensorMap* out_tmap, const TileGeom& tg,
+                             int64_t grid, const float* wv, const float* wh, cudaStream_t stream) {
     using C = SepCfg<CFG>;
+    using Op = SepOpOf<CFG, EXACT>;
     const dim3 block{unsigned(C::NW * 32)}, gridd{unsigned(grid)};
-    if (exact) {
-        typename Sep3x3Op<true, C::CH>::Params p{{wv[0], wv[1], wv[2]}, {wh[0], wh[1], wh[2]}};
-        sep_kernel<CFG, true>()<<<gridd, block, sep_smem<CFG>(), stream>>>(tmap, tg, p);
+    typename Sep3x3Op<EXACT, C::CH>::Params base{{wv[0], wv[1], wv[2]}, {wh[0], wh[1], wh[2]}};
+    if constexpr (SepTs<CFG>::value) {
+        typename Op::Params p;
+        p.out = *out_tmap;
+        p.base = base;
+        sep_kernel<CFG, EXACT>()<<<gridd, block, sep_smem<CFG>(), stream>>>(tmap, tg, p);
     } else {
-        typename Sep3x3Op<false, C::CH>::Params p{{wv[0], wv[1], wv[2]}, {wh[0], wh[1], wh[2]}};
-        sep_kernel<CFG, false>()<<<gridd, block, sep_smem<CFG>(), stream>>>(tmap, tg, p);
+        (void)out_tmap;
+        sep_kernel<CFG, EXACT>()<<<gridd, block, sep_smem<CFG>(), stream>>>(tmap, tg, base);
     }
+}
+
+template <int CFG>
+static cudaError_t sep_launch_one(bool exact, const CUtensorMap& tmap, const CUtensorMap* out_tmap,
+                                  const TileGeom& tg, int64_t grid, const float* wv, const float* wh,
+                                  cudaStream_t stream) {
+    if (SepTs<CFG>::value && !out_tmap) return cudaErrorInvalidValue;
+    if (exact)
+        sep_launch_order<CFG, true>(tmap, out_tmap, tg, grid, wv, wh, stream);
+    else
+        sep_launch_order<CFG, false>(tmap, out_tmap, tg, grid, wv, wh, stream);
     return cudaGetLastError();
 }
 
-cudaError_t launch_tma_sep(int cfg, bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid,
-                           const float* wv, const float* wh, cudaStream_t stream) {
+bool sep_config_tma_store(int cfg) { return cfg == 3; }
+
+cudaError_t launch_tma_sep(int cfg, bool exact, const CUtensorMap& tmap, const CUtensorMap* out_tmap,
+                           const TileGeom& tg, int64_t grid, const float* wv, const float* wh, cudaStream_t stream) {
     switch (cfg) {
-        case 0: return sep_launch_one<0>(exact, tmap, tg, grid, wv, wh, stream);
-        case 1: return sep_launch_one<1>(exact, tmap, tg, grid, wv, wh, stream);
-        case 2: return sep_launch_one<2>(exact, tmap, tg, grid, wv, wh, stream);
+        case 0: return sep_launch_one<0>(exact, tmap, out_tmap, tg, grid, wv, wh, stream);
+        case 1: return sep_launch_one<1>(exact, tmap, out_tmap, tg, grid, wv, wh, stream);
+        case 2: return sep_launch_one<2>(exact, tmap, out_tmap, tg, grid, wv, wh, stream);
+        case 3: return sep_launch_one<3>(exact, tmap, out_tmap, tg, grid, wv, wh, stream);
+        case 4: return sep_launch_one<4>(exact, tmap, out_tmap, tg, grid, wv, wh, stream);
+        case 5: return sep_launch_one<5>(exact, tmap, out_tmap, tg, grid, wv, wh, stream);
+        case 6: return sep_launch_one<6>(exact, tmap, out_tmap, tg, grid, wv, wh, stream);
+        case 7: return sep_launch_one<7>(exact, tmap, out_tmap, tg, grid, wv, wh, stream);
+        case 8: return sep_launch_one<8>(exact, tmap, out_tmap, tg, grid, wv, wh, stream);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -20,6 +20,7 @@ struct Sep3x3Op {
     static constexpr int kRowsPerStage = CH;
     static constexpr int kHaloRows = 2;
     static constexpr bool kTwoStoreVariants = true;  // measured +5 % on unaligned planes
+    static constexpr bool kRealignStores = true;     // 8-byte aligned output rows: 16-byte stores anyway
     static constexpr uint32_t kTxBytes = uint32_t(CH) * kBoxCols * 4u;
     static constexpr uint32_t kStageBytes = (kTxBytes + 127u) / 128u * 128u;
     struct Params {
@@ -79,6 +80,24 @@ struct Sep3x3Op {
             }
         }
     }
+};
+
+// The same stencil with TMA-store outputs (strip engine kTmaStore): a lane writes its 4
+// outputs per row to the warp's staging buffer, lane 0 stores 128 x 2-row boxes through the
+// output tensor map.  The 1:1 read/write mix of this op leaves the register-store version
+// short of the copy ceiling (outstanding writes per SM with 8 warps); bulk stores move the
+// write stream to the TMA unit.  Needs 16-byte aligned output rows (tensor-map strides).
+template <bool EXACT, int CH>
+struct Sep3x3TsOp : Sep3x3Op<EXACT, CH> {
+    using Base = Sep3x3Op<EXACT, CH>;
+    static constexpr bool kTmaStore = true;
+    static constexpr uint32_t kOutStageBytes = uint32_t(CH) * kWarpCols * 4u;
+    struct Params {
+        CUtensorMap out;  // {m, n, batch} f32, box {128, 2, 1}
+        typename Base::Params base;
+    };
+    __device__ __forceinline__ explicit Sep3x3TsOp(const Params& p) : Base(p.base) {}
+    __device__ __forceinline__ static const void* out_tmap(const Params& p) { return &p.out; }
 };
 
 }  // namespace harris

@@ -118,6 +118,58 @@ struct SplitStoresOf : std::false_type {};
 template <class Op>
 struct SplitStoresOf<Op, std::void_t<decltype(Op::kSplitStores)>> : std::integral_constant<bool, Op::kSplitStores> {};
 
+// Op::kRealignStores is optional (default false; single-strip ops): output rows that are only
+// 8-byte aligned (TileGeom::vec_store == 1 — e.g. the 1918-float rows of a contiguous stencil
+// output, whose rows alternate between 16- and 8-byte alignment) are written with 16-byte
+// stores anyway: on a row that starts 8 bytes past a 16-byte boundary, lane L stores its last
+// two outputs and lane L+1's first two (one shuffle pair) at the aligned address, lane 0 adds
+// its first two and lane 31 its last two as 8-byte stores.  Rows that are 16-byte aligned keep
+// one float4 per lane.  Replaces four scalar stores per lane per row.
+template <class Op, class = void>
+struct RealignStoresOf : std::false_type {};
+template <class Op>
+struct RealignStoresOf<Op, std::void_t<decltype(Op::kRealignStores)>>
+    : std::integral_constant<bool, Op::kRealignStores> {};
+
+// one output row of 4 values per lane at po (lane column cg of an m-column row whose start is
+// 8-byte aligned); warp-uniform alignment test per row
+__device__ __forceinline__ void stg_realigned_row(float* po, const float (&o)[4], int cg, int m, int lane) {
+    const float n0 = __shfl_down_sync(0xffffffffu, o[0], 1);
+    const float n1 = __shfl_down_sync(0xffffffffu, o[1], 1);
+    if ((reinterpret_cast<uintptr_t>(po) & 15u) == 0) {
+        if (cg + 4 <= m) {
+            stg128_cs(po, o[0], o[1], o[2], o[3]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (cg + k < m) po[k] = o[k];
+        }
+        return;
+    }
+    if (lane == 0) {
+        if (cg + 2 <= m)
+            stg64_cs(po, o[0], o[1]);
+        else if (cg < m)
+            po[0] = o[0];
+    }
+    if (lane < 31) {
+        if (cg + 6 <= m) {
+            stg128_cs(po + 2, o[2], o[3], n0, n1);
+        } else {
+            const float v[4] = {o[2], o[3], n0, n1};
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (cg + 2 + k < m) po[2 + k] = v[k];
+        }
+    } else {
+        if (cg + 4 <= m) {
+            stg64_cs(po + 2, o[2], o[3]);
+        } else if (cg + 2 < m) {
+            po[2] = o[2];
+        }
+    }
+}
+
 // Op::kTwoStoreVariants is optional (default false): compile the consumer's stage loop twice,
 // with and without the scalar-store code for ragged / unaligned output lanes.  Measured per
 // op (tools/perf_matrix.sh): issue-bound u8 TMA 840 -> 887 k MP/s, stencil on 1918-wide
@@ -149,10 +201,29 @@ struct HasBeginTile : std::false_type {};
 template <class Op>
 struct HasBeginTile<Op, std::void_t<decltype(&Op::begin_tile)>> : std::true_type {};
 
+// Op::kTmaStore is optional (default false): outputs leave through TMA stores instead of
+// per-lane st.global.  Each warp owns two output staging buffers of kRowsPerStage x 128
+// floats (Op::kOutStageBytes); the lanes write a stage's output rows there (st.shared.v4),
+// fence them into the async proxy, and lane 0 stores them as 128 x 2-row boxes through the
+// output tensor map Op::out_tmap(params) (cp.async.bulk.tensor, one bulk group per stage)
+// while the warp computes the next stage into the other buffer.  The tensor map clips the
+// right / bottom edges; band_rows must be even (a row pair never straddles two tiles).
+// Single-strip ops (kGroups == 1, 128-column strips) only.
+template <class Op, class = void>
+struct TmaStoreOf : std::false_type {};
+template <class Op>
+struct TmaStoreOf<Op, std::void_t<decltype(Op::kTmaStore)>> : std::integral_constant<bool, Op::kTmaStore> {};
+
+template <class Op, bool TS = TmaStoreOf<Op>::value>
+struct OutStageBytesOf : std::integral_constant<size_t, 0> {};
+template <class Op>
+struct OutStageBytesOf<Op, true> : std::integral_constant<size_t, Op::kOutStageBytes> {};
+
 template <int NW, int NS, class Op>
 struct StripShape {
     static_assert(Op::kStageBytes % 128 == 0, "TMA destinations must be 128-byte aligned");
-    static constexpr size_t kSmemBytes = size_t(NW) * NS * Op::kStageBytes + size_t(NW) * NS * 8 + 128;
+    static constexpr size_t kOutBytes = size_t(NW) * 2 * OutStageBytesOf<Op>::value;  // TMA-store staging
+    static constexpr size_t kSmemBytes = size_t(NW) * NS * Op::kStageBytes + kOutBytes + size_t(NW) * NS * 8 + 128;
 };
 
 // Completion notification for fused gathers (TileGeom::notify_flag): every thread
@@ -176,7 +247,8 @@ __device__ __forceinline__ void notify_epilogue(const TileGeom& g) {
 
 template <class Op, int NW, int NS, int MINB = 1>
 __global__ void __launch_bounds__(NW * 32, MINB)
-    strip_kernel(const __grid_constant__ CUtensorMap tmap, const TileGeom g, const typename Op::Params p) {
+    strip_kernel(const __grid_constant__ CUtensorMap tmap, const TileGeom g,
+                 const __grid_constant__ typename Op::Params p) {
     constexpr int CH = Op::kRowsPerStage;
     constexpr int HALO = Op::kHaloRows;
     constexpr int G = Op::kGroups;
@@ -188,7 +260,14 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     unsigned char* ring = base + size_t(warp) * NS * Op::kStageBytes;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(base + size_t(NW) * NS * Op::kStageBytes) + warp * NS;
+    constexpr bool TS = TmaStoreOf<Op>::value;
+    constexpr size_t kOutStage = OutStageBytesOf<Op>::value;
+    static_assert(!TS || (G == 1 && Op::kStripCols == kWarpCols && CH % 2 == 0 && HALO % 2 == 0 &&
+                          kOutStage == size_t(CH) * kWarpCols * 4 && kOutStage % 128 == 0),
+                  "TMA-store ops: one 128-column strip, row pairs aligned with the stage and the halo");
+    unsigned char* ostage = base + size_t(NW) * NS * Op::kStageBytes + size_t(warp) * 2 * kOutStage;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(base + size_t(NW) * NS * Op::kStageBytes +
+                                                 StripShape<NW, NS, Op>::kOutBytes) + warp * NS;
 
     const int64_t GW = int64_t(gridDim.x) * NW;
     const int64_t gw = int64_t(blockIdx.x) * NW + warp;
@@ -280,6 +359,9 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     Op op(p);
     int stage = 0;
     uint32_t phase = 0;
+    int obuf = 0;  // TMA-store ops: staging buffer of the current stage
+    (void)obuf;
+    (void)ostage;
     for (int64_t k = 0; k < waves; ++k) {
         const int64_t t = gw + k * GW;
         // Re-align the CTA's warps at every tile boundary.  They work on adjacent strips
@@ -300,6 +382,45 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                 im[k] = tc.b[k];
             }
             op.begin_tile(c0, tc.band * g.band_rows, im);
+        }
+        if constexpr (TS) {
+            // ---- TMA-store stage loop: outputs go to the staging buffer, lane 0 stores row pairs
+            const int ox = tc.cs[0] * kWarpCols, oy0 = tc.band * g.band_rows, oz = tc.b[0];
+            const void* otm = Op::out_tmap(p);
+            for (int c = 0; c < nch; ++c) {
+                mbar_wait(&bars[stage], phase);
+                const unsigned char* sm = ring + stage * Op::kStageBytes;
+                float* so = reinterpret_cast<float*>(ostage + obuf * kOutStage);
+                // the buffer's previous bulk group (two stages ago) must have finished reading it
+                if (lane == 0) bulk_wait_read<1>();
+                __syncwarp();
+                static_for(
+                    [&](auto rc) {
+                        constexpr int R = decltype(rc)::value;
+                        float out4[1][4];
+                        op.template row<R>(sm, lane, out4);
+                        sts128(so + R * kWarpCols + lane * kColsPerLane, out4[0][0], out4[0][1], out4[0][2],
+                               out4[0][3]);
+                    },
+                    std::make_integer_sequence<int, CH>{});
+                fence_proxy_async_shared();
+                __syncwarp();
+                if (lane == 0) {
+#pragma unroll
+                    for (int q = 0; q < CH / 2; ++q) {
+                        const int o = c * CH + 2 * q - HALO;  // first output row of the pair (tile-relative)
+                        if (o >= 0 && o < rows_out) tma_store_3d(otm, so + 2 * q * kWarpCols, ox, oy0 + o, oz);
+                    }
+                    bulk_commit();
+                }
+                issue(stage);
+                obuf ^= 1;
+                if (++stage == NS) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
+            }
+            continue;
         }
         int colg[G];
         float* orow[G];
@@ -342,7 +463,9 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                         stg128_cs_if(vec[gi], po, out4[gi][0], out4[gi][1], out4[gi][2], out4[gi][3]);           \
                         if (RAGGED) { /* unaligned output rows, or the ragged right edge */                      \
                             const int cg = colg[gi];                                                             \
-                            if (!vec[gi] && cg < g.m) {                                                          \
+                            if (RealignStoresOf<Op>::value && g.vec_store == 1) {                                \
+                                stg_realigned_row(po, out4[gi], cg, g.m, lane);                                  \
+                            } else if (!vec[gi] && cg < g.m) {                                                   \
                                 if (SplitStoresOf<Op>::value && g.vec_store == 1 && cg + kColsPerLane <= g.m) {  \
                                     stg2x2_cs(po, out4[gi][0], out4[gi][1], out4[gi][2], out4[gi][3]);           \
                                 } else {                                                                         \
@@ -372,6 +495,9 @@ __global__ void __launch_bounds__(NW * 32, MINB)
             HARRIS_STAGE_LOOP(ragged)
         }
 #undef HARRIS_STAGE_LOOP
+    }
+    if constexpr (TS) {
+        if (lane == 0) bulk_wait_all();  // every TMA store performed (and its staging read) before exit
     }
     notify_epilogue(g);
 }

@@ -278,7 +278,7 @@ BINOMIAL = (1.0, 2.0, 1.0)  # weightsV = weightsH of the reference (evalref.py:1
 
 def stencil3x3_sep(img: torch.Tensor, wv=BINOMIAL, wh=BINOMIAL, *, out: Optional[torch.Tensor] = None,
                    exact: bool = False, force_generic: bool = False, force_tma: bool = False,
-                   stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+                   stream: Optional[torch.cuda.Stream] = None, ctx: Optional[HarrisContext] = None) -> torch.Tensor:
     """Separable 3x3 stencil ``(H, W)`` / ``(B, H, W)`` float32 CUDA -> ``(H-2, W-2)`` /
     ``(B, H-2, W-2)``: vertical ``wv`` then horizontal ``wh`` (the separated form of the
     reference's binomial rewrite goal)."""
@@ -301,7 +301,7 @@ def stencil3x3_sep(img: torch.Tensor, wv=BINOMIAL, wh=BINOMIAL, *, out: Optional
     fwh = (ctypes.c_float * 3)(*[float(v) for v in wh])
     dev = img.device.index if img.device.index is not None else torch.cuda.current_device()
     st = stream if stream is not None else torch.cuda.current_stream(dev)
-    ctx = context(dev)
+    ctx = ctx or context(dev)
     rc = lib().harris_stencil3x3_sep(ctx.handle, out.data_ptr(), out.stride(-2),
                                      out.stride(0) if batched else n * out.stride(-2), n, m, img.data_ptr(),
                                      img.stride(-2), img.stride(0) if batched else H * img.stride(-2), B,

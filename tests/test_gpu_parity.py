@@ -390,6 +390,102 @@ def test_stencil_unaligned_layouts(cuda_ctx, off):
             assert np.array_equal(got[b].cpu().numpy(), cref.sep3x3_f32(imgs[b])), (off, pad, b)
 
 
+# TMA-loaded stencil planes (W % 4 == 0).  Outputs with a 16-byte aligned pitch (here the
+# thesis-style pitch = input width) run the TMA-store epilogue (config 3, the default);
+# contiguous outputs (pitch m = W - 2, rows alternately 16- and 8-byte aligned) store from
+# registers with the realigned 16-byte stores.  Configs 0-2 store from registers always.
+# Odd output heights, 1-row outputs, ragged right edges, batches, row-band views; EXACT
+# equals the C oracle, FAST is identical across configs and store modes.
+SEP_TS_SHAPES = [(3, 8), (4, 12), (7, 132), (8, 260), (41, 516), (300, 1032), (1081, 2052)]
+
+
+@pytest.mark.parametrize("cfg", range(4))
+def test_every_sep_config_bitexact(cuda_ctx, cfg):
+    ctx = _ctx_with({"HARRIS_SEP_CONFIG": cfg})
+    for H, W in SEP_TS_SHAPES:
+        img = synth.synth_numpy(1, H, W, seed=cfg * 31 + H + W)[0]
+        x = _dev(img)
+        # (a) the whole plane, contiguous output (m = W - 2: rows alternately 16- / 8-byte
+        #     aligned, realigned register stores) or a padded output (pitch W + 4)
+        # (b) a column-crop view x[:, :W-2] (pitch W): m = W - 4 is a multiple of 4, so a
+        #     16-byte aligned output pitch takes the TMA-store epilogue (config 3)
+        for xin, mm in ((x, W - 2), (x[:, :W - 2], W - 4)):
+            ref = cref.sep3x3_f32(np.ascontiguousarray(img[:, :mm + 2]))
+            padded = torch.full((H - 2, W + 4), float("nan"), device="cuda")
+            for out in (None, padded[:, :mm]):
+                ex = hb.stencil3x3_sep(xin, exact=True, ctx=ctx, out=out)
+                torch.cuda.synchronize()
+                assert ctx.last_path == _lib.PATH_TMA
+                assert np.array_equal(ex.cpu().numpy(), ref), (cfg, H, W, mm, out is None)
+                fast = hb.stencil3x3_sep(xin, ctx=ctx, out=out)
+                assert torch.equal(fast, hb.stencil3x3_sep(xin)), (cfg, H, W, mm)
+            assert torch.isnan(padded[:, mm:]).all(), (cfg, H, W, mm)  # nothing past the view's columns
+    B, H, W = 3, 37, 132
+    imgs = synth.synth_numpy(B, H, W, seed=cfg)
+    x = _dev(imgs)
+    for out in (None, torch.empty(B, H - 2, W, device="cuda")[..., :W - 2]):
+        got = hb.stencil3x3_sep(x, exact=True, ctx=ctx, out=out)
+        torch.cuda.synchronize()
+        for b in range(B):
+            assert np.array_equal(got[b].cpu().numpy(), cref.sep3x3_f32(imgs[b])), (cfg, b)
+    # a row band (view with the parent's pitch) into a padded output view (pitch m + 6)
+    outbuf = torch.full((20, 136), float("nan"), device="cuda")
+    band = hb.stencil3x3_sep(x[2, 5:27], exact=True, ctx=ctx, out=outbuf[:, :130])
+    torch.cuda.synchronize()
+    assert torch.equal(band, got[2, 5:25])
+    assert torch.isnan(outbuf[:, 130:]).all()
+
+
+@pytest.mark.parametrize("H,W", [(5, 8), (9, 68), (40, 132), (77, 1920), (1080, 1920)])
+def test_sep_realigned_stores(cuda_ctx, H, W):
+    """Contiguous outputs of TMA-loaded planes: m = W - 2 is 2 (mod 4), so output rows
+    alternate between 16- and 8-byte alignment (and batches add an image stride that is
+    itself 8 mod 16 when n is odd): every row, every lane, ragged right edges, nothing
+    written outside the output."""
+    B = 3
+    imgs = synth.synth_numpy(B, H, W, seed=H * W)
+    x = _dev(imgs)
+    n, m = H - 2, W - 2
+    buf = torch.full((B * n * m + 64,), float("nan"), device="cuda")
+    out = buf[32:32 + B * n * m].view(B, n, m)  # base 16-byte aligned (32 floats in)
+    hb.stencil3x3_sep(x, exact=True, out=out)
+    torch.cuda.synchronize()
+    assert cuda_ctx.last_path == _lib.PATH_TMA
+    for b in range(B):
+        assert np.array_equal(out[b].cpu().numpy(), cref.sep3x3_f32(imgs[b])), (H, W, b)
+    assert torch.isnan(buf[:32]).all() and torch.isnan(buf[32 + B * n * m:]).all()
+    # 8-byte aligned base (rows start at 8 mod 16 first)
+    out2 = buf[2:2 + B * n * m].view(B, n, m)
+    buf.fill_(float("nan"))
+    hb.stencil3x3_sep(x, exact=True, out=out2)
+    torch.cuda.synchronize()
+    for b in range(B):
+        assert np.array_equal(out2[b].cpu().numpy(), cref.sep3x3_f32(imgs[b])), (H, W, b, "base+8")
+    assert torch.isnan(buf[:2]).all() and torch.isnan(buf[2 + B * n * m:]).all()
+
+
+@pytest.mark.parametrize("band_rows", [1, 2, 7, 30])
+def test_sep_tma_store_tiles_never_overlap(cuda_ctx, band_rows):
+    """TMA stores write row pairs: tiles get an even height (a forced odd height is rounded
+    up), only an image's last band may be odd and its extra row falls outside the tensor
+    map.  Output padding rows / columns around a view stay untouched."""
+    ctx = hb.HarrisContext(0, band_rows=band_rows)
+    for B, H, W in [(1, 2 + 37, 130), (2, 2 + 64, 262), (3, 2 + 9, 514)]:
+        imgs = synth.synth_numpy(B, H, W + 2, seed=band_rows + H)
+        x = _dev(imgs)[..., :W]  # column-crop view, pitch W + 2: m = W - 2 is a multiple of 4
+        imgs = np.ascontiguousarray(imgs[..., :W])
+        n, m = H - 2, W - 2
+        big = torch.full((B, n + 3, m + 12), float("nan"), device="cuda")  # pitch m + 12: 16-byte multiple
+        out = big[:, 1:n + 1, 4:m + 4]
+        hb.stencil3x3_sep(x, exact=True, ctx=ctx, out=out)
+        torch.cuda.synchronize()
+        for b in range(B):
+            assert np.array_equal(out[b].cpu().numpy(), cref.sep3x3_f32(imgs[b])), (band_rows, B, H, W, b)
+        mask = torch.ones_like(big, dtype=torch.bool)
+        mask[:, 1:n + 1, 4:m + 4] = False
+        assert torch.isnan(big[mask]).all(), (band_rows, H, W)
+
+
 def _ctx_with(env: dict):
     import os
     env = dict(env, HARRIS_DEV=1)  # developer knobs are read only with HARRIS_DEV=1

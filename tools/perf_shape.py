@@ -1,4 +1,4 @@
-"""A/B timing of one shape: python tools/perf_shape.py {f32,f32crop,u8,sep} B H W [reps]; HARRIS_LIB selects the .so."""
+"""A/B timing of one shape: python tools/perf_shape.py {f32,f32crop,u8,sep,seppad,sepcrop} B H W [reps]; HARRIS_LIB selects the .so."""
 import sys, torch
 sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
 import paper_2212_12035_b200 as hb
@@ -10,6 +10,14 @@ if kind == "u8":
     f = lambda: hb.harris_u8(x, out=out)
 elif kind == "sep":
     x = torch.rand((B, H, W), device="cuda", generator=g)
+    out2 = torch.empty((B, H - 2, W - 2), device="cuda")
+    f = lambda: hb.stencil3x3_sep(x, out=out2)
+elif kind == "seppad":  # thesis-style output pitch = input width (16-byte aligned rows)
+    x = torch.rand((B, H, W), device="cuda", generator=g)
+    out2 = torch.empty((B, H - 2, W), device="cuda")[..., :W - 2]
+    f = lambda: hb.stencil3x3_sep(x, out=out2)
+elif kind == "sepcrop":  # column-crop view x[..., :W] of (W+2)-pitch planes: TMA loads, m = W - 2
+    x = torch.rand((B, H, W + 2), device="cuda", generator=g)[..., :W]
     out2 = torch.empty((B, H - 2, W - 2), device="cuda")
     f = lambda: hb.stencil3x3_sep(x, out=out2)
 elif kind == "f32crop":  # column-crop view: base 4-byte aligned only
@@ -28,5 +36,5 @@ for _ in range(reps):
 torch.cuda.synchronize()
 ts = sorted(a.elapsed_time(b) for a, b in evs)
 med = ts[len(ts) // 2]
-px = B * (H - 2) * (W - 2) if kind == "sep" else B * (H - 4) * (W - 4)
+px = B * (H - 2) * (W - 2) if kind.startswith("sep") else B * (H - 4) * (W - 4)
 print(f"{sys.argv[1:]} {'old' if 'HARRIS_LIB' in __import__('os').environ else 'new'} median_ms {med:.4f} MP/s {px/med/1e3:.0f}")
