@@ -600,6 +600,70 @@ def time_launches(fn, iters: int, flush=None) -> list[float]:
     return [a.elapsed_time(b) for a, b in evs]
 
 
+# ---------------------------------------------------------- frame streams
+def frame_stream(H, W, n_frames=240, ring=None,
+                  modes=("plain", "pdl", "independent", "graph", "frames", "frames_graph")) -> dict:
+    """Back-to-back UNBATCHED single frames over a ring of distinct frames (> L2, so every frame
+    streams from HBM).  Modes: plain launches; pdl (HARRIS_FLAG_PDL); independent
+    (HARRIS_FLAG_PDL_INDEPENDENT); graph (the independent ring captured in a CUDA graph and
+    replayed); frames (harris_run_frames: the ring in one C call, one launch per frame);
+    frames_graph.  Per mode: us per frame = CUDA-event time of N frames / N."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    import paper_2212_12035_b200 as hb
+    frame_bytes = 12 * H * W
+    ring = ring or max(4, -(-(384 << 20) // frame_bytes))  # >= 384 MB of inputs: 3x the L2
+    xs = [torch.empty((3, H, W), device=dev) for _ in range(ring)]
+    for i, x in enumerate(xs):
+        hb.synth_(x, seed=12035 + i)
+    outs = [torch.empty((H - 4, W - 4), device=dev) for _ in range(ring)]
+    peak, _ = measured_peak()
+    nbytes = hb.algorithmic_bytes(H - 4, W - 4)
+    res = {"frame": f"{W}x{H} RGB f32", "ring_frames": ring, "ring_input_mb": ring * frame_bytes / 2**20}
+    ref = [hb.harris(x) for x in xs]
+    for mode in modes:
+        pdl = {"plain": False, "pdl": True, "independent": "independent", "graph": "independent"}.get(mode)
+
+        if mode.startswith("frames"):
+            def one_pass():
+                hb.harris_frames(xs, outs)
+        else:
+            def one_pass():
+                for x, o in zip(xs, outs):
+                    hb.harris(x, out=o, pdl=pdl)
+        for _ in range(3):
+            one_pass()
+        torch.cuda.synchronize()
+        if mode in ("graph", "frames_graph"):
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                one_pass()  # warm on the capture stream
+                torch.cuda.synchronize()
+                with torch.cuda.graph(g, stream=s):
+                    one_pass()
+            torch.cuda.synchronize()
+            run = g.replay
+        else:
+            run = one_pass
+        reps = max(1, n_frames // ring)
+        run()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            run()
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / (reps * ring)
+        ok = all(torch.equal(o, r) for o, r in zip(outs, ref))
+        res[mode] = {"us_per_frame": us, "value": (H - 4) * (W - 4) / us, "unit": "MP/s",
+                     "frac_of_measured_hbm": nbytes / (us * 1e-6) / 1e9 / peak, "frames": reps * ring,
+                     "outputs_identical": ok}
+    return res
+
+
+
 def run_extra(a, ctx, dev) -> dict:
     """Single-GPU roofline runs of the other configs (not the headline line)."""
     import paper_2212_12035_b200 as hb
@@ -671,6 +735,11 @@ def run_extra(a, ctx, dev) -> dict:
                                 "achieved_gbs": gbs, "frac_of_measured_hbm": gbs / peak}
     del xb, ob
     del scratch, scratch2
+    torch.cuda.empty_cache()
+    # single-frame streams (the thesis's per-frame measurement): back-to-back
+    # unbatched launches over a ring of distinct frames (> L2), plain / PDL / independent-PDL /
+    # CUDA-graph / harris_run_frames (tools/frame_stream.py)
+    res["frame_stream"] = {f"{W}x{H}": frame_stream(H, W, 180) for H, W in ((1536, 2560), (2560, 1536), (2832, 4256))}
     torch.cuda.empty_cache()
 
     # other input formats / stencils on the same engine, batch of 1024 x 1080x1920 (inputs >> L2)

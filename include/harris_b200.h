@@ -62,6 +62,19 @@ extern "C" {
 #define HARRIS_FLAG_FORCE_GENERIC 0x2u  /* use the generic (non-TMA) kernel */
 #define HARRIS_FLAG_FORCE_TMA     0x4u  /* fail with HARRIS_ERR_ALIGNMENT instead of falling
                                            back to the generic GPU kernel */
+#define HARRIS_FLAG_PDL           0x8u  /* programmatic dependent launch: the kernel is launched
+                                           while the previous kernel on the stream may still run;
+                                           its prologue overlaps that kernel's tail and it waits
+                                           for it (griddepcontrol.wait) before touching memory.
+                                           Safe for any stream content. */
+#define HARRIS_FLAG_PDL_INDEPENDENT 0x10u /* PDL without the wait before the work: the CALLER
+                                           guarantees that no earlier work on the stream that may
+                                           still be running writes this call's input or reads or
+                                           writes its output (a stream of independent frames in
+                                           distinct buffers).  Loads start at once and the kernel
+                                           fills the SMs the previous one leaves; it still
+                                           completes only after the previous kernel, so later
+                                           stream work sees stream order. */
 
 /* which kernel the last harris_run* on a ctx launched */
 #define HARRIS_PATH_NONE    0
@@ -128,6 +141,17 @@ HARRIS_API int harris_run_strided(harris_ctx* ctx, float* out, int64_t out_pitch
                        int64_t n, int64_t m, const float* rgb, int64_t in_pitch,
                        int64_t in_chan_stride, int64_t in_image_stride, int64_t batch,
                        float kappa, uint32_t flags, void* cuda_stream);
+
+/* A stream of independent single frames, one launch per frame, back to back (the thesis's
+ * per-frame measurement, without batching them): frame k reads the
+ * planar image rgbs[k] (3 x (n+4) x (m+4), row pitch in_pitch, channel stride in_chan_stride)
+ * and writes outs[k] (n x m, row pitch out_pitch).  Frame 0 is launched with HARRIS_FLAG_PDL
+ * (it waits for earlier stream work; HARRIS_FLAG_PDL_INDEPENDENT in flags drops that wait),
+ * frames 1.. with HARRIS_FLAG_PDL_INDEPENDENT, so each frame's kernel starts on the SMs the
+ * previous frame leaves.  All outs[] must be distinct and must not overlap any rgbs[]. */
+HARRIS_API int harris_run_frames(harris_ctx* ctx, float* const* outs, int64_t out_pitch, int64_t n, int64_t m,
+                                 const float* const* rgbs, int64_t in_pitch, int64_t in_chan_stride,
+                                 int64_t frames, float kappa, uint32_t flags, void* cuda_stream);
 
 /* HOST buffers (pinned for full speed; pageable works).  Row bands (batch == 1) or
  * image groups are pipelined H2D -> kernel -> D2H over three streams; returns when

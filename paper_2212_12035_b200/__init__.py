@@ -16,6 +16,6 @@ no CPU fallback: without the library or a B200 every entry point raises.
 """
 from ._lib import HarrisError, build  # noqa: F401
 from .harris import (GROUPINGS, KAPPA, HarrisContext, algorithmic_bytes, context, grouping_hbm_bytes,  # noqa: F401
-                     harris, harris_grouping, harris_u8, stencil3x3_sep, synth_)
+                     harris, harris_frames, harris_grouping, harris_u8, stencil3x3_sep, synth_)
 
 __version__ = "0.1.0"

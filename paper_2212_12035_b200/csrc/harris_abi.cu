@@ -87,7 +87,7 @@ struct harris_ctx {
         harris::TileGeom tg;
         CUtensorMap tmap;
     };
-    static constexpr int kCacheSize = 8;
+    static constexpr int kCacheSize = 32;  // a frame ring (harris_run_frames) of up to 32 buffers
     std::mutex cache_mu;
     LaunchEntry cache[kCacheSize];
     int cache_next = 0;
@@ -272,6 +272,10 @@ int choose_path(const Call& c) {
     return ldg_eligible(c) ? HARRIS_PATH_LDG : HARRIS_PATH_GENERIC;
 }
 
+int pdl_mode(uint32_t flags) {
+    return (flags & HARRIS_FLAG_PDL_INDEPENDENT) ? 2 : (flags & HARRIS_FLAG_PDL) ? 1 : 0;
+}
+
 void plan_launch(const harris_ctx* ctx, const Call& c, TileGeom& tg, int64_t& grid) {
     const bool u8 = c.fmt == kU8Interleaved;
     const int fcfg = c.cfg >= 0 ? c.cfg : ctx->tma_cfg;
@@ -296,6 +300,7 @@ void plan_launch(const harris_ctx* ctx, const Call& c, TileGeom& tg, int64_t& gr
     tg.l2_policy = ctx->l2_policy;
     tg.vec_store = store_mode(c.g.out, c.g.out_pitch, c.g.batch, c.g.out_image_stride);
     tg.sync_waves = ctx->sync_waves;
+    tg.pdl = pdl_mode(c.flags);
 }
 
 // Short tiles (a small image fills the GPU with a few rows per warp): the pipeline ramp
@@ -728,6 +733,23 @@ int harris_run_strided(harris_ctx* ctx, float* out, int64_t out_pitch, int64_t o
                static_cast<cudaStream_t>(stream));
 }
 
+int harris_run_frames(harris_ctx* ctx, float* const* outs, int64_t out_pitch, int64_t n, int64_t m,
+                      const float* const* rgbs, int64_t in_pitch, int64_t in_chan_stride, int64_t frames,
+                      float kappa, uint32_t flags, void* stream) {
+    if (!ctx || !outs || !rgbs || frames < 1) return HARRIS_ERR_INVALID_ARGUMENT;
+    const uint32_t base = flags & ~(uint32_t(HARRIS_FLAG_PDL) | uint32_t(HARRIS_FLAG_PDL_INDEPENDENT));
+    for (int64_t k = 0; k < frames; ++k) {
+        const uint32_t pdl = k > 0 || (flags & HARRIS_FLAG_PDL_INDEPENDENT) ? HARRIS_FLAG_PDL_INDEPENDENT
+                                                                            : HARRIS_FLAG_PDL;
+        const int rc = run(ctx,
+                           make_call(outs[k], out_pitch, n * out_pitch, n, m, rgbs[k], in_pitch, in_chan_stride,
+                                     3 * in_chan_stride, 1, kappa, base | pdl),
+                           static_cast<cudaStream_t>(stream));
+        if (rc) return rc;
+    }
+    return HARRIS_OK;
+}
+
 int harris_run_notify(harris_ctx* ctx, float* out, int64_t out_pitch, int64_t out_image_stride, int64_t n,
                       int64_t m, const float* rgb, int64_t in_pitch, int64_t in_chan_stride, int64_t in_image_stride,
                       int64_t batch, float kappa, uint32_t flags, uint32_t* notify_flag, uint32_t epoch,
@@ -796,6 +818,7 @@ int harris_stencil3x3_sep(harris_ctx* ctx, float* out, int64_t out_pitch, int64_
         tg.l2_policy = ctx->l2_policy;
         tg.vec_store = store_mode(out, out_pitch, batch, out_image_stride);
         tg.sync_waves = ctx->sync_waves;
+        tg.pdl = pdl_mode(flags);
         if (tg.tiles > INT32_MAX) return HARRIS_ERR_SIZE;
         e = launch_sep_ldg(exact, in, in_pitch, img_stride, m + 2, n + 2, tg, grid, wv, wh, stream);
     } else if (tma) {
@@ -833,6 +856,7 @@ int harris_stencil3x3_sep(harris_ctx* ctx, float* out, int64_t out_pitch, int64_
         tg.l2_policy = ctx->l2_policy;
         tg.vec_store = out_vec;
         tg.sync_waves = ctx->sync_waves;
+        tg.pdl = pdl_mode(flags);
         if (tg.tiles > INT32_MAX) return HARRIS_ERR_SIZE;  // beyond the engine's 32-bit tile index
         CUtensorMap out_tmap;
         const bool ts = sep_config_tma_store(cfg);

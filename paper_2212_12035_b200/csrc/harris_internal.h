@@ -26,6 +26,8 @@ struct TileGeom {
     int32_t l2_policy;  // 0 evict_first, 1 evict_normal, 2 evict_last (default, harris_options)
     int32_t vec_store;  // 2: output rows 16-byte aligned (float4 stores); 1: 8-byte aligned (2 x float2); 0: scalar
     int32_t sync_waves; // 1: CTA barrier at every tile boundary (keeps neighbour strips in step)
+    int32_t pdl = 0;    // programmatic dependent launch: 0 off; 1 on (griddepcontrol.wait before the first
+                        // global access); 2 on, caller-declared independent of the previous stream work (no wait)
     int64_t tiles;
     int64_t out_pitch, out_image_stride;
     float* out;

@@ -530,7 +530,7 @@ static void launch_u8_ldg_one(const Geom& geom, const TileGeom& tg, int64_t grid
     const typename U8LdgOp<EXACT, kU8LdgCH, A>::Params p{geom.kappa, reinterpret_cast<const uint8_t*>(geom.rgb),
                                                          geom.in_pitch, img_stride, int32_t(geom.m + 4),
                                                          int32_t(geom.n + 4)};
-    u8_ldg_kernel<EXACT, A>()<<<unsigned(grid), unsigned(kU8LdgNW * 32), u8_ldg_smem(), stream>>>(unused, tg, p);
+    launch_strip(u8_ldg_kernel<EXACT, A>(), unsigned(grid), unsigned(kU8LdgNW * 32), u8_ldg_smem(), stream, tg.pdl, unused, tg, p);
 }
 
 template <bool EXACT>
@@ -544,7 +544,7 @@ static void launch_u8_bulk_one(const Geom& geom, const TileGeom& tg, int64_t gri
         constexpr bool S = decltype(strict)::value;
         const typename U8BulkOpT<EXACT, S>::Params p{geom.kappa, rgb, geom.in_pitch, img_stride, int32_t(geom.m + 4),
                                                      int32_t(geom.n + 4), limit};
-        u8_bulk_kernel<EXACT, S>()<<<unsigned(grid), unsigned(kU8BulkNW * 32), u8_bulk_smem(), stream>>>(unused, tg, p);
+        launch_strip(u8_bulk_kernel<EXACT, S>(), unsigned(grid), unsigned(kU8BulkNW * 32), u8_bulk_smem(), stream, tg.pdl, unused, tg, p);
     };
     // STRICT only when the 16-byte rounding could pass the view's end
     (reinterpret_cast<uintptr_t>(limit) & 15u) ? go(std::true_type{}) : go(std::false_type{});
@@ -650,8 +650,7 @@ static void launch_ldg_one(const Geom& geom, const TileGeom& tg, int64_t grid, c
         using Op = typename LdgCfg<CFG>::template Op<EXACT, S>;
         const typename Op::Params p{{geom.kappa}, geom.rgb, geom.in_pitch, geom.in_chan_stride, img_stride,
                                     int32_t(geom.m + 4), int32_t(geom.n + 4), limit, tg.l2_policy};
-        ldg_kernel<CFG, EXACT, S>()<<<unsigned(grid), unsigned(LdgCfg<CFG>::NW * 32), ldg_smem<CFG>(), stream>>>(
-            unused, tg, p);
+        launch_strip(ldg_kernel<CFG, EXACT, S>(), unsigned(grid), unsigned(LdgCfg<CFG>::NW * 32), ldg_smem<CFG>(), stream, tg.pdl, unused, tg, p);
     };
     (reinterpret_cast<uintptr_t>(limit) & 15u) ? go(std::true_type{}) : go(std::false_type{});
 }
@@ -768,7 +767,7 @@ static void launch_sep_ldg_one(const float* in, int64_t in_pitch, int64_t in_ima
         using Op = SepLdgOpT<EXACT, S>;
         const typename Op::Params p{{{wv[0], wv[1], wv[2]}, {wh[0], wh[1], wh[2]}}, in, in_pitch, 0, img_stride, W,
                                     H, limit};
-        sep_ldg_kernel<EXACT, S>()<<<unsigned(grid), unsigned(kSepLdgNW * 32), sep_ldg_smem(), stream>>>(unused, tg, p);
+        launch_strip(sep_ldg_kernel<EXACT, S>(), unsigned(grid), unsigned(kSepLdgNW * 32), sep_ldg_smem(), stream, tg.pdl, unused, tg, p);
     };
     (reinterpret_cast<uintptr_t>(limit) & 15u) ? go(std::true_type{}) : go(std::false_type{});
 }

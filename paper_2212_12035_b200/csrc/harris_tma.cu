@@ -121,10 +121,10 @@ static cudaError_t launch_one(bool exact, const CUtensorMap& tmap, const TileGeo
     const dim3 block{unsigned(C::NW * 32)}, gridd{unsigned(grid)};
     if (exact) {
         const typename F32OpOf<CFG, true>::Params p{tg.kappa};
-        f32_kernel<CFG, true>()<<<gridd, block, f32_smem<CFG>(), stream>>>(tmap, tg, p);
+        launch_strip(f32_kernel<CFG, true>(), gridd, block, f32_smem<CFG>(), stream, tg.pdl, tmap, tg, p);
     } else {
         const typename F32OpOf<CFG, false>::Params p{tg.kappa};
-        f32_kernel<CFG, false>()<<<gridd, block, f32_smem<CFG>(), stream>>>(tmap, tg, p);
+        launch_strip(f32_kernel<CFG, false>(), gridd, block, f32_smem<CFG>(), stream, tg.pdl, tmap, tg, p);
     }
     return cudaGetLastError();
 }
@@ -206,11 +206,10 @@ cudaError_t launch_tma_pair(bool exact, const CUtensorMap& tmap, const TileGeom&
                             cudaStream_t stream) {
     const dim3 block{unsigned(kPairNW * 32)}, gridd{unsigned(grid)};
     if (exact)
-        pair_kernel<true>()<<<gridd, block, pair_smem(), stream>>>(tmap, tg,
+        launch_strip(pair_kernel<true>(), gridd, block, pair_smem(), stream, tg.pdl, tmap, tg,
                                                                   typename HarrisF32PairRowOp<true>::Params{tg.kappa, pitch});
     else
-        pair_kernel<false>()<<<gridd, block, pair_smem(), stream>>>(
-            tmap, tg, typename HarrisF32PairRowOp<false>::Params{tg.kappa, pitch});
+        launch_strip(pair_kernel<false>(), gridd, block, pair_smem(), stream, tg.pdl, tmap, tg, typename HarrisF32PairRowOp<false>::Params{tg.kappa, pitch});
     return cudaGetLastError();
 }
 
@@ -244,11 +243,10 @@ cudaError_t launch_tma_quad(bool exact, const CUtensorMap& tmap, const TileGeom&
                             cudaStream_t stream) {
     const dim3 block{unsigned(kQuadNW * 32)}, gridd{unsigned(grid)};
     if (exact)
-        quad_kernel<true>()<<<gridd, block, quad_smem(), stream>>>(tmap, tg,
+        launch_strip(quad_kernel<true>(), gridd, block, quad_smem(), stream, tg.pdl, tmap, tg,
                                                                   typename HarrisF32QuadRowOp<true>::Params{tg.kappa, pitch});
     else
-        quad_kernel<false>()<<<gridd, block, quad_smem(), stream>>>(
-            tmap, tg, typename HarrisF32QuadRowOp<false>::Params{tg.kappa, pitch});
+        launch_strip(quad_kernel<false>(), gridd, block, quad_smem(), stream, tg.pdl, tmap, tg, typename HarrisF32QuadRowOp<false>::Params{tg.kappa, pitch});
     return cudaGetLastError();
 }
 

@@ -104,10 +104,10 @@ static cudaError_t u8_launch_one(bool exact, const CUtensorMap& tmap, const Tile
     const dim3 block{unsigned(C::NW * 32)}, gridd{unsigned(grid)};
     if (exact) {
         const typename U8OpOf<CFG, true>::Params p{tg.kappa};
-        u8_kernel<CFG, true>()<<<gridd, block, u8_smem<CFG>(), stream>>>(tmap, tg, p);
+        launch_strip(u8_kernel<CFG, true>(), gridd, block, u8_smem<CFG>(), stream, tg.pdl, tmap, tg, p);
     } else {
         const typename U8OpOf<CFG, false>::Params p{tg.kappa};
-        u8_kernel<CFG, false>()<<<gridd, block, u8_smem<CFG>(), stream>>>(tmap, tg, p);
+        launch_strip(u8_kernel<CFG, false>(), gridd, block, u8_smem<CFG>(), stream, tg.pdl, tmap, tg, p);
     }
     return cudaGetLastError();
 }
@@ -212,8 +212,7 @@ template <bool EXACT, int K>
 static void u8_group_launch_one(const CUtensorMap& tmap, const TileGeom& tg, int64_t grid, int32_t pitch_words,
                                 cudaStream_t stream) {
     const typename HarrisU8RowGroupOp<EXACT, K>::Params p{tg.kappa, pitch_words};
-    u8_group_kernel<EXACT, K>()<<<unsigned(grid), unsigned(U8GroupCfg<K>::NW * 32), u8_group_smem<K>(), stream>>>(
-        tmap, tg, p);
+    launch_strip(u8_group_kernel<EXACT, K>(), unsigned(grid), unsigned(U8GroupCfg<K>::NW * 32), u8_group_smem<K>(), stream, tg.pdl, tmap, tg, p);
 }
 
 cudaError_t launch_tma_u8_group(int k, bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid,

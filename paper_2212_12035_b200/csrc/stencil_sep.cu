@@ -134,10 +134,10 @@ static void sep_launch_order(const CUtensorMap& tmap, const CUtensorMap* out_tma
         typename Op::Params p;
         p.out = *out_tmap;
         p.base = base;
-        sep_kernel<CFG, EXACT>()<<<gridd, block, sep_smem<CFG>(), stream>>>(tmap, tg, p);
+        launch_strip(sep_kernel<CFG, EXACT>(), gridd, block, sep_smem<CFG>(), stream, tg.pdl, tmap, tg, p);
     } else {
         (void)out_tmap;
-        sep_kernel<CFG, EXACT>()<<<gridd, block, sep_smem<CFG>(), stream>>>(tmap, tg, base);
+        launch_strip(sep_kernel<CFG, EXACT>(), gridd, block, sep_smem<CFG>(), stream, tg.pdl, tmap, tg, base);
     }
 }
 

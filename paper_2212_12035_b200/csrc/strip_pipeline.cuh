@@ -245,6 +245,32 @@ __device__ __forceinline__ void notify_epilogue(const TileGeom& g) {
     }
 }
 
+// Host-side launch of a strip kernel, with programmatic dependent launch when pdl != 0
+// (cudaLaunchAttributeProgrammaticStreamSerialization): the kernel may start while the previous
+// kernel on the stream is still running; it releases its own dependents at entry
+// (griddepcontrol.launch_dependents) and, with pdl == 1, waits for the previous grid
+// (griddepcontrol.wait) before its first global-memory access.
+template <class Kern, class... Args>
+inline cudaError_t launch_strip(Kern kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t stream, int pdl,
+                                const Args&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = pdl ? attr : nullptr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 template <class Op, int NW, int NS, int MINB = 1>
 __global__ void __launch_bounds__(NW * 32, MINB)
     strip_kernel(const __grid_constant__ CUtensorMap tmap, const TileGeom g,
@@ -272,8 +298,18 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     const int64_t GW = int64_t(gridDim.x) * NW;
     const int64_t gw = int64_t(blockIdx.x) * NW + warp;
     const int64_t cta0 = int64_t(blockIdx.x) * NW;  // first warp-tile index of this CTA
+    // PDL (TileGeom::pdl).  Mode 2 (independent): release the next kernel at once — its CTAs
+    // take the SMs this grid leaves — and let CTA 0 wait for the PREVIOUS grid before exiting,
+    // so this grid still completes after everything before it (stream order for later work).
+    // Mode 1: wait for the previous grid before the first global access (below), then release.
+    if (g.pdl == 2) pdl_launch_dependents();
     if (cta0 >= g.tiles) {                          // whole CTA idle
+        if (g.pdl == 1) {
+            pdl_wait();
+            pdl_launch_dependents();
+        }
         notify_epilogue(g);
+        if (g.pdl == 2 && blockIdx.x == 0) pdl_wait();
         return;
     }
     // waves in which at least one warp of this CTA has a tile: every warp of the CTA runs
@@ -353,6 +389,12 @@ __global__ void __launch_bounds__(NW * 32, MINB)
             }
         }
     };
+    // PDL mode 1: the prologue above (barrier init, tensor-map prefetch, first tile decode)
+    // overlapped the previous kernel; memory is only touched after it completed
+    if (g.pdl == 1) {
+        pdl_wait();
+        pdl_launch_dependents();
+    }
 #pragma unroll
     for (int s = 0; s < NS; ++s) issue(s);
 
@@ -500,6 +542,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
         if (lane == 0) bulk_wait_all();  // every TMA store performed (and its staging read) before exit
     }
     notify_epilogue(g);
+    if (g.pdl == 2 && blockIdx.x == 0) pdl_wait();  // complete only after the previous grid
 }
 
 }  // namespace harris

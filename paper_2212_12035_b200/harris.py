@@ -143,9 +143,15 @@ def _stream_handle(dev: int, stream: Optional[torch.cuda.Stream]) -> int:
     return torch.cuda.current_stream(dev).cuda_stream
 
 
-def _flags(exact: bool, force_generic: bool, force_tma: bool) -> int:
+def _flags(exact: bool, force_generic: bool, force_tma: bool, pdl=False) -> int:
+    """pdl: False; True = HARRIS_FLAG_PDL (prologue overlaps the previous kernel, waits before
+    touching memory); "independent" = HARRIS_FLAG_PDL_INDEPENDENT (the caller guarantees the
+    still-running stream work neither writes this call's input nor touches its output)."""
+    if pdl not in (False, True, "independent"):
+        raise ValueError('pdl must be False, True or "independent"')
     return (FLAG_EXACT_ORDER if exact else 0) | (FLAG_FORCE_GENERIC if force_generic else 0) | (
-        FLAG_FORCE_TMA if force_tma else 0)
+        FLAG_FORCE_TMA if force_tma else 0) | (_lib.FLAG_PDL if pdl is True else 0) | (
+        _lib.FLAG_PDL_INDEPENDENT if pdl == "independent" else 0)
 
 
 def _check_rgb(rgb) -> tuple[int, int, int]:
@@ -168,7 +174,7 @@ def _check_rgb(rgb) -> tuple[int, int, int]:
 
 def harris(rgb, kappa: float = KAPPA, *, out: Optional[torch.Tensor] = None, exact: bool = False,
            force_generic: bool = False, force_tma: bool = False, stream: Optional[torch.cuda.Stream] = None,
-           ctx: Optional[HarrisContext] = None):
+           ctx: Optional[HarrisContext] = None, pdl=False):
     """Fused Harris coarsity of planar RGB f32.
 
     rgb: ``(3, H, W)`` or ``(B, 3, H, W)`` float32; CUDA tensor (device path,
@@ -176,9 +182,10 @@ def harris(rgb, kappa: float = KAPPA, *, out: Optional[torch.Tensor] = None, exa
     (host path through the device).  Returns ``(H-4, W-4)`` / ``(B, H-4, W-4)``.
     ``exact=True`` selects the Appendix-B op order (bit-identical to the C
     oracle); the default is the FMA/separable order, within the SURVEY.md §8(d)
-    tolerance of the f64 reference.
+    tolerance of the f64 reference.  ``pdl`` (device path): programmatic dependent launch for
+    back-to-back frame streams (see ``_flags``).
     """
-    flags = _flags(exact, force_generic, force_tma)
+    flags = _flags(exact, force_generic, force_tma, pdl)
     if isinstance(rgb, np.ndarray) or (isinstance(rgb, torch.Tensor) and not rgb.is_cuda):
         _check_rgb(rgb)
         arr = rgb if isinstance(rgb, np.ndarray) else rgb.numpy()
@@ -219,14 +226,56 @@ def harris(rgb, kappa: float = KAPPA, *, out: Optional[torch.Tensor] = None, exa
     return out
 
 
+def harris_frames(frames, outs=None, kappa: float = KAPPA, *, exact: bool = False, independent: bool = False,
+                  stream: Optional[torch.cuda.Stream] = None, ctx: Optional[HarrisContext] = None):
+    """A stream of independent single frames through ``harris_run_frames``: one launch per
+    frame, back to back, chained with programmatic dependent launch (frame 0 waits for earlier
+    stream work unless ``independent``).  ``frames``: sequence of (3, H, W) float32 CUDA tensors of
+    one shape and layout (unit column stride, same row pitch / channel stride); ``outs``: matching
+    (H-4, W-4) outputs (allocated when None), all distinct.  Returns ``outs``."""
+    frames = list(frames)
+    if not frames:
+        raise ValueError("no frames")
+    B, H, W = _check_rgb(frames[0])
+    f0 = frames[0]
+    if f0.dim() != 3 or not f0.is_cuda or f0.stride(-1) != 1:
+        raise ValueError("frames must be (3, H, W) CUDA tensors with unit column stride")
+    for f in frames:
+        if f.shape != f0.shape or f.stride() != f0.stride() or f.dtype != torch.float32 or f.device != f0.device:
+            raise ValueError("all frames must share shape, strides, dtype and device")
+    n, m = H - 4, W - 4
+    if outs is None:
+        outs = [torch.empty((n, m), dtype=torch.float32, device=f0.device) for _ in frames]
+    outs = list(outs)
+    if len(outs) != len(frames):
+        raise ValueError("one output per frame")
+    o0 = outs[0]
+    for o in outs:
+        if o.shape != (n, m) or o.dtype != torch.float32 or o.device != f0.device or o.stride() != o0.stride() or \
+                o.stride(-1) != 1:
+            raise ValueError("outputs must be float32 (H-4, W-4) tensors on the frames' device with one row pitch")
+    if len({o.data_ptr() for o in outs}) != len(outs):
+        raise ValueError("outputs must be distinct")
+    dev = f0.device.index if f0.device.index is not None else torch.cuda.current_device()
+    vp = ctypes.c_void_p
+    optrs = (vp * len(outs))(*[o.data_ptr() for o in outs])
+    iptrs = (vp * len(frames))(*[f.data_ptr() for f in frames])
+    flags = _flags(exact, False, False, "independent" if independent else False)
+    ctx = ctx or context(dev)
+    rc = lib().harris_run_frames(ctx.handle, optrs, o0.stride(0), n, m, iptrs, f0.stride(1), f0.stride(0), len(frames),
+                                 kappa, flags, _stream_handle(dev, stream))
+    check(rc, "harris_run_frames", ctx.handle)
+    return outs
+
+
 def harris_u8(rgb8, kappa: float = KAPPA, *, out: Optional[torch.Tensor] = None, exact: bool = False,
               force_generic: bool = False, force_tma: bool = False, stream: Optional[torch.cuda.Stream] = None,
-              ctx: Optional[HarrisContext] = None):
+              ctx: Optional[HarrisContext] = None, pdl=False):
     """Fused Harris on interleaved 8-bit RGB: ``(H, W, 3)`` or ``(B, H, W, 3)`` uint8
     (value/255), CUDA (device path) or CPU/numpy (host path through the device).
     Returns ``(H-4, W-4)`` / ``(B, H-4, W-4)`` float32, equal to ``harris`` on the planar
     image ``rgb8/255`` (bit-for-bit with ``exact=True``)."""
-    flags = _flags(exact, force_generic, force_tma)
+    flags = _flags(exact, force_generic, force_tma, pdl)
     shape = tuple(rgb8.shape)
     if rgb8.dtype not in (torch.uint8, np.uint8):
         raise TypeError("harris_u8 expects uint8 interleaved RGB")
@@ -278,7 +327,8 @@ BINOMIAL = (1.0, 2.0, 1.0)  # weightsV = weightsH of the reference (evalref.py:1
 
 def stencil3x3_sep(img: torch.Tensor, wv=BINOMIAL, wh=BINOMIAL, *, out: Optional[torch.Tensor] = None,
                    exact: bool = False, force_generic: bool = False, force_tma: bool = False,
-                   stream: Optional[torch.cuda.Stream] = None, ctx: Optional[HarrisContext] = None) -> torch.Tensor:
+                   stream: Optional[torch.cuda.Stream] = None, ctx: Optional[HarrisContext] = None,
+                   pdl=False) -> torch.Tensor:
     """Separable 3x3 stencil ``(H, W)`` / ``(B, H, W)`` float32 CUDA -> ``(H-2, W-2)`` /
     ``(B, H-2, W-2)``: vertical ``wv`` then horizontal ``wh`` (the separated form of the
     reference's binomial rewrite goal)."""
@@ -305,7 +355,7 @@ def stencil3x3_sep(img: torch.Tensor, wv=BINOMIAL, wh=BINOMIAL, *, out: Optional
     rc = lib().harris_stencil3x3_sep(ctx.handle, out.data_ptr(), out.stride(-2),
                                      out.stride(0) if batched else n * out.stride(-2), n, m, img.data_ptr(),
                                      img.stride(-2), img.stride(0) if batched else H * img.stride(-2), B,
-                                     fwv, fwh, _flags(exact, force_generic, force_tma), st.cuda_stream)
+                                     fwv, fwh, _flags(exact, force_generic, force_tma, pdl), st.cuda_stream)
     check(rc, "harris_stencil3x3_sep", ctx.handle)
     return out
 
@@ -384,5 +434,5 @@ def algorithmic_bytes(n: int, m: int, batch: int = 1) -> int:
     return batch * (12 * (n + 4) * (m + 4) + 4 * n * m)
 
 
-__all__ = ["HarrisContext", "context", "harris", "harris_u8", "stencil3x3_sep", "BINOMIAL", "harris_grouping", "grouping_hbm_bytes", "GROUPINGS", "synth_",
+__all__ = ["HarrisContext", "context", "harris", "harris_frames", "harris_u8", "stencil3x3_sep", "BINOMIAL", "harris_grouping", "grouping_hbm_bytes", "GROUPINGS", "synth_",
            "algorithmic_bytes", "KAPPA", "_lib"]

@@ -127,3 +127,63 @@ def test_host_pipeline_error_returns_after_drain(cuda_ctx):
     # the ctx is still usable
     got = hb.harris(rgb, exact=True)
     assert np.array_equal(np.asarray(got), cref.harris_f32(rgb))
+
+
+@pytest.mark.parametrize("pdl", [True, "independent"])
+def test_pdl_launches_bit_identical_and_stream_ordered(cuda_ctx, pdl):
+    """PDL launches (HARRIS_FLAG_PDL / _PDL_INDEPENDENT) give the same bits as plain launches on
+    every kernel path, and stream order holds for the work around them: a producer kernel
+    (synth_) right before a PDL-waiting launch, and a consumer (clone) right after a chain."""
+    shapes = [(70, 260), (70, 262), (72, 263), (71, 263), (1536, 2560)]
+    for H, W in shapes:
+        x = torch.empty((3, H, W), device="cuda")
+        ref_x = torch.from_numpy(synth.synth_numpy(3, H, W, seed=H * W)).cuda()
+        plain = hb.harris(ref_x)
+        for rep in range(3):
+            x.zero_()
+            torch.cuda.synchronize()
+            hb.synth_(x, seed=H * W)             # producer on the stream
+            y = hb.harris(x, pdl=True)           # waits for the producer (mode 1)
+            z = hb.harris(ref_x, pdl=pdl)        # independent of the previous launch
+            yc, zc = y.clone(), z.clone()        # consumers after the chain
+            torch.cuda.synchronize()
+            assert torch.equal(yc, plain), (H, W, rep)
+            assert torch.equal(zc, plain), (H, W, rep)
+    img = torch.from_numpy(synth.synth_numpy(1, 40, 132, seed=2)[0]).cuda()
+    assert torch.equal(hb.stencil3x3_sep(img, pdl=pdl), hb.stencil3x3_sep(img))
+    u8 = torch.randint(0, 256, (40, 70, 3), dtype=torch.uint8, device="cuda")
+    assert torch.equal(hb.harris_u8(u8, pdl=pdl), hb.harris_u8(u8))
+
+
+def test_harris_frames_ring(cuda_ctx):
+    """harris_run_frames: a ring of distinct frames, one launch each, chained with PDL; equal
+    to one harris() per frame, also when the ring is rewritten by a producer right before the
+    call and consumed right after it, and under CUDA-graph replay."""
+    H, W, K = 516, 900, 6
+    xs = [torch.empty((3, H, W), device="cuda") for _ in range(K)]
+    for it in range(3):
+        for i, x in enumerate(xs):
+            hb.synth_(x, seed=100 * it + i)
+        outs = hb.harris_frames(xs)
+        copies = [o.clone() for o in outs]
+        torch.cuda.synchronize()
+        for i, x in enumerate(xs):
+            assert torch.equal(copies[i], hb.harris(x)), (it, i)
+    # graph capture / replay of the ring
+    outs = [torch.empty((H - 4, W - 4), device="cuda") for _ in range(K)]
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        hb.harris_frames(xs, outs)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            hb.harris_frames(xs, outs)
+    for o in outs:
+        o.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    for i, x in enumerate(xs):
+        assert torch.equal(outs[i], hb.harris(x)), i
+    with pytest.raises(ValueError):
+        hb.harris_frames(xs, [outs[0]] * K)  # outputs must be distinct
