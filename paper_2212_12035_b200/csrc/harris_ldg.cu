@@ -103,14 +103,13 @@ struct LdgOp : BaseOp {
         int64_t in_pitch, in_plane_stride, in_image_stride;  // elements
         int32_t W, H;                                        // input columns / rows per image
         const void* limit;  // one past the view's last element (used by the bulk-copy ops)
-        int32_t l2_policy;  // unused here (F32BulkOp's Params shares this initializer)
     };
 
     __device__ __forceinline__ explicit LdgOp(const Params& p) : BaseOp(p.base) {}
 
     __device__ __forceinline__ static void load_warp(void* smem, const Params& p, uint64_t* bar,
                                                      const int (&col0)[G], int row0, const int (&image)[G],
-                                                     int lane) {
+                                                     int lane, uint64_t policy) {
         unsigned char* s = static_cast<unsigned char*>(smem);
 #pragma unroll
         for (int k = 0; k < G; ++k) {
@@ -132,14 +131,15 @@ struct LdgOp : BaseOp {
     }
 };
 
-// HINT: an L2 cache-policy hint like the TMA input loads (`which`: the ctx's l2_policy, 2 =
-// evict_last, whose halo sectors are re-read by the neighbouring strip): +2 % on memory-bound
+// HINT: an L2 cache-policy hint like the TMA input loads (`policy`: the kernel's createpolicy
+// value of the ctx's l2_policy, evict_last by default, whose halo sectors are re-read by the
+// neighbouring strip): +2 % on memory-bound
 // f32 planes, -1 % on the issue-bound u8 / stencil ops (the extra createpolicy), so only
 // F32BulkOp asks for it
 template <bool HINT = false>
-__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar, int which = 2) {
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy = 0) {
     if constexpr (HINT) {
-        const uint64_t policy = l2_policy(which);
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
             "%4;" ::"r"(smem_u32(smem)),
@@ -187,7 +187,7 @@ template <bool STRICT, bool HINT = false>
 __device__ __forceinline__ void bulk_stage_fill(unsigned char* dst, const void* src, uint32_t need, uint32_t cap,
                                                 const void* limit, uint64_t* bar, bool active,
                                                 bool stage_has_last_row, bool last_row, int lane,
-                                                int l2_which = 2) {
+                                                uint64_t policy = 0) {
     uint32_t nb = 0;
     const unsigned char* al = nullptr;
     if (active) {
@@ -203,7 +203,7 @@ __device__ __forceinline__ void bulk_stage_fill(unsigned char* dst, const void* 
     if constexpr (STRICT) __syncwarp();  // the tail's shared stores before lane 0's release
     if (lane == 0) mbar_arrive_expect_tx(bar, total);
     __syncwarp();
-    if (nb) bulk_g2s<HINT>(dst, al, nb, bar, l2_which);
+    if (nb) bulk_g2s<HINT>(dst, al, nb, bar, policy);
 }
 
 // ---- planar f32 through the bulk-copy engine (K1b): every (channel, row) of a stage is
@@ -230,7 +230,6 @@ struct F32BulkOp : std::conditional_t<G == 2, HarrisF32x2Op<EXACT, CH, 124>, Har
         int64_t in_pitch, in_plane_stride, in_image_stride;  // elements
         int32_t W, H;                                        // input columns / rows per image
         const void* limit;                                   // one past the view's last element
-        int32_t l2_policy;                                   // TileGeom::l2_policy of the ctx
     };
     uint32_t base_r, pitch_r, plane_r, image_r;  // float-index residues mod 4
     uint32_t sk[G][3];                           // current row's skew per strip and channel
@@ -253,7 +252,7 @@ struct F32BulkOp : std::conditional_t<G == 2, HarrisF32x2Op<EXACT, CH, 124>, Har
 
     __device__ __forceinline__ static void load_warp(void* smem, const Params& p, uint64_t* bar,
                                                      const int (&col0)[G], int row0, const int (&image)[G],
-                                                     int lane) {
+                                                     int lane, uint64_t policy) {
         const int k = lane >= 3 * CH ? 1 : 0, rem = lane - k * 3 * CH;
         const int ch = rem / CH, r = rem - ch * CH;
         const int y = row0 + r;
@@ -263,7 +262,7 @@ struct F32BulkOp : std::conditional_t<G == 2, HarrisF32x2Op<EXACT, CH, 124>, Har
         bulk_stage_fill<STRICT, true>(
             static_cast<unsigned char*>(smem) + k * kBoxStride + (ch * CH + r) * (kRowFloats * 4), src,
             uint32_t(p.W - c0) * 4u, kRowFloats * 4, p.limit, bar, lane < G * 3 * CH && y < p.H,
-            row0 + CH > p.H - 1 && row0 <= p.H - 1, y == p.H - 1, lane, p.l2_policy);
+            row0 + CH > p.H - 1 && row0 <= p.H - 1, y == p.H - 1, lane, policy);
     }
 
     // 4 floats at q + s (q 16-byte aligned, s warp-uniform in 0..3)
@@ -342,7 +341,7 @@ struct U8LdgOp : HarrisU8Op<EXACT, CH, 124> {
 
     __device__ __forceinline__ static void load_warp(void* smem, const Params& p, uint64_t* bar,
                                                      const int (&col0)[1], int row0, const int (&image)[1],
-                                                     int lane) {
+                                                     int lane, uint64_t policy) {
         uint32_t* s = static_cast<uint32_t*>(smem);
         const uint8_t* img = p.rgb + int64_t(image[0]) * p.in_image_stride + int64_t(col0[0]) * 3;
         const int avail_px = p.W - col0[0];
@@ -429,7 +428,7 @@ struct U8BulkOp : std::conditional_t<G == 2, HarrisU8x2Op<EXACT, CH, 124>, Harri
 
     __device__ __forceinline__ static void load_warp(void* smem, const Params& p, uint64_t* bar,
                                                      const int (&col0)[G], int row0, const int (&image)[G],
-                                                     int lane) {
+                                                     int lane, uint64_t policy) {
         const int k = lane >= CH ? 1 : 0, r = lane - k * CH;
         const int y = row0 + r;
         const int img = k ? image[G - 1] : image[0], c0 = k ? col0[G - 1] : col0[0];  // selects: no local array
@@ -649,7 +648,7 @@ static void launch_ldg_one(const Geom& geom, const TileGeom& tg, int64_t grid, c
         constexpr bool S = decltype(strict)::value;
         using Op = typename LdgCfg<CFG>::template Op<EXACT, S>;
         const typename Op::Params p{{geom.kappa}, geom.rgb, geom.in_pitch, geom.in_chan_stride, img_stride,
-                                    int32_t(geom.m + 4), int32_t(geom.n + 4), limit, tg.l2_policy};
+                                    int32_t(geom.m + 4), int32_t(geom.n + 4), limit};
         launch_strip(ldg_kernel<CFG, EXACT, S>(), unsigned(grid), unsigned(LdgCfg<CFG>::NW * 32), ldg_smem<CFG>(), stream, tg.pdl, unused, tg, p);
     };
     (reinterpret_cast<uintptr_t>(limit) & 15u) ? go(std::true_type{}) : go(std::false_type{});
@@ -704,7 +703,7 @@ struct SepBulkOp : Sep3x3Op<EXACT, CH> {
 
     __device__ __forceinline__ static void load_warp(void* smem, const Params& p, uint64_t* bar,
                                                      const int (&col0)[1], int row0, const int (&image)[1],
-                                                     int lane) {
+                                                     int lane, uint64_t policy) {
         const int y = row0 + lane;
         const float* src = p.src + int64_t(image[0]) * p.in_image_stride + int64_t(y) * p.in_pitch + col0[0];
         bulk_stage_fill<STRICT>(static_cast<unsigned char*>(smem) + lane * (kRowFloats * 4), src, uint32_t(p.W - col0[0]) * 4u,

@@ -92,7 +92,7 @@ __device__ __forceinline__ void static_for(F&& f, std::integer_sequence<int, Rs.
 }
 
 // Op::kWarpLoad is optional (default false): the stage is filled by all 32 lanes with
-// Op::load_warp(smem, params, bar, cols, row0, imgs, lane) (cp.async, for inputs TMA
+// Op::load_warp(smem, params, bar, cols, row0, imgs, lane, l2_policy) (cp.async, for inputs TMA
 // cannot describe) instead of one TMA issue by lane 0; the stage barrier then counts
 // 32 arrivals instead of an expect_tx byte count
 template <class Op, class = void>
@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     auto issue = [&](int s) {
         if (pt < g.tiles) {
             if constexpr (kWarpLoad) {
-                Op::load_warp(ring + s * Op::kStageBytes, p, &bars[s], pcols, prow0 + pc * CH, pimgs, lane);
+                Op::load_warp(ring + s * Op::kStageBytes, p, &bars[s], pcols, prow0 + pc * CH, pimgs, lane, policy);
             } else if (lane == 0) {
                 if constexpr (kCacheP) {
                     mbar_arrive_expect_tx(&bars[s], Op::kTxBytes);
