@@ -37,6 +37,12 @@ def lib() -> ctypes.CDLL:
         L.oracle_harris_f32.restype = ctypes.c_int
         L.oracle_harris_f64.argtypes = [vp, i64, i64, i64, vp, i64, i64, ctypes.c_double, ctypes.c_int]
         L.oracle_harris_f64.restype = ctypes.c_int
+        L.oracle_harris_f32_window.argtypes = [vp, i64, i64, i64, vp, i64, i64, ctypes.c_float, ctypes.c_int,
+                                                ctypes.c_int]
+        L.oracle_harris_f32_window.restype = ctypes.c_int
+        L.oracle_harris_f64_window.argtypes = [vp, i64, i64, i64, vp, i64, i64, ctypes.c_double, ctypes.c_int,
+                                                ctypes.c_int]
+        L.oracle_harris_f64_window.restype = ctypes.c_int
         L.oracle_harris_f32_batched.argtypes = [vp, i64, i64, vp, i64, ctypes.c_float, ctypes.c_int]
         L.oracle_harris_f32_batched.restype = ctypes.c_int
         L.oracle_harris_f32_rrot.argtypes = [vp, i64, i64, i64, vp, i64, i64, ctypes.c_float, ctypes.c_int]
@@ -69,12 +75,17 @@ def _check_rgb(rgb: np.ndarray) -> tuple[int, int]:
     return H, W
 
 
-def harris_f32(rgb: np.ndarray, kappa: float = 0.04, nthreads: int = 0) -> np.ndarray:
-    """f32 Appendix-B restatement. ``rgb``: (3, H, W) float32 -> (H-4, W-4) f32."""
+WINDOWS = {"box": 0, "binomial": 1}
+
+
+def harris_f32(rgb: np.ndarray, kappa: float = 0.04, nthreads: int = 0, window: str = "box") -> np.ndarray:
+    """f32 Appendix-B restatement. ``rgb``: (3, H, W) float32 -> (H-4, W-4) f32.
+    ``window``: "box" (the thesis's 3x3 '+') or "binomial" (weights2d)."""
     rgb = np.ascontiguousarray(rgb)
     H, W = _check_rgb(rgb)
     out = np.empty((H - 4, W - 4), dtype=np.float32)
-    rc = lib().oracle_harris_f32(_ptr(out), W - 4, H - 4, W - 4, _ptr(rgb), W, H * W, kappa, nthreads)
+    rc = lib().oracle_harris_f32_window(_ptr(out), W - 4, H - 4, W - 4, _ptr(rgb), W, H * W, kappa, nthreads,
+                                        WINDOWS[window])
     if rc:
         raise RuntimeError(f"oracle_harris_f32 failed ({rc})")
     return out
@@ -91,12 +102,13 @@ def harris_f32_rrot(rgb: np.ndarray, kappa: float = 0.04, nthreads: int = 0) -> 
     return out
 
 
-def harris_f64(rgb: np.ndarray, kappa: float = 0.04, nthreads: int = 0) -> np.ndarray:
+def harris_f64(rgb: np.ndarray, kappa: float = 0.04, nthreads: int = 0, window: str = "box") -> np.ndarray:
     """f64 restatement in sges evaluation order, from the f32 input."""
     rgb = np.ascontiguousarray(rgb)
     H, W = _check_rgb(rgb)
     out = np.empty((H - 4, W - 4), dtype=np.float64)
-    rc = lib().oracle_harris_f64(_ptr(out), W - 4, H - 4, W - 4, _ptr(rgb), W, H * W, kappa, nthreads)
+    rc = lib().oracle_harris_f64_window(_ptr(out), W - 4, H - 4, W - 4, _ptr(rgb), W, H * W, kappa, nthreads,
+                                        WINDOWS[window])
     if rc:
         raise RuntimeError(f"oracle_harris_f64 failed ({rc})")
     return out

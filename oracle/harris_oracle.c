@@ -123,6 +123,17 @@ static void products_line_f32(float* pxx, float* pxy, float* pyy, const float* i
     }
 }
 
+/* the reference's binomial window weights2d = [[1,2,1],[2,4,2],[1,2,1]] (evalref.py:114-115),
+ * the "binomial filter instead of the 3x3 '+' convolution" Harris variant:
+ * S = dot(join weights2d, join window) = row-major sum from 0 of w*p (w*p exact in f32) */
+static inline float wsum9_f32(const float* a, const float* b, const float* c, int64_t x) {
+    float s = 0.0f;
+    s = s + 1.0f * a[x]; s = s + 2.0f * a[x + 1]; s = s + 1.0f * a[x + 2];
+    s = s + 2.0f * b[x]; s = s + 4.0f * b[x + 1]; s = s + 2.0f * b[x + 2];
+    s = s + 1.0f * c[x]; s = s + 2.0f * c[x + 1]; s = s + 1.0f * c[x + 2];
+    return s;
+}
+
 static inline float sum9_f32(const float* a, const float* b, const float* c, int64_t x) {
     float s = 0.0f;
     s = s + a[x]; s = s + a[x + 1]; s = s + a[x + 2];
@@ -131,9 +142,12 @@ static inline float sum9_f32(const float* a, const float* b, const float* c, int
     return s;
 }
 
+int oracle_harris_f32_window(float* out, int64_t out_pitch, int64_t n, int64_t m, const float* rgb,
+                             int64_t in_pitch, int64_t chan_stride, float kappa, int nthreads, int window);
+
 /* one 32-row strip of the cbuf schedule; buf: 3W + 15Ws floats of per-thread line buffers */
-static void cbuf_strip_f32(float* buf, float* out, int64_t out_pitch, int64_t n, int64_t m, const float* rgb,
-                           int64_t in_pitch, int64_t chan_stride, float kappa, int64_t s) {
+static void cbuf_strip_f32_w(float* buf, float* out, int64_t out_pitch, int64_t n, int64_t m, const float* rgb,
+                             int64_t in_pitch, int64_t chan_stride, float kappa, int64_t s, int window) {
     const int64_t W = m + 4, Ws = m + 2;
     float* gl[3] = {buf, buf + W, buf + 2 * W};
     float* sb = buf + 3 * W;
@@ -164,9 +178,9 @@ static void cbuf_strip_f32(float* buf, float* out, int64_t out_pitch, int64_t n,
             int a = (int)(y % 3), b = (int)((y + 1) % 3), c = (int)((y + 2) % 3);
             float* o = out + y * out_pitch;
             for (int64_t x = 0; x < m; ++x) {
-                float sxx = sum9_f32(pxx[a], pxx[b], pxx[c], x);
-                float sxy = sum9_f32(pxy[a], pxy[b], pxy[c], x);
-                float syy = sum9_f32(pyy[a], pyy[b], pyy[c], x);
+                float sxx = window ? wsum9_f32(pxx[a], pxx[b], pxx[c], x) : sum9_f32(pxx[a], pxx[b], pxx[c], x);
+                float sxy = window ? wsum9_f32(pxy[a], pxy[b], pxy[c], x) : sum9_f32(pxy[a], pxy[b], pxy[c], x);
+                float syy = window ? wsum9_f32(pyy[a], pyy[b], pyy[c], x) : sum9_f32(pyy[a], pyy[b], pyy[c], x);
                 float det = sxx * syy - sxy * sxy;
                 float tr = sxx + syy;
                 o[x] = det - kappa * tr * tr;          /* PAPER.md:4730 */
@@ -175,11 +189,23 @@ static void cbuf_strip_f32(float* buf, float* out, int64_t out_pitch, int64_t n,
     }
 }
 
+static void cbuf_strip_f32(float* buf, float* out, int64_t out_pitch, int64_t n, int64_t m, const float* rgb,
+                           int64_t in_pitch, int64_t chan_stride, float kappa, int64_t s) {
+    cbuf_strip_f32_w(buf, out, out_pitch, n, m, rgb, in_pitch, chan_stride, kappa, s, 0);
+}
+
 #define CBUF_BUF_FLOATS(W, Ws) ((size_t)(3 * (W) + 15 * (Ws)))
 
 int oracle_harris_f32(float* out, int64_t out_pitch, int64_t n, int64_t m,
                       const float* rgb, int64_t in_pitch, int64_t chan_stride,
                       float kappa, int nthreads) {
+    return oracle_harris_f32_window(out, out_pitch, n, m, rgb, in_pitch, chan_stride, kappa, nthreads, 0);
+}
+
+/* window 0: the 3x3 '+' box sums (Appendix B); 1: the reference's binomial window */
+int oracle_harris_f32_window(float* out, int64_t out_pitch, int64_t n, int64_t m,
+                             const float* rgb, int64_t in_pitch, int64_t chan_stride,
+                             float kappa, int nthreads, int window) {
     if (n < 1 || m < 1 || !out || !rgb || out_pitch < m || in_pitch < m + 4) return -1;
     const int64_t W = m + 4, Ws = m + 2;
     const int64_t nstrips = (n + STRIP - 1) / STRIP;
@@ -199,7 +225,7 @@ int oracle_harris_f32(float* out, int64_t out_pitch, int64_t n, int64_t m,
         }
 #pragma omp for schedule(dynamic, 1)
         for (int64_t s = 0; s < nstrips; ++s)
-            if (buf) cbuf_strip_f32(buf, out, out_pitch, n, m, rgb, in_pitch, chan_stride, kappa, s);
+            if (buf) cbuf_strip_f32_w(buf, out, out_pitch, n, m, rgb, in_pitch, chan_stride, kappa, s, window);
         free(buf);
     }
     return err;
@@ -235,9 +261,22 @@ static const double DGR = 0.299, DGG = 0.587, DGB = 0.114;
 #define DA (1.0 / 12.0)
 #define DB (2.0 / 12.0)
 
+int oracle_harris_f64_window(double* out, int64_t out_pitch, int64_t n, int64_t m,
+                             const float* rgb, int64_t in_pitch, int64_t chan_stride,
+                             double kappa, int nthreads, int window);
+
 int oracle_harris_f64(double* out, int64_t out_pitch, int64_t n, int64_t m,
                       const float* rgb, int64_t in_pitch, int64_t chan_stride,
                       double kappa, int nthreads) {
+    return oracle_harris_f64_window(out, out_pitch, n, m, rgb, in_pitch, chan_stride, kappa, nthreads, 0);
+}
+
+/* window 0: `+3x3` = map (map (reduce add 0)) over the 3x3 neighbourhood (a left fold from 0);
+ * window 1: the binomial window = dot (join weights2d) (evalref.py:110-111, 114-115): Python
+ * sum of w*p in row-major order, i.e. py_sum (Neumaier-compensated, Python >= 3.12) */
+int oracle_harris_f64_window(double* out, int64_t out_pitch, int64_t n, int64_t m,
+                             const float* rgb, int64_t in_pitch, int64_t chan_stride,
+                             double kappa, int nthreads, int window) {
     if (n < 1 || m < 1 || !out || !rgb || out_pitch < m || in_pitch < m + 4) return -1;
     const int64_t W = m + 4, Ws = m + 2;
     const int64_t nstrips = (n + STRIP - 1) / STRIP;
@@ -302,15 +341,29 @@ int oracle_harris_f64(double* out, int64_t out_pitch, int64_t n, int64_t m,
                     int64_t y = r - 4;
                     int a = (int)(y % 3), b = (int)((y + 1) % 3), c = (int)((y + 2) % 3);
                     double* o = out + y * out_pitch;
+                    static const double w2d[9] = {1.0, 2.0, 1.0, 2.0, 4.0, 2.0, 1.0, 2.0, 1.0};
                     for (int64_t x = 0; x < m; ++x) {
                         double sxx = 0.0, sxy = 0.0, syy = 0.0;
                         const int rr[3] = {a, b, c};
-                        for (int i = 0; i < 3; ++i)
-                            for (int j = 0; j < 3; ++j) {
-                                sxx = sxx + pxx[rr[i]][x + j];
-                                sxy = sxy + pxy[rr[i]][x + j];
-                                syy = syy + pyy[rr[i]][x + j];
-                            }
+                        if (window) {
+                            double vxx[9], vxy[9], vyy[9];
+                            for (int i = 0; i < 3; ++i)
+                                for (int j = 0; j < 3; ++j) {
+                                    vxx[3 * i + j] = w2d[3 * i + j] * pxx[rr[i]][x + j];
+                                    vxy[3 * i + j] = w2d[3 * i + j] * pxy[rr[i]][x + j];
+                                    vyy[3 * i + j] = w2d[3 * i + j] * pyy[rr[i]][x + j];
+                                }
+                            sxx = py_sum(vxx, 9);
+                            sxy = py_sum(vxy, 9);
+                            syy = py_sum(vyy, 9);
+                        } else {
+                            for (int i = 0; i < 3; ++i)
+                                for (int j = 0; j < 3; ++j) {
+                                    sxx = sxx + pxx[rr[i]][x + j];
+                                    sxy = sxy + pxy[rr[i]][x + j];
+                                    syy = syy + pyy[rr[i]][x + j];
+                                }
+                        }
                         double det = sxx * syy + (-1.0) * (sxy * sxy);
                         double tr = sxx + syy;
                         o[x] = det + (-1.0) * ((kappa * tr) * tr);

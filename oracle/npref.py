@@ -12,7 +12,7 @@ from __future__ import annotations
 import numpy as np
 
 
-def harris_np(rgb: np.ndarray, kappa: float = 0.04, dtype=np.float32) -> np.ndarray:
+def harris_np(rgb: np.ndarray, kappa: float = 0.04, dtype=np.float32, window: str = "box") -> np.ndarray:
     rgb = np.asarray(rgb, dtype=np.float32)
     if rgb.ndim != 3 or rgb.shape[0] != 3 or rgb.shape[1] < 5 or rgb.shape[2] < 5:
         raise ValueError("rgb must be (3, H>=5, W>=5)")
@@ -41,11 +41,18 @@ def harris_np(rgb: np.ndarray, kappa: float = 0.04, dtype=np.float32) -> np.ndar
     Sxx = np.zeros((n, m), dtype=dtype)
     Sxy = np.zeros((n, m), dtype=dtype)
     Syy = np.zeros((n, m), dtype=dtype)
+    w2d = ((1, 2, 1), (2, 4, 2), (1, 2, 1))  # binomial window (evalref.py:114-115)
     for i in range(3):
         for j in range(3):
-            Sxx = Sxx + Ixx[i:i + n, j:j + m]
-            Sxy = Sxy + Ixy[i:i + n, j:j + m]
-            Syy = Syy + Iyy[i:i + n, j:j + m]
+            if window == "binomial":  # row-major w*p accumulation from 0 (f32: w*p is exact)
+                w = f(w2d[i][j])
+                Sxx = Sxx + w * Ixx[i:i + n, j:j + m]
+                Sxy = Sxy + w * Ixy[i:i + n, j:j + m]
+                Syy = Syy + w * Iyy[i:i + n, j:j + m]
+            else:
+                Sxx = Sxx + Ixx[i:i + n, j:j + m]
+                Sxy = Sxy + Ixy[i:i + n, j:j + m]
+                Syy = Syy + Iyy[i:i + n, j:j + m]
     k = f(kappa)
     det = Sxx * Syy - Sxy * Sxy
     tr = Sxx + Syy

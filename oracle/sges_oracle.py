@@ -89,11 +89,20 @@ def _sum3(i: str) -> str:
     return f"(map (map (reduce add 0)) {_nbh(i)})"
 
 
-def harris_source() -> str:
+def _binom3(i: str) -> str:
+    """the reference's binomial stencil (its `binomial` goal's initial form, evalref weights2d)"""
+    return f"(map (map (dot (join weights2d))) {_nbh(i)})"
+
+
+def harris_source(window: str = "box") -> str:
+    """The thesis Harris term; window "binomial" replaces the 3x3 '+' box sums by the binomial
+    filter, the variant PAPER.md:3937-3938 names ("sometimes used as part of the Harris corner
+    detection instead of the 3x3 '+' convolution")."""
     IX, IY = (f"(map (map (dot (join {w}))) {_nbh(GRAY)})" for w in ("wsx", "wsy"))
     coars = (r"(\p. (\a. (\b. (\c. (\det. (\tr. add det (mul neg1 (mul (mul 0.04 tr) tr)))"
              r" (add a c)) (add (mul a c) (mul neg1 (mul b b)))) (snd (snd p))) (fst (snd p))) (fst p))")
-    return f"map (map {coars}) {_zip2(_sum3(_mul2(IX, IX)), _zip2(_sum3(_mul2(IX, IY)), _sum3(_mul2(IY, IY))))}"
+    win = {"box": _sum3, "binomial": _binom3}[window]
+    return f"map (map {coars}) {_zip2(win(_mul2(IX, IX)), _zip2(win(_mul2(IX, IY)), win(_mul2(IY, IY))))}"
 
 
 WEIGHTS = {
@@ -104,18 +113,18 @@ WEIGHTS = {
 }
 
 
-def typed_term():
+def typed_term(window: str = "box"):
     """Parse and type the Harris term; returns (term, type_string)."""
     parser, types, nat, infer, _ = _sges()
     n, m = nat.var("n"), nat.var("m")
     env = {"rgb": _arr(types, nat, 3, nat.add(n, nat.const(4)), nat.add(m, nat.const(4))),
            "wgray": _arr(types, nat, 3), "wsx": _arr(types, nat, 3, 3),
            "wsy": _arr(types, nat, 3, 3), "neg1": types.data(types.scalar())}
-    term = infer.from_named(parser.parse_term(harris_source()), env=env, sizes={"n", "m"})
+    term = infer.from_named(parser.parse_term(harris_source(window)), env=env, sizes={"n", "m"})
     return term, types.show(term.ty) if hasattr(types, "show") else str(term.ty)
 
 
-def harris_sges(rgb: np.ndarray) -> np.ndarray:
+def harris_sges(rgb: np.ndarray, window: str = "box") -> np.ndarray:
     """Evaluate the thesis Harris program with the reference evaluator (f64).
 
     ``rgb``: float32 (3, H, W); the f32 values are passed exactly (as Python
@@ -125,7 +134,7 @@ def harris_sges(rgb: np.ndarray) -> np.ndarray:
     if H < 5 or W < 5:
         raise ValueError("H, W must be >= 5")
     _, _, _, _, evalref = _sges()
-    term, _ = typed_term()
+    term, _ = typed_term(window)
     amb = dict(WEIGHTS)
     amb["rgb"] = rgb.astype(np.float64).tolist()
     out = evalref.eval_term(term, (), amb, {"n": H - 4, "m": W - 4})

@@ -183,3 +183,38 @@ def test_opencv_composition_meets_tolerance(oracle_lib):
         x = cref.synth(3, H, W, seed=seed)
         ok, m = synth.within_tolerance(opencv_ref.harris_opencv(x), cref.harris_f64(x))
         assert ok, m
+
+
+# ---- Harris with the binomial window, pinned to the reference evaluator
+def _binwin_golden():
+    import json
+    import os
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    meta = json.load(open(os.path.join(here, "harris_binwin_golden.json")))
+    return meta, dict(np.load(os.path.join(here, "harris_binwin_golden.npz")))
+
+
+def test_binomial_window_f64_bitexact_vs_reference_goldens(oracle_lib):
+    meta, arrays = _binwin_golden()
+    assert len(meta["cases"]) >= 9 and "weights2d" in meta["term"]
+    for case in meta["cases"]:
+        rgb = synth.synth_numpy(3, case["H"], case["W"], seed=case["seed"], dist=case["dist"])
+        assert hashlib.sha256(rgb.tobytes()).hexdigest() == case["input_sha256"]
+        out = cref.harris_f64(rgb, window="binomial")
+        assert np.array_equal(out, arrays[case["name"]]), case["name"]
+        assert hashlib.sha256(out.tobytes()).hexdigest() == case["output_sha256"]
+        # the f32 restatement (the GPU's EXACT order) within the §8(d) tolerance, and equal to
+        # the independent numpy restatement bit for bit
+        f32 = cref.harris_f32(rgb, window="binomial")
+        ok, m = synth.within_tolerance(f32, out)
+        assert ok, (case["name"], m)
+        assert np.array_equal(f32, npref.harris_np(rgb, dtype=np.float32, window="binomial")), case["name"]
+    # the window changes the result (not the box sums under another name)
+    rgb = synth.synth_numpy(3, 20, 30, seed=1)
+    assert not np.allclose(cref.harris_f64(rgb, window="binomial"), cref.harris_f64(rgb))
+
+
+@needs_ref
+def test_binomial_window_live_reference(oracle_lib):
+    rgb = synth.synth_numpy(3, 11, 19, seed=404, dist=2)
+    assert np.array_equal(sges_oracle.harris_sges(rgb, "binomial"), cref.harris_f64(rgb, window="binomial"))
