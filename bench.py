@@ -744,6 +744,22 @@ def run_extra(a, ctx, dev) -> dict:
 
     # other input formats / stencils on the same engine, batch of 1024 x 1080x1920 (inputs >> L2)
     B, H, W = 1024, 1080, 1920
+    # Harris with the binomial window (HARRIS_FLAG_BINOMIAL_WINDOW)
+    xw = torch.empty((B, 3, H, W), device=dev)
+    hb.synth_(xw.view(B * 3, H, W), seed=SEED)
+    ow = torch.empty((B, H - 4, W - 4), device=dev)
+    for _ in range(3):
+        hb.harris(xw, out=ow, window="binomial")
+    torch.cuda.synchronize()
+    ts = sorted(time_launches(lambda: hb.harris(xw, out=ow, window="binomial"), 10))
+    med = ts[len(ts) // 2]
+    nbytes = hb.algorithmic_bytes(H - 4, W - 4, B)
+    res["batch_binomial_window"] = {"workload": "configs[4] batch, Harris with the binomial window in place of the "
+                                                "3x3 box sums", "ms_median_of_10": med,
+                                    "value": B * (H - 4) * (W - 4) / (med * 1e-3) / 1e6, "unit": "MP/s",
+                                    "frac_of_measured_hbm": nbytes / (med * 1e-3) / 1e9 / peak}
+    del xw, ow
+    torch.cuda.empty_cache()
     g = torch.Generator(device=dev)
     g.manual_seed(SEED)
     x8 = torch.randint(0, 256, (B, H, W, 3), dtype=torch.uint8, device=dev, generator=g)

@@ -76,6 +76,16 @@ extern "C" {
                                            completes only after the previous kernel, so later
                                            stream work sees stream order. */
 
+#define HARRIS_FLAG_BINOMIAL_WINDOW 0x20u /* Harris with the reference's binomial window
+                                           weights2d = [1,2,1]^T [1,2,1] in place of the 3x3 '+'
+                                           box sums ("sometimes used as part of the Harris corner
+                                           detection instead of the 3x3 '+' convolution",
+                                           PAPER.md:3937-3938; weights at evalref.py:114-115).
+                                           Planar f32 with TMA-describable layouts runs the fused
+                                           TMA kernel; every other layout / u8 the generic kernel.
+                                           EXACT order: row-major sum of w*p from 0 (oracle
+                                           oracle_harris_f32_window). */
+
 /* which kernel the last harris_run* on a ctx launched */
 #define HARRIS_PATH_NONE    0
 #define HARRIS_PATH_TMA     1  /* K1: TMA-staged warp-strip kernel (W%4==0, aligned) */

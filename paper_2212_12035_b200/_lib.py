@@ -30,6 +30,7 @@ FLAG_FORCE_GENERIC = 0x2
 FLAG_FORCE_TMA = 0x4
 FLAG_PDL = 0x8
 FLAG_PDL_INDEPENDENT = 0x10
+FLAG_BINOMIAL_WINDOW = 0x20
 
 PATH_NONE, PATH_TMA, PATH_GENERIC, PATH_LDG, PATH_PAIR, PATH_QUAD = 0, 1, 2, 3, 4, 5
 

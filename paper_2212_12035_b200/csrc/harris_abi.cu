@@ -58,6 +58,7 @@ struct harris_ctx {
     int64_t force_band_rows = 0;  // dev knob (HARRIS_BAND_ROWS): override the planner
     CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;  // dev knob HARRIS_L2_PROMO
     int occ[kNumTmaConfigs] = {0};
+    int occ_win[2] = {0, 0};  // binomial-window kernels of TMA configs 0 and 6
     PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     std::atomic<int> last_path{HARRIS_PATH_NONE};  // diagnostic; calls may race on different streams
     char last_err[256] = {0};
@@ -267,6 +268,9 @@ bool pair_eligible(const Call& c) { return row_group(c) != 0; }
 
 int choose_path(const Call& c) {
     if (c.flags & HARRIS_FLAG_FORCE_GENERIC) return HARRIS_PATH_GENERIC;
+    // binomial window: the planar-f32 TMA kernels (configs 0 / 6) or the generic kernel
+    if (c.flags & HARRIS_FLAG_BINOMIAL_WINDOW)
+        return c.fmt == kF32Planar && tma_eligible(c) ? HARRIS_PATH_TMA : HARRIS_PATH_GENERIC;
     if (tma_eligible(c)) return HARRIS_PATH_TMA;
     if (const int k = row_group(c)) return k == 2 ? HARRIS_PATH_PAIR : HARRIS_PATH_QUAD;
     return ldg_eligible(c) ? HARRIS_PATH_LDG : HARRIS_PATH_GENERIC;
@@ -288,6 +292,7 @@ void plan_launch(const harris_ctx* ctx, const Call& c, TileGeom& tg, int64_t& gr
                                                 : (c.group == 4 ? ctx->occ_quad : ctx->occ_pair))
                                 : c.ldg ? (u8 ? (ctx->u8ldg_chunk ? ctx->occ_u8ldg : ctx->occ_u8bulk) : ctx->occ_ldg[ctx->ldg_cfg])
                                 : u8    ? ctx->occ_u8[ctx->u8_cfg]
+                                : c.g.window ? ctx->occ_win[fcfg == 6 ? 1 : 0]
                                         : ctx->occ[fcfg]);
     const int64_t resident_ctas = int64_t(ctx->num_sms) * occ;
     plan_tiles(c.g.n, c.g.m, c.g.batch, resident_ctas * cfg.warps, cfg.rows, ctx->force_band_rows, tg, 4,
@@ -464,6 +469,7 @@ int run(harris_ctx* ctx, const Call& c, cudaStream_t stream) {
             cc.group = group;
             if (!ldg) {
                 cc.cfg = pair ? 0 : resolve_cfg(ctx, c);
+                if (c.g.window && !tma_window_config(cc.cfg)) cc.cfg = kTmaConfigs[cc.cfg].groups == 2 ? 6 : 0;
                 rc = encode_tmap(ctx, cc, &ent.tmap);
                 if (rc) return rc;
             }
@@ -485,6 +491,7 @@ int run(harris_ctx* ctx, const Call& c, cudaStream_t stream) {
             : ldg ? (c.fmt == kU8Interleaved ? launch_u8_ldg(exact, ctx->u8ldg_chunk, c.g, tg, ent.grid, stream)
                                              : launch_ldg(ctx->ldg_cfg, exact, c.g, tg, ent.grid, stream))
             : c.fmt == kU8Interleaved ? launch_tma_u8(ctx->u8_cfg, exact, ent.tmap, tg, ent.grid, stream)
+            : c.g.window              ? launch_tma_window(ent.cfg, exact, ent.tmap, tg, ent.grid, stream)
                                       : launch_tma(ent.cfg, exact, ent.tmap, tg, ent.grid, stream);
     } else {
         e = c.fmt == kU8Interleaved ? launch_generic_u8(exact, c.g, stream) : launch_generic(exact, c.g, stream);
@@ -515,6 +522,7 @@ Call make_call(float* out, int64_t out_pitch, int64_t out_image_stride, int64_t 
     c.g.out_pitch = out_pitch;
     c.g.out_image_stride = out_image_stride;
     c.g.kappa = kappa;
+    c.g.window = (flags & HARRIS_FLAG_BINOMIAL_WINDOW) ? 1 : 0;
     c.flags = flags;
     return c;
 }
@@ -654,7 +662,10 @@ int harris_init_ex(harris_ctx** out_ctx, int cuda_device, const harris_options* 
             return rc;
         }
     }
-    e = pair_configure(&ctx->occ_pair);
+    if (e == cudaSuccess) e = tma_window_configure();
+    if (e == cudaSuccess) e = tma_window_occupancy(0, &ctx->occ_win[0]);
+    if (e == cudaSuccess) e = tma_window_occupancy(6, &ctx->occ_win[1]);
+    e = e == cudaSuccess ? pair_configure(&ctx->occ_pair) : e;
     if (e == cudaSuccess) e = quad_configure(&ctx->occ_quad);
     if (e == cudaSuccess) e = sep_ldg_configure(&ctx->occ_sepldg);
     if (e == cudaSuccess) e = u8_ldg_configure(&ctx->occ_u8ldg, &ctx->occ_u8bulk);

@@ -36,6 +36,7 @@ __global__ void __launch_bounds__(kGThreadsX* kGThreadsY)
     const int64_t tiles = int64_t(tiles_x) * tiles_y;
     const float WX[9] = {-kSobA, 0.f, kSobA, -kSobB, 0.f, kSobB, -kSobA, 0.f, kSobA};
     const float WY[9] = {-kSobA, -kSobB, -kSobA, 0.f, 0.f, 0.f, kSobA, kSobB, kSobA};
+    const float W2D[9] = {1.f, 2.f, 1.f, 2.f, 4.f, 2.f, 1.f, 2.f, 1.f};
 
     for (int64_t b = blockIdx.z; b < g.batch; b += gridDim.z) {
         const float* img = U8 ? g.rgb : g.rgb + b * g.in_image_stride;
@@ -102,13 +103,26 @@ __global__ void __launch_bounds__(kGThreadsX* kGThreadsY)
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
                     float(*p)[kGS + 1] = pp[q];
-                    if (EXACT)
+                    if (g.window) {  // binomial window (HARRIS_FLAG_BINOMIAL_WINDOW)
+                        if (EXACT) {
+                            s[q] = conv9_exact(W2D, p[yy][xx], p[yy][xx + 1], p[yy][xx + 2], p[yy + 1][xx],
+                                               p[yy + 1][xx + 1], p[yy + 1][xx + 2], p[yy + 2][xx], p[yy + 2][xx + 1],
+                                               p[yy + 2][xx + 2]);
+                        } else {
+                            float c[3];
+#pragma unroll
+                            for (int j = 0; j < 3; ++j)
+                                c[j] = fmaf(2.f, p[yy + 1][xx + j], p[yy][xx + j] + p[yy + 2][xx + j]);
+                            s[q] = fmaf(2.f, c[1], c[0] + c[2]);
+                        }
+                    } else if (EXACT) {
                         s[q] = sum9_exact(p[yy][xx], p[yy][xx + 1], p[yy][xx + 2], p[yy + 1][xx], p[yy + 1][xx + 1],
                                           p[yy + 1][xx + 2], p[yy + 2][xx], p[yy + 2][xx + 1], p[yy + 2][xx + 2]);
-                    else
+                    } else {
                         s[q] = (p[yy][xx] + p[yy + 1][xx] + p[yy + 2][xx]) +
                                (p[yy][xx + 1] + p[yy + 1][xx + 1] + p[yy + 2][xx + 1]) +
                                (p[yy][xx + 2] + p[yy + 1][xx + 2] + p[yy + 2][xx + 2]);
+                    }
                 }
                 out[y * g.out_pitch + x] =
                     EXACT ? coarsity_exact(s[0], s[1], s[2], g.kappa) : coarsity_fast(s[0], s[1], s[2], g.kappa);

@@ -15,6 +15,7 @@ struct Geom {
     float* out;
     int64_t out_pitch, out_image_stride;
     float kappa;
+    int32_t window = 0;  // 1: binomial window instead of the 3x3 box (generic kernel)
 };
 
 // Tile decomposition for the TMA kernel: a tile is one 128-column warp strip of
@@ -59,6 +60,13 @@ cudaError_t launch_tma(int cfg, bool exact, const CUtensorMap& tmap, const TileG
                        cudaStream_t stream);
 
 cudaError_t launch_generic(bool exact, const Geom& g, cudaStream_t stream);
+
+// Harris with the binomial window (HARRIS_FLAG_BINOMIAL_WINDOW): TMA configs 0 and 6
+bool tma_window_config(int cfg);
+cudaError_t tma_window_configure();
+cudaError_t tma_window_occupancy(int cfg, int* ctas_per_sm);
+cudaError_t launch_tma_window(int cfg, bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid,
+                              cudaStream_t stream);
 
 // pair-row TMA kernel for planar f32 whose row pitch is 2 (mod 4) floats (HarrisF32PairRowOp)
 extern const TmaConfig kPairConfig;

@@ -45,7 +45,22 @@ __device__ __forceinline__ void prodsum4(const float (&a)[6], const float (&b)[6
     o3 = fmaf(a[5], b[5], q3);
 }
 
-template <bool EXACT>
+// WIN = 1: the binomial window [1,2,1] x [1,2,1] (the reference's weights2d, evalref.py:114-115)
+// instead of the 3x3 '+' box — "sometimes used as part of the Harris corner detection instead of
+// the 3x3 '+' convolution".  FAST: horizontal [1,2,1] sums of the products,
+// vertical fma(2, mid, top + bottom); EXACT: row-major sum from 0 of w * p (oracle wsum9_f32).
+// products a*b of 6 columns into 4 horizontal [1,2,1] sums, every product folded into an
+// explicit FMA (o = a0 b0 + (2 a1) b1 + a2 b2; 2 a1 is exact): no separate mul + add pair
+// exists for ptxas to contract, so both cores produce the same bits
+__device__ __forceinline__ void prodwin4(const float (&a)[6], const float (&b)[6], float& o0, float& o1, float& o2,
+                                         float& o3) {
+    o0 = fmaf(a[0], b[0], fmaf(2.f * a[1], b[1], a[2] * b[2]));
+    o1 = fmaf(a[1], b[1], fmaf(2.f * a[2], b[2], a[3] * b[3]));
+    o2 = fmaf(a[2], b[2], fmaf(2.f * a[3], b[3], a[4] * b[4]));
+    o3 = fmaf(a[3], b[3], fmaf(2.f * a[4], b[4], a[5] * b[5]));
+}
+
+template <bool EXACT, int WIN = 0>
 struct HarrisCore {
     float kappa;
     // FAST state: horizontal Sobel partials (6 cols) and product 3-sums (3 x 4 cols)
@@ -79,6 +94,7 @@ struct HarrisCore {
     __device__ __forceinline__ void step(const float (&gown)[4], int lane, HaloFn&& halo, float (&out)[4]) {
         constexpr int s2 = R % 3, s0 = (R + 1) % 3, s1 = (R + 2) % 3;
         constexpr bool kLaneHalo = std::is_same_v<std::decay_t<HaloFn>, NoHalo>;
+        static_assert(!(WIN && kLaneHalo && !EXACT), "binomial window: 128-column strips only");
         if constexpr (!EXACT && kLaneHalo) {
             // lane-halo layout: every lane (lane 31 included) has a right neighbour holding
             // the next columns, so Sobel is evaluated on this lane's 4 columns only and the
@@ -150,20 +166,35 @@ struct HarrisCore {
                 ix[k] = fmaf(2.f, D[s1][k], D[s0][k] + D[s2][k]);
                 iy[k] = Hs[s2][k] - Hs[s0][k];
             }
-            // products folded into the shared-pair horizontal 3-sums with explicit FMAs
-            prodsum4(ix, ix, HB[s2][0], HB[s2][1], HB[s2][2], HB[s2][3]);
-            prodsum4(ix, iy, HB[s2][4], HB[s2][5], HB[s2][6], HB[s2][7]);
-            prodsum4(iy, iy, HB[s2][8], HB[s2][9], HB[s2][10], HB[s2][11]);
+            if constexpr (WIN) {
+                prodwin4(ix, ix, HB[s2][0], HB[s2][1], HB[s2][2], HB[s2][3]);
+                prodwin4(ix, iy, HB[s2][4], HB[s2][5], HB[s2][6], HB[s2][7]);
+                prodwin4(iy, iy, HB[s2][8], HB[s2][9], HB[s2][10], HB[s2][11]);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const float sxx = (HB[s0][0 + j] + HB[s1][0 + j]) + HB[s2][0 + j];
-                const float sxy = (HB[s0][4 + j] + HB[s1][4 + j]) + HB[s2][4 + j];
-                const float syy = (HB[s0][8 + j] + HB[s1][8 + j]) + HB[s2][8 + j];
-                out[j] = coarsity_fast(sxx, sxy, syy, kappa);
+                for (int j = 0; j < 4; ++j) {
+                    const float sxx = fmaf(2.f, HB[s1][0 + j], HB[s0][0 + j] + HB[s2][0 + j]);
+                    const float sxy = fmaf(2.f, HB[s1][4 + j], HB[s0][4 + j] + HB[s2][4 + j]);
+                    const float syy = fmaf(2.f, HB[s1][8 + j], HB[s0][8 + j] + HB[s2][8 + j]);
+                    out[j] = coarsity_fast(sxx, sxy, syy, kappa);
+                }
+            } else {
+                // products folded into the shared-pair horizontal 3-sums with explicit FMAs
+                prodsum4(ix, ix, HB[s2][0], HB[s2][1], HB[s2][2], HB[s2][3]);
+                prodsum4(ix, iy, HB[s2][4], HB[s2][5], HB[s2][6], HB[s2][7]);
+                prodsum4(iy, iy, HB[s2][8], HB[s2][9], HB[s2][10], HB[s2][11]);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float sxx = (HB[s0][0 + j] + HB[s1][0 + j]) + HB[s2][0 + j];
+                    const float sxy = (HB[s0][4 + j] + HB[s1][4 + j]) + HB[s2][4 + j];
+                    const float syy = (HB[s0][8 + j] + HB[s1][8 + j]) + HB[s2][8 + j];
+                    out[j] = coarsity_fast(sxx, sxy, syy, kappa);
+                }
             }
         } else {
             const float WX[9] = {-kSobA, 0.f, kSobA, -kSobB, 0.f, kSobB, -kSobA, 0.f, kSobA};
             const float WY[9] = {-kSobA, -kSobB, -kSobA, 0.f, 0.f, 0.f, kSobA, kSobB, kSobA};
+            const float W2D[9] = {1.f, 2.f, 1.f, 2.f, 4.f, 2.f, 1.f, 2.f, 1.f};  // binomial window (WIN)
+            (void)W2D;
 #pragma unroll
             for (int k = 0; k < 4; ++k) G3[s2][k] = gown[k];
 #pragma unroll
@@ -186,8 +217,12 @@ struct HarrisCore {
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
                     const int o = q * 6 + j;
-                    sq[q] = sum9_exact(P[s0][o], P[s0][o + 1], P[s0][o + 2], P[s1][o], P[s1][o + 1], P[s1][o + 2],
-                                       P[s2][o], P[s2][o + 1], P[s2][o + 2]);
+                    if constexpr (WIN)
+                        sq[q] = conv9_exact(W2D, P[s0][o], P[s0][o + 1], P[s0][o + 2], P[s1][o], P[s1][o + 1],
+                                            P[s1][o + 2], P[s2][o], P[s2][o + 1], P[s2][o + 2]);
+                    else
+                        sq[q] = sum9_exact(P[s0][o], P[s0][o + 1], P[s0][o + 2], P[s1][o], P[s1][o + 1],
+                                           P[s1][o + 2], P[s2][o], P[s2][o + 1], P[s2][o + 2]);
                 }
                 out[j] = coarsity_exact(sq[0], sq[1], sq[2], kappa);
             }
@@ -205,7 +240,7 @@ __device__ __forceinline__ float gray_of(float r, float g, float b) {
 }
 
 // ------------------------------------------------------------ planar RGB f32
-template <bool EXACT, int CH, int SC = 128>
+template <bool EXACT, int CH, int SC = 128, int WIN = 0>
 struct HarrisF32Op {
     static_assert(CH % 3 == 0, "row rotation needs CH % 3 == 0");
     using L = Strip<SC>;
@@ -219,7 +254,7 @@ struct HarrisF32Op {
     struct Params {
         float kappa;
     };
-    HarrisCore<EXACT> core;
+    HarrisCore<EXACT, WIN> core;
 
     __device__ __forceinline__ explicit HarrisF32Op(const Params& p) : core(p.kappa) {}
 

@@ -94,7 +94,7 @@ __device__ __forceinline__ float2 coarsity_exact2(float2 sxx, float2 sxy, float2
     return xsub2(det, xmul2(xmul2(f2(k), tr), tr));
 }
 
-template <bool EXACT>
+template <bool EXACT, int WIN = 0>  // WIN: the binomial window (harris_ops.cuh)
 struct HarrisCore2 {
     float kappa;
     float2 D[3][6], Hs[3][6], HB[3][12];   // FAST
@@ -125,6 +125,16 @@ struct HarrisCore2 {
         o1 = fma2(a[3], b[3], q1);
         o2 = fma2(a[2], b[2], q3);
         o3 = fma2(a[5], b[5], q3);
+    }
+
+    // products a*b of 6 columns into 4 horizontal [1,2,1] sums (binomial window), the same
+    // explicit-FMA form as the scalar core's prodwin4
+    __device__ __forceinline__ static void prodwin4(const float2 (&a)[6], const float2 (&b)[6], float2& o0,
+                                                    float2& o1, float2& o2, float2& o3) {
+        o0 = fma2(a[0], b[0], fma2(mul2(f2(2.f), a[1]), b[1], mul2(a[2], b[2])));
+        o1 = fma2(a[1], b[1], fma2(mul2(f2(2.f), a[2]), b[2], mul2(a[3], b[3])));
+        o2 = fma2(a[2], b[2], fma2(mul2(f2(2.f), a[3]), b[3], mul2(a[4], b[4])));
+        o3 = fma2(a[3], b[3], fma2(mul2(f2(2.f), a[4]), b[4], mul2(a[5], b[5])));
     }
 
     // gown: (A, B) gray of this lane's 4 columns; halo(h0..h3) fills the right halo of
@@ -165,12 +175,22 @@ struct HarrisCore2 {
                     iy[4 + k] = shfl_down2(iy[k]);
                 }
             }
-            prodsum4(ix, ix, HB[s2][0], HB[s2][1], HB[s2][2], HB[s2][3]);
-            prodsum4(ix, iy, HB[s2][4], HB[s2][5], HB[s2][6], HB[s2][7]);
-            prodsum4(iy, iy, HB[s2][8], HB[s2][9], HB[s2][10], HB[s2][11]);
+            static_assert(!WIN || (NC == 6 && !kPairRows), "binomial window: 128-column strips, 3-row sums");
+            if constexpr (WIN) {
+                prodwin4(ix, ix, HB[s2][0], HB[s2][1], HB[s2][2], HB[s2][3]);
+                prodwin4(ix, iy, HB[s2][4], HB[s2][5], HB[s2][6], HB[s2][7]);
+                prodwin4(iy, iy, HB[s2][8], HB[s2][9], HB[s2][10], HB[s2][11]);
+            } else {
+                prodsum4(ix, ix, HB[s2][0], HB[s2][1], HB[s2][2], HB[s2][3]);
+                prodsum4(ix, iy, HB[s2][4], HB[s2][5], HB[s2][6], HB[s2][7]);
+                prodsum4(iy, iy, HB[s2][8], HB[s2][9], HB[s2][10], HB[s2][11]);
+            }
             const float2 nk = f2(-kappa);
             float2 v[12];
-            if constexpr (kPairRows) {
+            if constexpr (WIN) {
+#pragma unroll
+                for (int q = 0; q < 12; ++q) v[q] = fma2(f2(2.f), HB[s1][q], add2(HB[s0][q], HB[s2][q]));
+            } else if constexpr (kPairRows) {
                 // odd row r: PV = H[r-1] + H[r], V = H[r-2] + PV; even row: V = PV + H[r]
                 if constexpr (R % 2 == 1) {
 #pragma unroll
@@ -200,6 +220,8 @@ struct HarrisCore2 {
         } else {
             const float WX[9] = {-kSobA, 0.f, kSobA, -kSobB, 0.f, kSobB, -kSobA, 0.f, kSobA};
             const float WY[9] = {-kSobA, -kSobB, -kSobA, 0.f, 0.f, 0.f, kSobA, kSobB, kSobA};
+            const float W2D[9] = {1.f, 2.f, 1.f, 2.f, 4.f, 2.f, 1.f, 2.f, 1.f};  // binomial window (WIN)
+            (void)W2D;
 #pragma unroll
             for (int k = 0; k < 8; ++k) G3[s2][k] = g[k];
 #pragma unroll
@@ -218,8 +240,12 @@ struct HarrisCore2 {
 #pragma unroll
                 for (int q = 0; q < 3; ++q) {
                     const int o = q * 6 + j;
-                    sq[q] = sum9_exact2(P[s0][o], P[s0][o + 1], P[s0][o + 2], P[s1][o], P[s1][o + 1], P[s1][o + 2],
-                                        P[s2][o], P[s2][o + 1], P[s2][o + 2]);
+                    if constexpr (WIN)
+                        sq[q] = conv9_exact2(W2D, P[s0][o], P[s0][o + 1], P[s0][o + 2], P[s1][o], P[s1][o + 1],
+                                             P[s1][o + 2], P[s2][o], P[s2][o + 1], P[s2][o + 2]);
+                    else
+                        sq[q] = sum9_exact2(P[s0][o], P[s0][o + 1], P[s0][o + 2], P[s1][o], P[s1][o + 1],
+                                            P[s1][o + 2], P[s2][o], P[s2][o + 1], P[s2][o + 2]);
                 }
                 const float2 o = coarsity_exact2(sq[0], sq[1], sq[2], kappa);
                 out[0][j] = o.x;
@@ -239,7 +265,7 @@ __device__ __forceinline__ float2 gray2_of(float2 r, float2 g, float2 b) {
 
 // ------------------------------------------------------------ planar RGB f32
 // Two TMA boxes per stage ({132 cols, CH rows, 3 channels, 1 image} at x and x+128).
-template <bool EXACT, int CH, int SC = 128>
+template <bool EXACT, int CH, int SC = 128, int WIN = 0>
 struct HarrisF32x2Op {
     static_assert(CH % 3 == 0, "row rotation needs CH % 3 == 0");
     using L = Strip<SC>;
@@ -256,7 +282,7 @@ struct HarrisF32x2Op {
     struct Params {
         float kappa;
     };
-    HarrisCore2<EXACT> core;
+    HarrisCore2<EXACT, WIN> core;
 
     __device__ __forceinline__ explicit HarrisF32x2Op(const Params& p) : core(p.kappa) {}
 

@@ -77,10 +77,10 @@ struct StripColsOf : std::integral_constant<int, 128> {};
 template <class C>
 struct StripColsOf<C, std::void_t<decltype(C::SC)>> : std::integral_constant<int, C::SC> {};
 
-template <int CFG, bool EXACT>
+template <int CFG, bool EXACT, int WIN = 0>
 using F32OpOf = std::conditional_t<F32Cfg<CFG>::G == 2,
-                                   HarrisF32x2Op<EXACT, F32Cfg<CFG>::CH, StripColsOf<F32Cfg<CFG>>::value>,
-                                   HarrisF32Op<EXACT, F32Cfg<CFG>::CH, StripColsOf<F32Cfg<CFG>>::value>>;
+                                   HarrisF32x2Op<EXACT, F32Cfg<CFG>::CH, StripColsOf<F32Cfg<CFG>>::value, WIN>,
+                                   HarrisF32Op<EXACT, F32Cfg<CFG>::CH, StripColsOf<F32Cfg<CFG>>::value, WIN>>;
 
 #define HARRIS_CFG_ROW(k) {F32Cfg<k>::NW, F32Cfg<k>::NS, F32Cfg<k>::CH, F32Cfg<k>::G, StripColsOf<F32Cfg<k>>::value}
 const TmaConfig kTmaConfigs[kNumTmaConfigs] = {
@@ -90,10 +90,10 @@ const TmaConfig kTmaConfigs[kNumTmaConfigs] = {
 };
 #undef HARRIS_CFG_ROW
 
-template <int CFG, bool EXACT>
+template <int CFG, bool EXACT, int WIN = 0>
 static constexpr auto f32_kernel() {
     using C = F32Cfg<CFG>;
-    return strip_kernel<F32OpOf<CFG, EXACT>, C::NW, C::NS, C::MINB>;
+    return strip_kernel<F32OpOf<CFG, EXACT, WIN>, C::NW, C::NS, C::MINB>;
 }
 
 template <int CFG>
@@ -104,29 +104,55 @@ static constexpr size_t f32_smem() {
 
 constexpr size_t kMaxDynSmem = 227 * 1024;  // sm_100 opt-in maximum per block
 
-template <int CFG>
+template <int CFG, int WIN = 0>
 static cudaError_t configure_one() {
     static_assert(f32_smem<CFG>() <= kMaxDynSmem, "TMA config exceeds 227 KB of shared memory");
-    cudaError_t e = cudaFuncSetAttribute(f32_kernel<CFG, false>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(f32_kernel<CFG, false, WIN>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(f32_smem<CFG>()));
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(f32_kernel<CFG, true>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
+    return cudaFuncSetAttribute(f32_kernel<CFG, true, WIN>(), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(f32_smem<CFG>()));
 }
 
-template <int CFG>
+template <int CFG, int WIN = 0>
 static cudaError_t launch_one(bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid,
                               cudaStream_t stream) {
     using C = F32Cfg<CFG>;
     const dim3 block{unsigned(C::NW * 32)}, gridd{unsigned(grid)};
     if (exact) {
-        const typename F32OpOf<CFG, true>::Params p{tg.kappa};
-        launch_strip(f32_kernel<CFG, true>(), gridd, block, f32_smem<CFG>(), stream, tg.pdl, tmap, tg, p);
+        const typename F32OpOf<CFG, true, WIN>::Params p{tg.kappa};
+        launch_strip(f32_kernel<CFG, true, WIN>(), gridd, block, f32_smem<CFG>(), stream, tg.pdl, tmap, tg, p);
     } else {
-        const typename F32OpOf<CFG, false>::Params p{tg.kappa};
-        launch_strip(f32_kernel<CFG, false>(), gridd, block, f32_smem<CFG>(), stream, tg.pdl, tmap, tg, p);
+        const typename F32OpOf<CFG, false, WIN>::Params p{tg.kappa};
+        launch_strip(f32_kernel<CFG, false, WIN>(), gridd, block, f32_smem<CFG>(), stream, tg.pdl, tmap, tg, p);
     }
     return cudaGetLastError();
+}
+
+// ---- Harris with the binomial window (WIN = 1): the default long-tile config (6, packed
+// dual-strip core) and the short-tile config (0, scalar core) only
+bool tma_window_config(int cfg) { return cfg == 0 || cfg == 6; }
+
+cudaError_t tma_window_configure() {
+    cudaError_t e = configure_one<0, 1>();
+    return e == cudaSuccess ? configure_one<6, 1>() : e;
+}
+
+cudaError_t tma_window_occupancy(int cfg, int* ctas_per_sm) {
+    if (cfg == 0)
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, f32_kernel<0, false, 1>(),
+                                                             F32Cfg<0>::NW * 32, f32_smem<0>());
+    if (cfg == 6)
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, f32_kernel<6, false, 1>(),
+                                                             F32Cfg<6>::NW * 32, f32_smem<6>());
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_tma_window(int cfg, bool exact, const CUtensorMap& tmap, const TileGeom& tg, int64_t grid,
+                              cudaStream_t stream) {
+    if (cfg == 0) return launch_one<0, 1>(exact, tmap, tg, grid, stream);
+    if (cfg == 6) return launch_one<6, 1>(exact, tmap, tg, grid, stream);
+    return cudaErrorInvalidValue;
 }
 
 template <int CFG>

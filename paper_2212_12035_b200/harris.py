@@ -143,6 +143,17 @@ def _stream_handle(dev: int, stream: Optional[torch.cuda.Stream]) -> int:
     return torch.cuda.current_stream(dev).cuda_stream
 
 
+WINDOWS = ("box", "binomial")
+
+
+def _window_flag(window: str) -> int:
+    """window "box": the thesis's 3x3 '+' sums; "binomial": the reference's weights2d window
+    (HARRIS_FLAG_BINOMIAL_WINDOW, PAPER.md:3937-3938)."""
+    if window not in WINDOWS:
+        raise ValueError(f"window must be one of {WINDOWS}")
+    return _lib.FLAG_BINOMIAL_WINDOW if window == "binomial" else 0
+
+
 def _flags(exact: bool, force_generic: bool, force_tma: bool, pdl=False) -> int:
     """pdl: False; True = HARRIS_FLAG_PDL (prologue overlaps the previous kernel, waits before
     touching memory); "independent" = HARRIS_FLAG_PDL_INDEPENDENT (the caller guarantees the
@@ -174,7 +185,7 @@ def _check_rgb(rgb) -> tuple[int, int, int]:
 
 def harris(rgb, kappa: float = KAPPA, *, out: Optional[torch.Tensor] = None, exact: bool = False,
            force_generic: bool = False, force_tma: bool = False, stream: Optional[torch.cuda.Stream] = None,
-           ctx: Optional[HarrisContext] = None, pdl=False):
+           ctx: Optional[HarrisContext] = None, pdl=False, window: str = "box"):
     """Fused Harris coarsity of planar RGB f32.
 
     rgb: ``(3, H, W)`` or ``(B, 3, H, W)`` float32; CUDA tensor (device path,
@@ -183,9 +194,10 @@ def harris(rgb, kappa: float = KAPPA, *, out: Optional[torch.Tensor] = None, exa
     ``exact=True`` selects the Appendix-B op order (bit-identical to the C
     oracle); the default is the FMA/separable order, within the SURVEY.md §8(d)
     tolerance of the f64 reference.  ``pdl`` (device path): programmatic dependent launch for
-    back-to-back frame streams (see ``_flags``).
+    back-to-back frame streams (see ``_flags``).  ``window="binomial"``: the binomial
+    window in place of the 3x3 box sums (``_window_flag``).
     """
-    flags = _flags(exact, force_generic, force_tma, pdl)
+    flags = _flags(exact, force_generic, force_tma, pdl) | _window_flag(window)
     if isinstance(rgb, np.ndarray) or (isinstance(rgb, torch.Tensor) and not rgb.is_cuda):
         _check_rgb(rgb)
         arr = rgb if isinstance(rgb, np.ndarray) else rgb.numpy()
@@ -270,12 +282,12 @@ def harris_frames(frames, outs=None, kappa: float = KAPPA, *, exact: bool = Fals
 
 def harris_u8(rgb8, kappa: float = KAPPA, *, out: Optional[torch.Tensor] = None, exact: bool = False,
               force_generic: bool = False, force_tma: bool = False, stream: Optional[torch.cuda.Stream] = None,
-              ctx: Optional[HarrisContext] = None, pdl=False):
+              ctx: Optional[HarrisContext] = None, pdl=False, window: str = "box"):
     """Fused Harris on interleaved 8-bit RGB: ``(H, W, 3)`` or ``(B, H, W, 3)`` uint8
     (value/255), CUDA (device path) or CPU/numpy (host path through the device).
     Returns ``(H-4, W-4)`` / ``(B, H-4, W-4)`` float32, equal to ``harris`` on the planar
     image ``rgb8/255`` (bit-for-bit with ``exact=True``)."""
-    flags = _flags(exact, force_generic, force_tma, pdl)
+    flags = _flags(exact, force_generic, force_tma, pdl) | _window_flag(window)
     shape = tuple(rgb8.shape)
     if rgb8.dtype not in (torch.uint8, np.uint8):
         raise TypeError("harris_u8 expects uint8 interleaved RGB")

@@ -45,7 +45,7 @@ def _sges(reference_src: Optional[str] = None):
     return parser, infer, evalref
 
 
-def gpu_impl(kappa: float = 0.04) -> Callable[[np.ndarray], np.ndarray]:
+def gpu_impl(kappa: float = 0.04, window: str = "box") -> Callable[[np.ndarray], np.ndarray]:
     """(3, H, W) float32 host array -> (H-4, W-4) through the fused kernel."""
     import torch
 
@@ -53,19 +53,21 @@ def gpu_impl(kappa: float = 0.04) -> Callable[[np.ndarray], np.ndarray]:
 
     def run(rgb: np.ndarray) -> np.ndarray:
         t = torch.from_numpy(np.ascontiguousarray(rgb, dtype=np.float32)).cuda()
-        out = harris(t, kappa)
+        out = harris(t, kappa, window=window)
         return out.cpu().numpy()
 
     return run
 
 
 def register(env: dict, amb: dict, impl: Optional[Callable[[np.ndarray], np.ndarray]] = None,
-             reference_src: Optional[str] = None) -> tuple[dict, dict]:
+             reference_src: Optional[str] = None, name: str = "harris", window: str = "box") -> tuple[dict, dict]:
     """Add the ``harris`` scheme to a type environment and its implementation to
-    an evaluator ambient map; ``impl`` defaults to the B200 kernel."""
+    an evaluator ambient map; ``impl`` defaults to the B200 kernel.  ``window="binomial"``
+    (registered e.g. as ``name="harris_binomial"``) is the Harris variant with the binomial
+    window, the sges program ``oracle/sges_oracle.harris_source("binomial")``."""
     parser, _, _ = _sges(reference_src)
-    fn = impl or gpu_impl()
-    env["harris"] = parser.parse_type(HARRIS_SCHEME)
+    fn = impl or gpu_impl(window=window)
+    env[name] = parser.parse_type(HARRIS_SCHEME)
 
     def _call(rgb_lists):
         arr = np.asarray(rgb_lists, dtype=np.float32)
@@ -73,7 +75,7 @@ def register(env: dict, amb: dict, impl: Optional[Callable[[np.ndarray], np.ndar
             raise ValueError(f"harris needs a 3 x (n+4) x (m+4) input with n, m >= 1, got {arr.shape}")
         return np.asarray(fn(arr), dtype=np.float64).tolist()
 
-    amb["harris"] = _call
+    amb[name] = _call
     return env, amb
 
 

@@ -1,4 +1,4 @@
-"""A/B timing of one shape: python tools/perf_shape.py {f32,f32crop,u8,sep,seppad,sepcrop} B H W [reps]; HARRIS_LIB selects the .so."""
+"""A/B timing of one shape: python tools/perf_shape.py {f32,f32crop,f32win,u8,sep,seppad,sepcrop} B H W [reps]; HARRIS_LIB selects the .so."""
 import sys, torch
 sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
 import paper_2212_12035_b200 as hb
@@ -23,6 +23,9 @@ elif kind == "sepcrop":  # column-crop view x[..., :W] of (W+2)-pitch planes: TM
 elif kind == "f32crop":  # column-crop view: base 4-byte aligned only
     x = torch.rand((B, 3, H, W + 1), device="cuda", generator=g)[..., 1:]
     f = lambda: hb.harris(x, out=out)
+elif kind == "f32win":  # Harris with the binomial window
+    x = torch.rand((B, 3, H, W), device="cuda", generator=g)
+    f = lambda: hb.harris(x, out=out, window="binomial")
 else:
     x = torch.rand((B, 3, H, W), device="cuda", generator=g)
     f = lambda: hb.harris(x, out=out)
