@@ -207,8 +207,13 @@ HARRIS_API int harris_synth_fill(float* dst, int64_t planes, int64_t rows, int64
 /* Kernel-grouping design space of the thesis, for the fusion
  * ablation: each group is a separate kernel that round-trips its intermediates
  * through HBM in caller-provided scratch (the thesis's t1..t3 temporaries).
- * Groupings 1-3 always evaluate the Appendix-B order (bit-identical to the oracle);
- * grouping 4 is harris_run_strided (flags honoured).  Contiguous single image. */
+ * Groupings 1-3 without HARRIS_FLAG_EXACT_ORDER run every group as a strip-engine kernel
+ * (TMA ring, register rotation, 16-byte stores) in the fused kernel's FAST arithmetic — the
+ * fair fusion ablation: grouping 3 is bit-identical to the fused FAST output, groupings 1-2
+ * round the products they materialise (within tolerance); needs W % 4 == 0 and 16-byte
+ * aligned buffers.  With HARRIS_FLAG_EXACT_ORDER (or other layouts) the groups are simple
+ * one-thread-per-pixel kernels in the Appendix-B order (bit-identical to the oracle).
+ * Grouping 4 is harris_run_strided (flags honoured).  Contiguous single image. */
 #define HARRIS_GROUPING_UNFUSED    1  /* [Sx],[Sy],[x],[+],[coarsity]  5 kernels */
 #define HARRIS_GROUPING_SOBEL_PROD 2  /* [Sx,Sy,x],[+,coarsity]        2 kernels */
 #define HARRIS_GROUPING_SOBEL      3  /* [Sx,Sy],[x,+,coarsity]        2 kernels */

@@ -59,6 +59,7 @@ struct harris_ctx {
     CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;  // dev knob HARRIS_L2_PROMO
     int occ[kNumTmaConfigs] = {0};
     int occ_win[2] = {0, 0};  // binomial-window kernels of TMA configs 0 and 6
+    int occ_grp = 0;          // strip-engine kernel groupings (fusion ablation)
     PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     std::atomic<int> last_path{HARRIS_PATH_NONE};  // diagnostic; calls may race on different streams
     char last_err[256] = {0};
@@ -529,6 +530,17 @@ Call make_call(float* out, int64_t out_pitch, int64_t out_image_stride, int64_t 
 
 }  // namespace
 
+namespace harris {
+void plan_tiles_ext(int64_t n, int64_t m, int64_t batch, int64_t gw, int rows_per_stage, int64_t force_rows,
+                    TileGeom& tg, int halo) {
+    plan_tiles(n, m, batch, gw, rows_per_stage, force_rows, tg, halo);
+}
+
+int store_mode_ext(const float* out, int64_t out_pitch, int64_t batch, int64_t out_image_stride) {
+    return store_mode(out, out_pitch, batch, out_image_stride);
+}
+}  // namespace harris
+
 extern "C" {
 
 int harris_abi_version(void) { return HARRIS_B200_ABI_VERSION; }
@@ -665,6 +677,7 @@ int harris_init_ex(harris_ctx** out_ctx, int cuda_device, const harris_options* 
     if (e == cudaSuccess) e = tma_window_configure();
     if (e == cudaSuccess) e = tma_window_occupancy(0, &ctx->occ_win[0]);
     if (e == cudaSuccess) e = tma_window_occupancy(6, &ctx->occ_win[1]);
+    if (e == cudaSuccess) e = grouping_fast_configure(&ctx->occ_grp);
     e = e == cudaSuccess ? pair_configure(&ctx->occ_pair) : e;
     if (e == cudaSuccess) e = quad_configure(&ctx->occ_quad);
     if (e == cudaSuccess) e = sep_ldg_configure(&ctx->occ_sepldg);
@@ -951,7 +964,10 @@ int harris_synth_fill(float* dst, int64_t planes, int64_t rows, int64_t W, int64
 int64_t harris_grouping_scratch_bytes(int grouping, int64_t n, int64_t m) {
     if (n < 1 || m < 1) return -1;
     const int64_t f = grouping_scratch_floats(grouping, n, m);
-    return f < 0 ? -1 : f * 4;
+    if (f < 0) return -1;
+    // enough for both implementations: the Appendix-B kernels (EXACT) and the strip-engine
+    // kernels (FAST, 16-byte aligned plane pitches)
+    return std::max(f, grouping_fast_scratch_floats(grouping, n, m)) * 4;
 }
 
 int harris_grouping_launches(int grouping) { return grouping_launches(grouping); }
@@ -970,6 +986,23 @@ int harris_run_grouping(harris_ctx* ctx, int grouping, float* out, int64_t n, in
     if (!scratch || scratch_bytes < need) return HARRIS_ERR_INVALID_ARGUMENT;
     DeviceGuard guard(ctx->device);
     if (!guard.ok) return cuda_fail(ctx, cudaGetLastError(), "cudaSetDevice");
+    // FAST (default): every group a strip-engine kernel in the fused kernel's arithmetic (the
+    // fair ablation; needs the TMA layout: W % 4 == 0, 16-byte aligned rgb / scratch / out);
+    // HARRIS_FLAG_EXACT_ORDER or other layouts: the Appendix-B one-thread-per-pixel kernels
+    const bool fast = !(flags & HARRIS_FLAG_EXACT_ORDER) && ((m + 4) & 3) == 0 && aligned16(rgb) &&
+                      aligned16(scratch) && aligned16(out) && (m & 3) == 0;
+    if (fast) {
+        const GroupLaunchEnv env{ctx->encode, ctx->num_sms, ctx->occ_grp, ctx->l2_policy};
+        const int rc = launch_grouping_fast(env, grouping, out, n, m, rgb, static_cast<float*>(scratch), kappa,
+                                            static_cast<cudaStream_t>(stream));
+        if (rc < 0) {
+            std::snprintf(ctx->last_err, sizeof(ctx->last_err), "cuTensorMapEncodeTiled (grouping) failed");
+            return HARRIS_ERR_TMA;
+        }
+        if (rc) return cuda_fail(ctx, cudaGetLastError(), "launch grouping (fast)");
+        ctx->last_path = HARRIS_PATH_TMA;
+        return HARRIS_OK;
+    }
     cudaError_t e = launch_grouping(grouping, out, n, m, rgb, static_cast<float*>(scratch), kappa, ctx->num_sms,
                                     static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(ctx, e, "launch grouping");

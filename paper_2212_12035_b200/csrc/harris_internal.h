@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <cstdint>
 
 namespace harris {
@@ -40,6 +41,7 @@ struct TileGeom {
     uint32_t* notify_counter = nullptr;
     uint32_t* notify_flag = nullptr;
     uint32_t notify_epoch = 0;
+    int64_t out_plane_stride = 0;  // Op::kOutPlanes > 1: elements between output planes
 };
 
 // TMA kernel configurations (warps per CTA, pipeline stages per warp, input rows
@@ -133,6 +135,21 @@ cudaError_t launch_tma_sep(int cfg, bool exact, const CUtensorMap& tmap, const C
 cudaError_t launch_generic_sep(bool exact, const float* in, int64_t in_pitch, int64_t in_image_stride, float* out,
                                int64_t out_pitch, int64_t out_image_stride, int64_t n, int64_t m, int64_t batch,
                                const float* wv, const float* wh, int num_sms, cudaStream_t stream);
+
+// planner / store-mode helpers of harris_abi.cu for other translation units
+void plan_tiles_ext(int64_t n, int64_t m, int64_t batch, int64_t gw, int rows_per_stage, int64_t force_rows,
+                    TileGeom& tg, int halo);
+int store_mode_ext(const float* out, int64_t out_pitch, int64_t batch, int64_t out_image_stride);
+
+// FAST kernel groupings on the strip engine (harris_groupings_tma.cu): the fair fusion ablation
+struct GroupLaunchEnv {
+    PFN_cuTensorMapEncodeTiled_v12000 encode;
+    int num_sms, occ, l2_policy;
+};
+int64_t grouping_fast_scratch_floats(int grouping, int64_t n, int64_t m);
+cudaError_t grouping_fast_configure(int* occ);
+int launch_grouping_fast(const GroupLaunchEnv& env, int grouping, float* out, int64_t n, int64_t m, const float* rgb,
+                         float* scratch, float kappa, cudaStream_t st);
 
 int64_t grouping_scratch_floats(int grouping, int64_t n, int64_t m);
 int grouping_launches(int grouping);

@@ -170,6 +170,14 @@ __device__ __forceinline__ void stg_realigned_row(float* po, const float (&o)[4]
     }
 }
 
+// Op::kOutPlanes is optional (default 1; single-strip ops only): the op produces that many
+// output planes per row (out[kOutPlanes][4]), stored at TileGeom::out_plane_stride apart —
+// the unfused kernel groupings of the fusion ablation write Ix/Iy or the three products
+template <class Op, class = void>
+struct OutPlanesOf : std::integral_constant<int, 1> {};
+template <class Op>
+struct OutPlanesOf<Op, std::void_t<decltype(Op::kOutPlanes)>> : std::integral_constant<int, Op::kOutPlanes> {};
+
 // Op::kTwoStoreVariants is optional (default false): compile the consumer's stage loop twice,
 // with and without the scalar-store code for ragged / unaligned output lanes.  Measured per
 // op (tools/perf_matrix.sh): issue-bound u8 TMA 840 -> 887 k MP/s, stencil on 1918-wide
@@ -278,6 +286,8 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     constexpr int CH = Op::kRowsPerStage;
     constexpr int HALO = Op::kHaloRows;
     constexpr int G = Op::kGroups;
+    constexpr int NP = OutPlanesOf<Op>::value;
+    static_assert(NP == 1 || G == 1, "multi-plane outputs: single-strip ops");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     // align by offsetting the __shared__ array itself (an integer round trip would turn
     // every stage read into a generic LD instead of LDS)
@@ -497,22 +507,25 @@ __global__ void __launch_bounds__(NW * 32, MINB)
             [&](auto rc) {                                                                                       \
                 constexpr int R = decltype(rc)::value;                                                           \
                 const int i = c * CH + R; /* input row within the tile */                                        \
-                float out4[G][4];                                                                                \
+                float out4[G * NP][4];                                                                           \
                 op.template row<R>(sm, lane, out4);                                                              \
                 if (i >= HALO && i - HALO < rows_out) {                                                          \
-                    _Pragma("unroll") for (int gi = 0; gi < G; ++gi) {                                           \
-                        float* po = orow[gi] + int64_t(i - HALO) * g.out_pitch;                                  \
-                        stg128_cs_if(vec[gi], po, out4[gi][0], out4[gi][1], out4[gi][2], out4[gi][3]);           \
+                    _Pragma("unroll") for (int gp = 0; gp < G * NP; ++gp) {                                      \
+                        /* NP > 1: output planes of one strip (G == 1) at out_plane_stride */                   \
+                        const int gi = NP > 1 ? 0 : gp;                                                          \
+                        float* po = orow[gi] + int64_t(i - HALO) * g.out_pitch +                                 \
+                                    (NP > 1 ? int64_t(gp) * g.out_plane_stride : 0);                             \
+                        stg128_cs_if(vec[gi], po, out4[gp][0], out4[gp][1], out4[gp][2], out4[gp][3]);           \
                         if (RAGGED) { /* unaligned output rows, or the ragged right edge */                      \
                             const int cg = colg[gi];                                                             \
                             if (RealignStoresOf<Op>::value && g.vec_store == 1) {                                \
-                                stg_realigned_row(po, out4[gi], cg, g.m, lane);                                  \
+                                stg_realigned_row(po, out4[gp], cg, g.m, lane);                                  \
                             } else if (!vec[gi] && cg < g.m) {                                                   \
                                 if (SplitStoresOf<Op>::value && g.vec_store == 1 && cg + kColsPerLane <= g.m) {  \
-                                    stg2x2_cs(po, out4[gi][0], out4[gi][1], out4[gi][2], out4[gi][3]);           \
+                                    stg2x2_cs(po, out4[gp][0], out4[gp][1], out4[gp][2], out4[gp][3]);           \
                                 } else {                                                                         \
                                     _Pragma("unroll") for (int k = 0; k < kColsPerLane; ++k) if (cg + k < g.m)   \
-                                        po[k] = out4[gi][k];                                                     \
+                                        po[k] = out4[gp][k];                                                     \
                                 }                                                                                \
                             }                                                                                    \
                         }                                                                                        \

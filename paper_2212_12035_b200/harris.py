@@ -396,7 +396,11 @@ def grouping_hbm_bytes(grouping: int, n: int, m: int) -> int:
 def harris_grouping(rgb: torch.Tensor, grouping: int, kappa: float = KAPPA, *, out: Optional[torch.Tensor] = None,
                     scratch: Optional[torch.Tensor] = None, exact: bool = False) -> torch.Tensor:
     """The thesis's kernel-grouping design space on one contiguous
-    (3, H, W) CUDA image; groupings 1-3 round-trip intermediates through HBM scratch."""
+    (3, H, W) CUDA image; groupings 1-3 round-trip intermediates through HBM scratch.
+    FAST (default): every group is a strip-engine kernel in the fused kernel's arithmetic
+    (grouping 3 is bit-identical to the fused FAST output, 1 and 2 round the products they
+    materialise); ``exact=True``: the Appendix-B one-thread-per-pixel kernels (bit-identical to
+    the oracle)."""
     B, H, W = _check_rgb(rgb)
     if rgb.dim() != 3 or not rgb.is_cuda or not rgb.is_contiguous():
         raise ValueError("harris_grouping takes one contiguous (3, H, W) CUDA image")

@@ -127,3 +127,15 @@ def test_plain_c_host_example_without_a_device():
         pytest.skip("a GPU is present (tests/test_gpu_parity.py runs the example)")
     r = subprocess.run([exe, "64", "136"], capture_output=True, text=True, timeout=60)
     assert r.returncode == 4 and "harris_init" in r.stderr
+
+
+def test_library_has_no_undefined_internal_symbols():
+    """Every internal (harris::) symbol the library references is defined in it: a missing
+    definition would only surface as a dlopen failure on the GPU box."""
+    import shutil
+    import subprocess
+    if not shutil.which("nm"):
+        pytest.skip("nm not available")
+    out = subprocess.run(["nm", "-D", "--undefined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    missing = [ln for ln in out.splitlines() if "_ZN6harris" in ln]
+    assert not missing, missing

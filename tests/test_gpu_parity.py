@@ -246,6 +246,24 @@ def test_kernel_groupings_bitexact(cuda_ctx, grouping, H, W):
     assert np.array_equal(got.cpu().numpy(), cref.harris_f32(rgb))
 
 
+@pytest.mark.parametrize("grouping", [1, 2, 3])
+@pytest.mark.parametrize("H,W", [(5, 8), (13, 20), (70, 260), (300, 1028), (1080, 1920)])
+def test_kernel_groupings_fast(cuda_ctx, grouping, H, W):
+    """FAST groupings (strip-engine kernels, the fair fusion ablation): grouping 3 equals the
+    fused FAST kernel bit for bit (its second kernel is the fused core's back half); groupings
+    1 and 2 materialise rounded products and meet the §8(d) tolerance of the f64 oracle."""
+    rgb = synth.synth_numpy(3, H, W, seed=H * 7 + W + grouping)
+    x = _dev(rgb)
+    got = hb.harris_grouping(x, grouping)
+    torch.cuda.synchronize()
+    assert cuda_ctx.last_path == _lib.PATH_TMA
+    fused = hb.harris(x)
+    if grouping == 3:
+        assert torch.equal(got, fused)
+    ok, m = synth.within_tolerance(got.cpu().numpy(), cref.harris_f64(rgb))
+    assert ok, (grouping, H, W, m)
+
+
 def test_grouping_scratch_contract(cuda_ctx):
     L = _lib.lib()
     assert L.harris_grouping_scratch_bytes(4, 10, 10) == 0
