@@ -48,7 +48,26 @@ for off in (1, 3):         # stencil K1b bulk rows (unaligned base, odd pitch)
     hb.stencil3x3_sep(buf[off:].view(2, 50, 263))
     hb.stencil3x3_sep(buf[off:].view(2, 50, 263), exact=True)
 for g in (1, 2, 3, 4):
-    hb.harris_grouping(torch.rand(3, 40, 132, device="cuda"), g)
+    for exact in (False, True):  # FAST: strip-engine groupings (round 2); EXACT: Appendix-B kernels
+        hb.harris_grouping(torch.rand(3, 40, 132, device="cuda"), g, exact=exact)
+# round 2: stencil TMA-store epilogue (config 3 on a column-crop view with a 16-byte aligned
+# output pitch), realigned stores (contiguous 1918-wide-style outputs), binomial window
+# (TMA configs 0 / 6 and generic), PDL launches, the frames API
+dev_ctx = None
+os.environ["HARRIS_DEV"] = "1"
+os.environ["HARRIS_SEP_CONFIG"] = "3"
+ts_ctx = hb.HarrisContext(0)
+del os.environ["HARRIS_SEP_CONFIG"], os.environ["HARRIS_DEV"]
+planes = torch.rand(2, 40, 134, device="cuda")
+hb.stencil3x3_sep(planes[..., :130], ctx=ts_ctx, out=torch.empty(2, 38, 132, device="cuda")[..., :128])
+hb.stencil3x3_sep(torch.rand(2, 41, 132, device="cuda"))          # m = 130: realigned 16-byte stores
+for kw in ({}, {"exact": True}, {"force_generic": True}):
+    hb.harris(torch.rand(3, 70, 264, device="cuda"), window="binomial", **kw)
+    hb.harris(torch.rand(3, 300, 1028, device="cuda"), window="binomial", **kw)
+x0 = torch.rand(3, 70, 264, device="cuda")
+hb.harris(x0, pdl=True)
+hb.harris(x0, pdl="independent")
+hb.harris_frames([torch.rand(3, 64, 260, device="cuda") for _ in range(3)])
 x = torch.rand(3, 40, 136, device="cuda")
 out = torch.empty(36, 132, device="cuda")
 flag = torch.zeros(2, dtype=torch.int32, device="cuda")
