@@ -605,7 +605,8 @@ def frame_stream(H, W, n_frames=240, ring=None,
                   modes=("plain", "pdl", "independent", "graph", "frames", "frames_graph")) -> dict:
     """Back-to-back UNBATCHED single frames over a ring of distinct frames (> L2, so every frame
     streams from HBM).  Modes: plain launches; pdl (HARRIS_FLAG_PDL); independent
-    (HARRIS_FLAG_PDL_INDEPENDENT); graph (the independent ring captured in a CUDA graph and
+    (HARRIS_FLAG_PDL_INDEPENDENT); "plain" uses a ctx with harris_options.pdl = 0 (the library
+    default is PDL with the wait); graph (the independent ring captured in a CUDA graph and
     replayed); frames (harris_run_frames: the ring in one C call, one launch per frame);
     frames_graph.  Per mode: us per frame = CUDA-event time of N frames / N."""
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -620,8 +621,10 @@ def frame_stream(H, W, n_frames=240, ring=None,
     nbytes = hb.algorithmic_bytes(H - 4, W - 4)
     res = {"frame": f"{W}x{H} RGB f32", "ring_frames": ring, "ring_input_mb": ring * frame_bytes / 2**20}
     ref = [hb.harris(x) for x in xs]
+    plain_ctx = hb.HarrisContext(torch.cuda.current_device(), pdl=False)  # plain launches (options.pdl = 0)
     for mode in modes:
         pdl = {"plain": False, "pdl": True, "independent": "independent", "graph": "independent"}.get(mode)
+        mctx = plain_ctx if mode == "plain" else None
 
         if mode.startswith("frames"):
             def one_pass():
@@ -629,7 +632,7 @@ def frame_stream(H, W, n_frames=240, ring=None,
         else:
             def one_pass():
                 for x, o in zip(xs, outs):
-                    hb.harris(x, out=o, pdl=pdl)
+                    hb.harris(x, out=o, pdl=pdl, ctx=mctx)
         for _ in range(3):
             one_pass()
         torch.cuda.synchronize()

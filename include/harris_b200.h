@@ -118,7 +118,10 @@ typedef struct harris_options {
     uint32_t struct_size;  /* sizeof(harris_options) */
     int32_t l2_policy;     /* HARRIS_L2_* for the input loads of every kernel path */
     int32_t band_rows;     /* output rows per tile; 0 = the library's planner */
-    int32_t reserved[5];
+    int32_t pdl;           /* 1 (default): every strip-kernel launch uses programmatic dependent
+                              launch with the wait (HARRIS_FLAG_PDL semantics: safe for any stream
+                              content; back-to-back calls overlap launch latency); 0: plain launches */
+    int32_t reserved[4];
 } harris_options;
 
 HARRIS_API void harris_options_default(harris_options* opts);

@@ -75,7 +75,7 @@ class PlanInfo(ctypes.Structure):
 class Options(ctypes.Structure):
     """harris_options (include/harris_b200.h): fill with harris_options_default first."""
     _fields_ = [("struct_size", ctypes.c_uint32), ("l2_policy", ctypes.c_int32), ("band_rows", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 5)]
+                ("pdl", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4)]
 
 
 class PeerHandle(ctypes.Structure):

@@ -60,6 +60,7 @@ struct harris_ctx {
     int occ[kNumTmaConfigs] = {0};
     int occ_win[2] = {0, 0};  // binomial-window kernels of TMA configs 0 and 6
     int occ_grp = 0;          // strip-engine kernel groupings (fusion ablation)
+    int pdl_default = 1;      // harris_options.pdl
     PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     std::atomic<int> last_path{HARRIS_PATH_NONE};  // diagnostic; calls may race on different streams
     char last_err[256] = {0};
@@ -277,8 +278,8 @@ int choose_path(const Call& c) {
     return ldg_eligible(c) ? HARRIS_PATH_LDG : HARRIS_PATH_GENERIC;
 }
 
-int pdl_mode(uint32_t flags) {
-    return (flags & HARRIS_FLAG_PDL_INDEPENDENT) ? 2 : (flags & HARRIS_FLAG_PDL) ? 1 : 0;
+int pdl_mode(const harris_ctx* ctx, uint32_t flags) {
+    return (flags & HARRIS_FLAG_PDL_INDEPENDENT) ? 2 : ((flags & HARRIS_FLAG_PDL) || ctx->pdl_default) ? 1 : 0;
 }
 
 void plan_launch(const harris_ctx* ctx, const Call& c, TileGeom& tg, int64_t& grid) {
@@ -306,7 +307,7 @@ void plan_launch(const harris_ctx* ctx, const Call& c, TileGeom& tg, int64_t& gr
     tg.l2_policy = ctx->l2_policy;
     tg.vec_store = store_mode(c.g.out, c.g.out_pitch, c.g.batch, c.g.out_image_stride);
     tg.sync_waves = ctx->sync_waves;
-    tg.pdl = pdl_mode(c.flags);
+    tg.pdl = pdl_mode(ctx, c.flags);
 }
 
 // Short tiles (a small image fills the GPU with a few rows per warp): the pipeline ramp
@@ -566,6 +567,7 @@ void harris_options_default(harris_options* o) {
     o->struct_size = uint32_t(sizeof(harris_options));
     o->l2_policy = HARRIS_L2_EVICT_LAST;
     o->band_rows = 0;
+    o->pdl = 1;
 }
 
 int harris_init(harris_ctx** out_ctx, int cuda_device) { return harris_init_ex(out_ctx, cuda_device, nullptr); }
@@ -578,9 +580,10 @@ int harris_init_ex(harris_ctx** out_ctx, int cuda_device, const harris_options* 
     if (opts) {
         if (opts->struct_size < uint32_t(offsetof(harris_options, reserved))) return HARRIS_ERR_INVALID_ARGUMENT;
         if (opts->l2_policy < HARRIS_L2_EVICT_FIRST || opts->l2_policy > HARRIS_L2_EVICT_LAST) return HARRIS_ERR_INVALID_ARGUMENT;
-        if (opts->band_rows < 0) return HARRIS_ERR_INVALID_ARGUMENT;
+        if (opts->band_rows < 0 || opts->pdl < 0 || opts->pdl > 1) return HARRIS_ERR_INVALID_ARGUMENT;
         o.l2_policy = opts->l2_policy;
         o.band_rows = opts->band_rows;
+        o.pdl = opts->pdl;
     }
     int count = 0;
     if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
@@ -608,6 +611,7 @@ int harris_init_ex(harris_ctx** out_ctx, int cuda_device, const harris_options* 
     }
     ctx->l2_policy = o.l2_policy;
     ctx->force_band_rows = o.band_rows;
+    ctx->pdl_default = o.pdl;
     // Developer knobs (kernel configuration, tiling, L2 promotion / policy): read only with
     // HARRIS_DEV=1 so a drop-in library never changes behaviour from the environment.
     const char* dev_env = std::getenv("HARRIS_DEV");
@@ -842,7 +846,7 @@ int harris_stencil3x3_sep(harris_ctx* ctx, float* out, int64_t out_pitch, int64_
         tg.l2_policy = ctx->l2_policy;
         tg.vec_store = store_mode(out, out_pitch, batch, out_image_stride);
         tg.sync_waves = ctx->sync_waves;
-        tg.pdl = pdl_mode(flags);
+        tg.pdl = pdl_mode(ctx, flags);
         if (tg.tiles > INT32_MAX) return HARRIS_ERR_SIZE;
         e = launch_sep_ldg(exact, in, in_pitch, img_stride, m + 2, n + 2, tg, grid, wv, wh, stream);
     } else if (tma) {
@@ -880,7 +884,7 @@ int harris_stencil3x3_sep(harris_ctx* ctx, float* out, int64_t out_pitch, int64_
         tg.l2_policy = ctx->l2_policy;
         tg.vec_store = out_vec;
         tg.sync_waves = ctx->sync_waves;
-        tg.pdl = pdl_mode(flags);
+        tg.pdl = pdl_mode(ctx, flags);
         if (tg.tiles > INT32_MAX) return HARRIS_ERR_SIZE;  // beyond the engine's 32-bit tile index
         CUtensorMap out_tmap;
         const bool ts = sep_config_tma_store(cfg);

@@ -28,10 +28,11 @@ KAPPA = 0.04
 class HarrisContext:
     """One ``harris_ctx`` bound to a CUDA device (``harris_init_ex`` / ``harris_destroy``).
 
-    ``l2_policy`` (``_lib.L2_EVICT_*``) and ``band_rows`` map to ``harris_options``; None keeps
-    the library default (evict_last input loads, planner-chosen tiles)."""
+    ``l2_policy`` (``_lib.L2_EVICT_*``), ``band_rows`` and ``pdl`` map to ``harris_options``; None
+    keeps the library default (evict_last input loads, planner-chosen tiles, PDL launches)."""
 
-    def __init__(self, device: int, l2_policy: Optional[int] = None, band_rows: Optional[int] = None):
+    def __init__(self, device: int, l2_policy: Optional[int] = None, band_rows: Optional[int] = None,
+                 pdl: Optional[bool] = None):
         self.device = int(device)
         h = ctypes.c_void_p()
         opts = _lib.Options()
@@ -40,6 +41,8 @@ class HarrisContext:
             opts.l2_policy = int(l2_policy)
         if band_rows is not None:
             opts.band_rows = int(band_rows)
+        if pdl is not None:
+            opts.pdl = 1 if pdl else 0
         check(lib().harris_init_ex(ctypes.byref(h), self.device, ctypes.byref(opts)),
               f"harris_init_ex(cuda:{self.device})")
         self._h = h

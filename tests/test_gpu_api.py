@@ -38,7 +38,8 @@ def test_init_ex_rejects_bad_options():
     o = _lib.Options()
     L.harris_options_default(ctypes.byref(o))
     assert o.struct_size == ctypes.sizeof(_lib.Options) and o.l2_policy == _lib.L2_EVICT_LAST and o.band_rows == 0
-    for field, val in [("l2_policy", 3), ("l2_policy", -1), ("band_rows", -5), ("struct_size", 4)]:
+    assert o.pdl == 1
+    for field, val in [("l2_policy", 3), ("l2_policy", -1), ("band_rows", -5), ("struct_size", 4), ("pdl", 2)]:
         bad = _lib.Options()
         L.harris_options_default(ctypes.byref(bad))
         setattr(bad, field, val)
@@ -131,6 +132,7 @@ def test_host_pipeline_error_returns_after_drain(cuda_ctx):
 
 @pytest.mark.parametrize("pdl", [True, "independent"])
 def test_pdl_launches_bit_identical_and_stream_ordered(cuda_ctx, pdl):
+    plain_ctx = hb.HarrisContext(0, pdl=False)  # harris_options.pdl = 0: plain launches
     """PDL launches (HARRIS_FLAG_PDL / _PDL_INDEPENDENT) give the same bits as plain launches on
     every kernel path, and stream order holds for the work around them: a producer kernel
     (synth_) right before a PDL-waiting launch, and a consumer (clone) right after a chain."""
@@ -138,7 +140,7 @@ def test_pdl_launches_bit_identical_and_stream_ordered(cuda_ctx, pdl):
     for H, W in shapes:
         x = torch.empty((3, H, W), device="cuda")
         ref_x = torch.from_numpy(synth.synth_numpy(3, H, W, seed=H * W)).cuda()
-        plain = hb.harris(ref_x)
+        plain = hb.harris(ref_x, ctx=plain_ctx)
         for rep in range(3):
             x.zero_()
             torch.cuda.synchronize()
