@@ -455,6 +455,8 @@ def run_gpu(a, world, rank, local) -> dict | None:
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_kind": peak_kind,
                 "algorithmic_bytes_per_launch": sh.algorithmic_bytes(),
+                # the north star's own yardstick: 12 B read + 4 B written per pixel against ~8 TB/s per GPU
+                "frac_of_nominal_8tbs": achieved / 8000.0,
                 "per": "one fused-kernel launch per rank per step (max over ranks)"}
     plan = ctx.plan(sh.rows, sh.m, sh.nb)
 

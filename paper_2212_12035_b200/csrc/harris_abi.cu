@@ -765,6 +765,12 @@ int harris_run_frames(harris_ctx* ctx, float* const* outs, int64_t out_pitch, in
                       const float* const* rgbs, int64_t in_pitch, int64_t in_chan_stride, int64_t frames,
                       float kappa, uint32_t flags, void* stream) {
     if (!ctx || !outs || !rgbs || frames < 1) return HARRIS_ERR_INVALID_ARGUMENT;
+    // frames 1.. run as independent of their predecessors: their outputs must be distinct
+    // (checked for rings of up to 256 frames; larger rings are the caller's contract)
+    if (frames <= 256)
+        for (int64_t a = 0; a < frames; ++a)
+            for (int64_t b = a + 1; b < frames; ++b)
+                if (outs[a] == outs[b]) return HARRIS_ERR_INVALID_ARGUMENT;
     const uint32_t base = flags & ~(uint32_t(HARRIS_FLAG_PDL) | uint32_t(HARRIS_FLAG_PDL_INDEPENDENT));
     for (int64_t k = 0; k < frames; ++k) {
         const uint32_t pdl = k > 0 || (flags & HARRIS_FLAG_PDL_INDEPENDENT) ? HARRIS_FLAG_PDL_INDEPENDENT

@@ -189,3 +189,9 @@ def test_harris_frames_ring(cuda_ctx):
         assert torch.equal(outs[i], hb.harris(x)), i
     with pytest.raises(ValueError):
         hb.harris_frames(xs, [outs[0]] * K)  # outputs must be distinct
+    vp = ctypes.c_void_p
+    L = _lib.lib()
+    same = (vp * 2)(outs[0].data_ptr(), outs[0].data_ptr())
+    ins = (vp * 2)(xs[0].data_ptr(), xs[1].data_ptr())
+    assert L.harris_run_frames(cuda_ctx.handle, same, W - 4, H - 4, W - 4, ins, W, H * W, 2, 0.04, 0,
+                               None) == _lib.HARRIS_ERR_INVALID_ARGUMENT  # the C-ABI checks it too
