@@ -65,6 +65,17 @@ def test_fuzz_f32_layouts(cuda_ctx, seed):
     for b in range(B):
         ok, mt = synth.within_tolerance(fast[b].cpu().numpy(), cref.harris_f64(rgb[b]))
         assert ok, (seed, b, mt)
+    # every third layout also through the binomial-window variant and a PDL launch (round 2):
+    # EXACT bit-exact with the window oracle on whichever kernel the layout selects
+    if seed % 3 == 0:
+        obuf.fill_(-3.0)
+        hb.harris(x, out=out, exact=True, window="binomial", pdl=True)
+        torch.cuda.synchronize()
+        got = out.cpu().numpy()
+        for b in range(B):
+            assert np.array_equal(got[b], cref.harris_f32(rgb[b], window="binomial")), (seed, b, "window")
+        if opad:
+            assert torch.all(obuf[: B * n * (m + opad)].view(B, n, m + opad)[:, :, m:] == -3.0)
 
 
 @pytest.mark.parametrize("seed", range(N_CASES // 2))
