@@ -20,6 +20,8 @@
 #include <cstring>
 #include <new>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost a pointer check unless a tool attaches
+
 #include "../../include/harris_b200.h"
 #include "harris_common.cuh"
 #include "harris_internal.h"
@@ -97,6 +99,15 @@ struct harris_ctx {
 };
 
 namespace {
+
+// NVTX range per C-ABI call (SURVEY.md §5 tracing): library work shows up by name in nsys /
+// ncu timelines without the caller instrumenting anything
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Makes ctx->device current for the duration of a call, restores the caller's.
 struct DeviceGuard {
@@ -450,6 +461,7 @@ void cache_insert(harris_ctx* ctx, const Call& c, harris_ctx::LaunchEntry ent) {
 
 int run(harris_ctx* ctx, const Call& c, cudaStream_t stream) {
     if (!ctx) return HARRIS_ERR_INVALID_ARGUMENT;
+    NvtxRange nvtx(c.fmt == kU8Interleaved ? "harris_run_u8" : "harris_run");
     int rc = validate(c);
     if (rc) return rc;
     const bool exact = (c.flags & HARRIS_FLAG_EXACT_ORDER) != 0;
@@ -772,6 +784,7 @@ int harris_run_frames(harris_ctx* ctx, float* const* outs, int64_t out_pitch, in
             for (int64_t b = a + 1; b < frames; ++b)
                 if (outs[a] == outs[b]) return HARRIS_ERR_INVALID_ARGUMENT;
     const uint32_t base = flags & ~(uint32_t(HARRIS_FLAG_PDL) | uint32_t(HARRIS_FLAG_PDL_INDEPENDENT));
+    NvtxRange nvtx("harris_run_frames");
     for (int64_t k = 0; k < frames; ++k) {
         const uint32_t pdl = k > 0 || (flags & HARRIS_FLAG_PDL_INDEPENDENT) ? HARRIS_FLAG_PDL_INDEPENDENT
                                                                             : HARRIS_FLAG_PDL;
@@ -823,6 +836,7 @@ int harris_stencil3x3_sep(harris_ctx* ctx, float* out, int64_t out_pitch, int64_
     if (!ctx || !out || !in || !wv || !wh) return HARRIS_ERR_INVALID_ARGUMENT;
     if (n < 1 || m < 1) return HARRIS_ERR_SIZE;
     if (n + 2 > INT32_MAX || m + 2 > INT32_MAX) return HARRIS_ERR_SIZE;
+    NvtxRange nvtx("harris_stencil3x3_sep");
     if (batch < 1 || in_pitch < m + 2 || out_pitch < m) return HARRIS_ERR_INVALID_ARGUMENT;
     if (batch > 1 && (in_image_stride < (n + 2) * in_pitch || out_image_stride < n * out_pitch))
         return HARRIS_ERR_INVALID_ARGUMENT;
@@ -1061,6 +1075,7 @@ static int run_host_impl(harris_ctx* ctx, int fmt, float* out_host, int64_t out_
     if (!ctx || !out_host || !in_host) return HARRIS_ERR_INVALID_ARGUMENT;
     if (n < 1 || m < 1) return HARRIS_ERR_SIZE;
     if (batch < 1 || out_pitch < m) return HARRIS_ERR_INVALID_ARGUMENT;
+    NvtxRange nvtx(fmt == kU8Interleaved ? "harris_run_host_u8" : "harris_run_host");
     DeviceGuard guard(ctx->device);
     if (!guard.ok) return cuda_fail(ctx, cudaGetLastError(), "cudaSetDevice");
     const bool u8 = fmt == kU8Interleaved;
