@@ -605,25 +605,37 @@ def time_launches(fn, iters: int, flush=None) -> list[float]:
 # ---------------------------------------------------------- frame streams
 GRAPH_PASSES = 8
 def frame_stream(H, W, n_frames=240, ring=None,
-                  modes=("plain", "pdl", "independent", "graph", "frames", "frames_graph")) -> dict:
+                  modes=("plain", "pdl", "independent", "graph", "frames", "frames_graph"), u8: bool = False) -> dict:
     """Back-to-back UNBATCHED single frames over a ring of distinct frames (> L2, so every frame
     streams from HBM).  Modes: plain launches; pdl (HARRIS_FLAG_PDL); independent
     (HARRIS_FLAG_PDL_INDEPENDENT); "plain" uses a ctx with harris_options.pdl = 0 (the library
     default is PDL with the wait); graph (the independent ring captured in a CUDA graph and
     replayed); frames (harris_run_frames: the ring in one C call, one launch per frame);
-    frames_graph.  Per mode: us per frame = CUDA-event time of N frames / N."""
+    frames_graph.  Per mode: us per frame = CUDA-event time of N frames / N.  u8=True: interleaved
+    8-bit RGB frames (the thesis's PNG inputs) through harris_u8 (no frames
+    modes: harris_run_frames is planar f32)."""
     dev = torch.device("cuda", torch.cuda.current_device())
     import paper_2212_12035_b200 as hb
-    frame_bytes = 12 * H * W
+    frame_bytes = (3 if u8 else 12) * H * W
     ring = ring or max(4, -(-(384 << 20) // frame_bytes))  # >= 384 MB of inputs: 3x the L2
-    xs = [torch.empty((3, H, W), device=dev) for _ in range(ring)]
-    for i, x in enumerate(xs):
-        hb.synth_(x, seed=12035 + i)
+    if u8:
+        g = torch.Generator(device=dev)
+        g.manual_seed(SEED)
+        xs = [torch.randint(0, 256, (H, W, 3), dtype=torch.uint8, device=dev, generator=g) for _ in range(ring)]
+        modes = tuple(m for m in modes if not m.startswith("frames"))
+        run1 = hb.harris_u8
+        nbytes = 3 * H * W + 4 * (H - 4) * (W - 4)
+    else:
+        xs = [torch.empty((3, H, W), device=dev) for _ in range(ring)]
+        for i, x in enumerate(xs):
+            hb.synth_(x, seed=12035 + i)
+        run1 = hb.harris
+        nbytes = hb.algorithmic_bytes(H - 4, W - 4)
     outs = [torch.empty((H - 4, W - 4), device=dev) for _ in range(ring)]
     peak, _ = measured_peak()
-    nbytes = hb.algorithmic_bytes(H - 4, W - 4)
-    res = {"frame": f"{W}x{H} RGB f32", "ring_frames": ring, "ring_input_mb": ring * frame_bytes / 2**20}
-    ref = [hb.harris(x) for x in xs]
+    res = {"frame": f"{W}x{H} RGB {'u8 interleaved' if u8 else 'f32'}", "ring_frames": ring,
+           "ring_input_mb": ring * frame_bytes / 2**20}
+    ref = [run1(x) for x in xs]
     plain_ctx = hb.HarrisContext(torch.cuda.current_device(), pdl=False)  # plain launches (options.pdl = 0)
     for mode in modes:
         pdl = {"plain": False, "pdl": True, "independent": "independent", "graph": "independent"}.get(mode)
@@ -635,7 +647,7 @@ def frame_stream(H, W, n_frames=240, ring=None,
         else:
             def one_pass():
                 for x, o in zip(xs, outs):
-                    hb.harris(x, out=o, pdl=pdl, ctx=mctx)
+                    run1(x, out=o, pdl=pdl, ctx=mctx)
         for _ in range(3):
             one_pass()
         torch.cuda.synchronize()
@@ -752,6 +764,8 @@ def run_extra(a, ctx, dev) -> dict:
     # unbatched launches over a ring of distinct frames (> L2), plain / PDL / independent-PDL /
     # CUDA-graph / harris_run_frames (tools/frame_stream.py)
     res["frame_stream"] = {f"{W}x{H}": frame_stream(H, W, 180) for H, W in ((1536, 2560), (2560, 1536), (2832, 4256))}
+    # the thesis's evaluation images are 8-bit PNGs: the same stream of u8 interleaved frames
+    res["frame_stream_u8"] = {f"{W}x{H}": frame_stream(H, W, 180, u8=True) for H, W in ((1536, 2560), (2832, 4256))}
     torch.cuda.empty_cache()
 
     # other input formats / stencils on the same engine, batch of 1024 x 1080x1920 (inputs >> L2)

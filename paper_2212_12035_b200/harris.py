@@ -329,10 +329,9 @@ def harris_u8(rgb8, kappa: float = KAPPA, *, out: Optional[torch.Tensor] = None,
     out_pitch = out.stride(-2)
     out_image = out.stride(0) if batched else n * out_pitch
     dev = rgb8.device.index if rgb8.device.index is not None else torch.cuda.current_device()
-    st = stream if stream is not None else torch.cuda.current_stream(dev)
     ctx = ctx or context(dev)
     rc = lib().harris_run_u8(ctx.handle, out.data_ptr(), out_pitch, out_image, n, m, rgb8.data_ptr(), in_pitch,
-                             in_image, B, kappa, flags, st.cuda_stream)
+                             in_image, B, kappa, flags, _stream_handle(dev, stream))
     check(rc, "harris_run_u8", ctx.handle)
     return out
 
@@ -365,12 +364,12 @@ def stencil3x3_sep(img: torch.Tensor, wv=BINOMIAL, wh=BINOMIAL, *, out: Optional
     fwv = (ctypes.c_float * 3)(*[float(v) for v in wv])
     fwh = (ctypes.c_float * 3)(*[float(v) for v in wh])
     dev = img.device.index if img.device.index is not None else torch.cuda.current_device()
-    st = stream if stream is not None else torch.cuda.current_stream(dev)
     ctx = ctx or context(dev)
     rc = lib().harris_stencil3x3_sep(ctx.handle, out.data_ptr(), out.stride(-2),
                                      out.stride(0) if batched else n * out.stride(-2), n, m, img.data_ptr(),
                                      img.stride(-2), img.stride(0) if batched else H * img.stride(-2), B,
-                                     fwv, fwh, _flags(exact, force_generic, force_tma, pdl), st.cuda_stream)
+                                     fwv, fwh, _flags(exact, force_generic, force_tma, pdl),
+                                     _stream_handle(dev, stream))
     check(rc, "harris_stencil3x3_sep", ctx.handle)
     return out
 
