@@ -612,8 +612,8 @@ def frame_stream(H, W, n_frames=240, ring=None,
     default is PDL with the wait); graph (the independent ring captured in a CUDA graph and
     replayed); frames (harris_run_frames: the ring in one C call, one launch per frame);
     frames_graph.  Per mode: us per frame = CUDA-event time of N frames / N.  u8=True: interleaved
-    8-bit RGB frames (the thesis's PNG inputs) through harris_u8 (no frames
-    modes: harris_run_frames is planar f32)."""
+    8-bit RGB frames (the thesis's PNG inputs) through harris_u8 /
+    harris_run_frames_u8."""
     dev = torch.device("cuda", torch.cuda.current_device())
     import paper_2212_12035_b200 as hb
     frame_bytes = (3 if u8 else 12) * H * W
@@ -622,7 +622,6 @@ def frame_stream(H, W, n_frames=240, ring=None,
         g = torch.Generator(device=dev)
         g.manual_seed(SEED)
         xs = [torch.randint(0, 256, (H, W, 3), dtype=torch.uint8, device=dev, generator=g) for _ in range(ring)]
-        modes = tuple(m for m in modes if not m.startswith("frames"))
         run1 = hb.harris_u8
         nbytes = 3 * H * W + 4 * (H - 4) * (W - 4)
     else:

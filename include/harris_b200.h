@@ -165,6 +165,11 @@ HARRIS_API int harris_run_strided(harris_ctx* ctx, float* out, int64_t out_pitch
 HARRIS_API int harris_run_frames(harris_ctx* ctx, float* const* outs, int64_t out_pitch, int64_t n, int64_t m,
                                  const float* const* rgbs, int64_t in_pitch, int64_t in_chan_stride,
                                  int64_t frames, float kappa, uint32_t flags, void* cuda_stream);
+/* the same for interleaved 8-bit RGB frames (HWC, value/255; e.g. the thesis's PNG inputs):
+ * frame k at rgb8s[k] with row pitch in_pitch_bytes */
+HARRIS_API int harris_run_frames_u8(harris_ctx* ctx, float* const* outs, int64_t out_pitch, int64_t n, int64_t m,
+                                    const uint8_t* const* rgb8s, int64_t in_pitch_bytes, int64_t frames, float kappa,
+                                    uint32_t flags, void* cuda_stream);
 
 /* HOST buffers (pinned for full speed; pageable works).  Row bands (batch == 1) or
  * image groups are pipelined H2D -> kernel -> D2H over three streams; returns when

@@ -37,7 +37,7 @@ PATH_NONE, PATH_TMA, PATH_GENERIC, PATH_LDG, PATH_PAIR, PATH_QUAD = 0, 1, 2, 3, 
 # every symbol include/harris_b200.h declares (checked by tests/test_abi.py)
 EXPORTED_SYMBOLS = (
     "harris_init", "harris_init_ex", "harris_options_default", "harris_destroy", "harris_run", "harris_run_batched", "harris_run_strided",
-    "harris_run_host", "harris_run_frames", "harris_synth_fill", "harris_plan", "harris_last_path", "harris_device",
+    "harris_run_host", "harris_run_frames", "harris_run_frames_u8", "harris_synth_fill", "harris_plan", "harris_last_path", "harris_device",
     "harris_num_sms", "harris_strerror", "harris_last_cuda_error", "harris_abi_version",
     "harris_grouping_scratch_bytes", "harris_grouping_launches", "harris_run_grouping",
     "harris_run_u8", "harris_run_host_u8", "harris_stencil3x3_sep",
@@ -126,6 +126,8 @@ def lib() -> ctypes.CDLL:
         "harris_run_host": ([vp, vp, i64, i64, i64, vp, i64, f32, u32], i32),
         "harris_run_frames": ([vp, ctypes.POINTER(vp), i64, i64, i64, ctypes.POINTER(vp), i64, i64, i64, f32, u32, vp],
                               i32),
+        "harris_run_frames_u8": ([vp, ctypes.POINTER(vp), i64, i64, i64, ctypes.POINTER(vp), i64, i64, f32, u32, vp],
+                                 i32),
         "harris_synth_fill": ([vp, i64, i64, i64, i64, i64, i64, i64, i64, u64, i32, vp], i32),
         "harris_plan": ([vp, i64, i64, i64, vp, i64, i64, i64, vp, i64, i64, u32, ctypes.POINTER(PlanInfo)], i32),
         "harris_last_path": ([vp], i32),

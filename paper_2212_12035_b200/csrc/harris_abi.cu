@@ -63,6 +63,8 @@ struct harris_ctx {
     int occ_win[2] = {0, 0};  // binomial-window kernels of TMA configs 0 and 6
     int occ_grp = 0;          // strip-engine kernel groupings (fusion ablation)
     int pdl_default = 1;      // harris_options.pdl
+    int stream_share = 4;     // frames of an independent PDL stream are planned for 1/stream_share of the GPU
+                              // (profiles/stream_share_r02.txt: 2-8 within a few %, 16 starves eager launches)
     PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     std::atomic<int> last_path{HARRIS_PATH_NONE};  // diagnostic; calls may race on different streams
     char last_err[256] = {0};
@@ -293,6 +295,12 @@ int pdl_mode(const harris_ctx* ctx, uint32_t flags) {
     return (flags & HARRIS_FLAG_PDL_INDEPENDENT) ? 2 : ((flags & HARRIS_FLAG_PDL) || ctx->pdl_default) ? 1 : 0;
 }
 
+constexpr int64_t kStreamFrameMaxPixels = int64_t(16) << 20;  // frames up to 16 MP (4256x2832 = 12 MP)
+// internal flag bit (never in the public header): plan an independent frame for the whole GPU —
+// harris_run_frames uses it for rings too short to keep stream_share frames in flight, where
+// the call boundary (frame 0 waits) would leave the GPU under-filled
+constexpr uint32_t kFlagFullGpuPlan = 0x80000000u;
+
 void plan_launch(const harris_ctx* ctx, const Call& c, TileGeom& tg, int64_t& grid) {
     const bool u8 = c.fmt == kU8Interleaved;
     const int fcfg = c.cfg >= 0 ? c.cfg : ctx->tma_cfg;
@@ -308,8 +316,19 @@ void plan_launch(const harris_ctx* ctx, const Call& c, TileGeom& tg, int64_t& gr
                                 : c.g.window ? ctx->occ_win[fcfg == 6 ? 1 : 0]
                                         : ctx->occ[fcfg]);
     const int64_t resident_ctas = int64_t(ctx->num_sms) * occ;
-    plan_tiles(c.g.n, c.g.m, c.g.batch, resident_ctas * cfg.warps, cfg.rows, ctx->force_band_rows, tg, 4,
-               cfg.groups, cfg.strip_cols, /*cap_rows=*/!u8, /*row_align=*/c.pair ? c.group : 1);
+    // A single frame of a PDL-independent stream (harris_run_frames, HARRIS_FLAG_PDL_INDEPENDENT)
+    // shares the GPU with its neighbours: plan it for 1/kStreamShare of the warps, i.e. fewer,
+    // taller tiles (less halo re-read and per-tile overhead) while the next frames fill the
+    // other SMs.  Isolated launches keep the whole-GPU plan.
+    int64_t plan_warps = resident_ctas * cfg.warps;
+    if ((c.flags & HARRIS_FLAG_PDL_INDEPENDENT) && !(c.flags & kFlagFullGpuPlan) && c.g.batch == 1 &&
+        (c.g.n + 4) * (c.g.m + 4) <= kStreamFrameMaxPixels)
+        plan_warps = std::max<int64_t>(cfg.warps, plan_warps / ctx->stream_share);
+    // u8 ops sum the box rows in pairs (kPairRows) by the row's parity within the stage: even
+    // tile heights keep every tile start on an even absolute row, so the pairing — and the FAST
+    // bits — do not depend on the tile plan (f32 ops do not pair rows)
+    plan_tiles(c.g.n, c.g.m, c.g.batch, plan_warps, cfg.rows, ctx->force_band_rows, tg, 4,
+               cfg.groups, cfg.strip_cols, /*cap_rows=*/!u8, /*row_align=*/c.pair ? c.group : u8 ? 2 : 1);
     grid = std::min<int64_t>((tg.tiles + cfg.warps - 1) / cfg.warps, resident_ctas);
     tg.out = c.g.out;
     tg.out_pitch = c.g.out_pitch;
@@ -666,6 +685,8 @@ int harris_init_ex(harris_ctx** out_ctx, int cuda_device, const harris_options* 
         }
         env = std::getenv("HARRIS_BAND_ROWS");
         if (env) ctx->force_band_rows = std::atoll(env);
+        env = std::getenv("HARRIS_STREAM_SHARE");
+        if (env && std::atoi(env) >= 1) ctx->stream_share = std::atoi(env);
         env = std::getenv("HARRIS_L2_POLICY");
         if (env) {
             int v = std::atoi(env);
@@ -773,28 +794,48 @@ int harris_run_strided(harris_ctx* ctx, float* out, int64_t out_pitch, int64_t o
                static_cast<cudaStream_t>(stream));
 }
 
-int harris_run_frames(harris_ctx* ctx, float* const* outs, int64_t out_pitch, int64_t n, int64_t m,
-                      const float* const* rgbs, int64_t in_pitch, int64_t in_chan_stride, int64_t frames,
-                      float kappa, uint32_t flags, void* stream) {
-    if (!ctx || !outs || !rgbs || frames < 1) return HARRIS_ERR_INVALID_ARGUMENT;
+// shared body of harris_run_frames / harris_run_frames_u8
+static int run_frames_impl(harris_ctx* ctx, int fmt, float* const* outs, int64_t out_pitch, int64_t n, int64_t m,
+                           const void* const* ins, int64_t in_pitch, int64_t in_chan_stride, int64_t frames,
+                           float kappa, uint32_t flags, void* stream) {
+    if (!ctx || !outs || !ins || frames < 1) return HARRIS_ERR_INVALID_ARGUMENT;
     // frames 1.. run as independent of their predecessors: their outputs must be distinct
     // (checked for rings of up to 256 frames; larger rings are the caller's contract)
     if (frames <= 256)
         for (int64_t a = 0; a < frames; ++a)
             for (int64_t b = a + 1; b < frames; ++b)
                 if (outs[a] == outs[b]) return HARRIS_ERR_INVALID_ARGUMENT;
-    const uint32_t base = flags & ~(uint32_t(HARRIS_FLAG_PDL) | uint32_t(HARRIS_FLAG_PDL_INDEPENDENT));
-    NvtxRange nvtx("harris_run_frames");
+    uint32_t base = flags & ~(uint32_t(HARRIS_FLAG_PDL) | uint32_t(HARRIS_FLAG_PDL_INDEPENDENT) | kFlagFullGpuPlan);
+    if (frames < 2 * int64_t(ctx->stream_share)) base |= kFlagFullGpuPlan;
+    NvtxRange nvtx(fmt == kU8Interleaved ? "harris_run_frames_u8" : "harris_run_frames");
     for (int64_t k = 0; k < frames; ++k) {
         const uint32_t pdl = k > 0 || (flags & HARRIS_FLAG_PDL_INDEPENDENT) ? HARRIS_FLAG_PDL_INDEPENDENT
                                                                             : HARRIS_FLAG_PDL;
-        const int rc = run(ctx,
-                           make_call(outs[k], out_pitch, n * out_pitch, n, m, rgbs[k], in_pitch, in_chan_stride,
-                                     3 * in_chan_stride, 1, kappa, base | pdl),
-                           static_cast<cudaStream_t>(stream));
+        if (!ins[k]) return HARRIS_ERR_INVALID_ARGUMENT;
+        Call c = fmt == kU8Interleaved
+                     ? make_call(outs[k], out_pitch, n * out_pitch, n, m, static_cast<const float*>(ins[k]), in_pitch,
+                                 0, (n + 4) * in_pitch, 1, kappa, base | pdl)
+                     : make_call(outs[k], out_pitch, n * out_pitch, n, m, static_cast<const float*>(ins[k]), in_pitch,
+                                 in_chan_stride, 3 * in_chan_stride, 1, kappa, base | pdl);
+        c.fmt = fmt;
+        const int rc = run(ctx, c, static_cast<cudaStream_t>(stream));
         if (rc) return rc;
     }
     return HARRIS_OK;
+}
+
+int harris_run_frames(harris_ctx* ctx, float* const* outs, int64_t out_pitch, int64_t n, int64_t m,
+                      const float* const* rgbs, int64_t in_pitch, int64_t in_chan_stride, int64_t frames,
+                      float kappa, uint32_t flags, void* stream) {
+    return run_frames_impl(ctx, kF32Planar, outs, out_pitch, n, m, reinterpret_cast<const void* const*>(rgbs),
+                           in_pitch, in_chan_stride, frames, kappa, flags, stream);
+}
+
+int harris_run_frames_u8(harris_ctx* ctx, float* const* outs, int64_t out_pitch, int64_t n, int64_t m,
+                         const uint8_t* const* rgb8s, int64_t in_pitch_bytes, int64_t frames, float kappa,
+                         uint32_t flags, void* stream) {
+    return run_frames_impl(ctx, kU8Interleaved, outs, out_pitch, n, m, reinterpret_cast<const void* const*>(rgb8s),
+                           in_pitch_bytes, 0, frames, kappa, flags, stream);
 }
 
 int harris_run_notify(harris_ctx* ctx, float* out, int64_t out_pitch, int64_t out_image_stride, int64_t n,

@@ -243,20 +243,30 @@ def harris(rgb, kappa: float = KAPPA, *, out: Optional[torch.Tensor] = None, exa
 
 def harris_frames(frames, outs=None, kappa: float = KAPPA, *, exact: bool = False, independent: bool = False,
                   stream: Optional[torch.cuda.Stream] = None, ctx: Optional[HarrisContext] = None):
-    """A stream of independent single frames through ``harris_run_frames``: one launch per
-    frame, back to back, chained with programmatic dependent launch (frame 0 waits for earlier
-    stream work unless ``independent``).  ``frames``: sequence of (3, H, W) float32 CUDA tensors of
-    one shape and layout (unit column stride, same row pitch / channel stride); ``outs``: matching
-    (H-4, W-4) outputs (allocated when None), all distinct.  Returns ``outs``."""
+    """A stream of independent single frames through ``harris_run_frames`` (planar f32) or
+    ``harris_run_frames_u8`` (interleaved uint8): one launch per frame, back to back, chained
+    with programmatic dependent launch (frame 0 waits for earlier stream work unless
+    ``independent``).  ``frames``: (3, H, W) float32 or (H, W, 3) uint8 CUDA tensors of one shape
+    and layout (same strides); ``outs``: matching (H-4, W-4) outputs (allocated when None), all
+    distinct.  Returns ``outs``."""
     frames = list(frames)
     if not frames:
         raise ValueError("no frames")
-    B, H, W = _check_rgb(frames[0])
     f0 = frames[0]
-    if f0.dim() != 3 or not f0.is_cuda or f0.stride(-1) != 1:
-        raise ValueError("frames must be (3, H, W) CUDA tensors with unit column stride")
+    u8 = f0.dtype == torch.uint8
+    if u8:
+        if f0.dim() != 3 or f0.shape[-1] != 3 or not f0.is_cuda or f0.stride(-1) != 1 or f0.stride(-2) != 3:
+            raise ValueError("u8 frames must be (H, W, 3) interleaved CUDA tensors")
+        H, W = f0.shape[0], f0.shape[1]
+        if H < 5 or W < 5:
+            raise ValueError(f"harris needs an input of at least 5x5, got {H}x{W}")
+    else:
+        _check_rgb(f0)
+        if f0.dim() != 3 or not f0.is_cuda or f0.stride(-1) != 1:
+            raise ValueError("frames must be (3, H, W) CUDA tensors with unit column stride")
+        H, W = f0.shape[1], f0.shape[2]
     for f in frames:
-        if f.shape != f0.shape or f.stride() != f0.stride() or f.dtype != torch.float32 or f.device != f0.device:
+        if f.shape != f0.shape or f.stride() != f0.stride() or f.dtype != f0.dtype or f.device != f0.device:
             raise ValueError("all frames must share shape, strides, dtype and device")
     n, m = H - 4, W - 4
     if outs is None:
@@ -277,9 +287,14 @@ def harris_frames(frames, outs=None, kappa: float = KAPPA, *, exact: bool = Fals
     iptrs = (vp * len(frames))(*[f.data_ptr() for f in frames])
     flags = _flags(exact, False, False, "independent" if independent else False)
     ctx = ctx or context(dev)
-    rc = lib().harris_run_frames(ctx.handle, optrs, o0.stride(0), n, m, iptrs, f0.stride(1), f0.stride(0), len(frames),
-                                 kappa, flags, _stream_handle(dev, stream))
-    check(rc, "harris_run_frames", ctx.handle)
+    if u8:
+        rc = lib().harris_run_frames_u8(ctx.handle, optrs, o0.stride(0), n, m, iptrs, f0.stride(0), len(frames),
+                                        kappa, flags, _stream_handle(dev, stream))
+        check(rc, "harris_run_frames_u8", ctx.handle)
+    else:
+        rc = lib().harris_run_frames(ctx.handle, optrs, o0.stride(0), n, m, iptrs, f0.stride(1), f0.stride(0),
+                                     len(frames), kappa, flags, _stream_handle(dev, stream))
+        check(rc, "harris_run_frames", ctx.handle)
     return outs
 
 

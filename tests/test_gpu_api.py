@@ -195,3 +195,32 @@ def test_harris_frames_ring(cuda_ctx):
     ins = (vp * 2)(xs[0].data_ptr(), xs[1].data_ptr())
     assert L.harris_run_frames(cuda_ctx.handle, same, W - 4, H - 4, W - 4, ins, W, H * W, 2, 0.04, 0,
                                None) == _lib.HARRIS_ERR_INVALID_ARGUMENT  # the C-ABI checks it too
+
+
+def test_harris_frames_u8_ring(cuda_ctx):
+    """harris_run_frames_u8: a ring of interleaved u8 frames, one PDL-chained launch each,
+    equal to one harris_u8 call per frame (EXACT and FAST), also with odd widths (bulk rows)."""
+    g = torch.Generator(device="cuda")
+    g.manual_seed(3)
+    for H, W in [(300, 516), (131, 517)]:
+        xs = [torch.randint(0, 256, (H, W, 3), dtype=torch.uint8, device="cuda", generator=g) for _ in range(5)]
+        for exact in (False, True):
+            outs = hb.harris_frames(xs, exact=exact)
+            torch.cuda.synchronize()
+            for i, x in enumerate(xs):
+                assert torch.equal(outs[i], hb.harris_u8(x, exact=exact)), (H, W, exact, i)
+
+
+@pytest.mark.parametrize("band_rows", [0, 7, 30, 136])
+def test_u8_fast_bits_do_not_depend_on_the_tile_plan(cuda_ctx, band_rows):
+    """The u8 ops sum box rows in pairs; tiles start on even rows, so every tile plan (forced
+    heights, the frame-stream plan of PDL-independent frames) gives the same FAST bits."""
+    g = torch.Generator(device="cuda")
+    g.manual_seed(band_rows)
+    ctx = hb.HarrisContext(0, band_rows=band_rows or None)
+    for H, W in [(300, 516), (301, 1918), (1080, 1080)]:
+        x = torch.randint(0, 256, (2, H, W, 3), dtype=torch.uint8, device="cuda", generator=g)
+        ref = hb.harris_u8(x)
+        assert torch.equal(hb.harris_u8(x, ctx=ctx), ref), (band_rows, H, W)
+        for b in range(2):
+            assert torch.equal(hb.harris_u8(x[b], ctx=ctx, pdl="independent"), ref[b]), (band_rows, H, W, b)
