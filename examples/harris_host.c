@@ -24,6 +24,8 @@ void oracle_synth_fill(float* dst, int64_t planes, int64_t rows, int64_t W, int6
                        int dist);
 int oracle_harris_f32(float* out, int64_t out_pitch, int64_t n, int64_t m, const float* rgb, int64_t in_pitch,
                       int64_t chan_stride, float kappa, int nthreads);
+int oracle_harris_f32_window(float* out, int64_t out_pitch, int64_t n, int64_t m, const float* rgb,
+                             int64_t in_pitch, int64_t chan_stride, float kappa, int nthreads, int window);
 
 int main(int argc, char** argv) {
     const int64_t H = argc > 2 ? atoll(argv[1]) : 1536, W = argc > 2 ? atoll(argv[2]) : 2560;
@@ -35,8 +37,13 @@ int main(int argc, char** argv) {
     oracle_synth_fill(rgb, 3, H, W, W, H * W, H, 0, 0, 12035, 0);
     if (oracle_harris_f32(ref, m, n, m, rgb, W, H * W, 0.04f, 0)) return 3;
 
+    /* options instead of environment variables: evict_normal input loads, plain launches */
+    harris_options opts;
+    harris_options_default(&opts);
+    opts.l2_policy = HARRIS_L2_EVICT_NORMAL;
+    opts.pdl = 0;
     harris_ctx* ctx = NULL;
-    int rc = harris_init(&ctx, 0);
+    int rc = harris_init_ex(&ctx, 0, &opts);
     if (rc) {
         fprintf(stderr, "harris_init: %s\n", harris_strerror(rc));
         return 4;
@@ -58,8 +65,16 @@ int main(int argc, char** argv) {
         if (d > maxd) maxd = d;
         if (r > maxr) maxr = r;
     }
-    printf("harris_host %lldx%lld: exact bit-identical, default norm-Linf %.3g, path %d\n", (long long)H,
-           (long long)W, maxd / (maxr > 0 ? maxr : 1), harris_last_path(ctx));
+    /* the binomial-window variant (HARRIS_FLAG_BINOMIAL_WINDOW), exact order vs its oracle */
+    if (oracle_harris_f32_window(ref, m, n, m, rgb, W, H * W, 0.04f, 0, 1)) return 9;
+    rc = harris_run_host(ctx, out, m, n, m, rgb, 1, 0.04f, HARRIS_FLAG_EXACT_ORDER | HARRIS_FLAG_BINOMIAL_WINDOW);
+    if (rc) return 10;
+    if (memcmp(out, ref, sizeof(float) * n * m) != 0) {
+        fprintf(stderr, "binomial window: exact order differs from the oracle\n");
+        return 11;
+    }
+    printf("harris_host %lldx%lld: exact bit-identical, default norm-Linf %.3g, binomial window exact bit-identical, "
+           "path %d\n", (long long)H, (long long)W, maxd / (maxr > 0 ? maxr : 1), harris_last_path(ctx));
     harris_destroy(ctx);
     free(rgb);
     free(out);
